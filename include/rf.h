@@ -1,0 +1,160 @@
+/*
+ * rf.h — C ABI of the B200-native random-features Gram / closed-form-kernel library
+ * (arXiv 2110.01899, "Ternary Random Features").  Shared library: paper_2110_01899_b200/librf_b200.so
+ *
+ * Citations "P:<line>" are lines of the paper text.  Notation follows the paper:
+ *   X = [x_1 … x_n] ∈ R^{p×n} data (P:5);  W ∈ R^{m×p} random projection, rows w_k;
+ *   Σ = σ(WX) ∈ R^{m×n} random features (P:3);  G = (1/m) ΣᵀΣ ∈ R^{n×n} (Eq. def_Gram);
+ *   Φ(x_i,x_j) = E_w σ(wᵀx_i)σ(wᵀx_j) approximated by the Taylor closed form EQ1;
+ *   τ estimated by Lemma 1, τ̂ = (1/n)Σ‖x_i‖² (Algorithm 1 step 1 P:739).
+ *
+ * MEMORY LAYOUT (all row-major, element strides in ELEMENTS):
+ *   X  : sample-major, X[i*ldx + l] = component l of sample x_i   (n rows of p values; = the paper's
+ *        column-major p×n).  ldx ≥ p.
+ *   W  : W[k*ldw + l] = component l of w_k                         (m_local rows of p values). ldw ≥ p.
+ *   G, Φ : out[i*ld + j] = entry (i, j), 0 ≤ i, j < n.  ld ≥ n.
+ *
+ * DTYPES / PRECISION MODES (validated; no silent casts):
+ *   RF_PREC_FP64   X, W f64 ; output f64 ; SIMT DFMA (small problems / reference mode)
+ *   RF_PREC_FP32   X, W f32 ; output f32 ; SIMT FFMA, fp32-accurate
+ *   RF_PREC_3XTF32 X, W f32 ; output f32 ; tcgen05 kind::tf32, hi·hi + hi·lo + lo·hi, fp32-accurate
+ *   RF_PREC_TF32   X, W f32 ; output f32 ; tcgen05 kind::tf32, one pass (≈1e-3 class)
+ *   RF_PREC_BF16   X, W bf16; output f32 ; tcgen05 kind::f16, Σ stored bf16, fp32 accumulation
+ *
+ * OWNERSHIP: the caller allocates every device buffer (inputs, outputs, workspace).  The library never
+ * allocates device memory on a call path and keeps no pointer after a call returns.
+ *
+ * ASYNC: GPU work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default stream)
+ * and the call returns after enqueue, EXCEPT: rf_moments (host-only, synchronous); rf_estimate_tau and
+ * rf_phi_closed_form with tau <= 0 (one 8-byte device→host copy + stream synchronize, because the
+ * moments depend on τ).
+ *
+ * ERRORS: every argument is validated before any launch; on failure nothing is enqueued and the
+ * status is returned with a message available from rf_last_error() (thread-local).  No C++ exception
+ * crosses the ABI.  There is no CPU fallback: a device that is not sm_100 gives RF_E_UNSUPPORTED.
+ */
+#ifndef RF_B200_H
+#define RF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RF_OK = 0,
+  RF_E_INVALID = 1,      /* bad size / pointer / alignment / dtype-precision pair / τ <= 0 in rf_moments */
+  RF_E_UNSUPPORTED = 2,  /* device is not sm_100 (B200) */
+  RF_E_NONFINITE = 3,    /* σ non-finite at a quadrature node */
+  RF_E_CUDA = 4,         /* a CUDA runtime/driver error (launch failure, earlier async fault) */
+  RF_E_NCCL = 5,         /* reserved for the collective layer */
+  RF_E_WORKSPACE = 6     /* workspace pointer NULL or smaller than rf_*_workspace_size() */
+} rf_status;
+
+/* σ ∈ {tanh, erf, sigmoid − 1/2}: the north star's activations (Assumption 3). */
+typedef enum { RF_ACT_TANH = 0, RF_ACT_ERF = 1, RF_ACT_SIGMOID_HALF = 2 } rf_act;
+typedef enum { RF_DT_F64 = 0, RF_DT_F32 = 1, RF_DT_BF16 = 2 } rf_dtype;
+typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_TF32 = 3, RF_PREC_BF16 = 4 } rf_prec;
+/* UPPER: write only entries j >= i (the rest of the buffer is untouched).
+ * FULL : write all n×n entries; the lower triangle mirrors the upper one (Φ: pivot = row, see below). */
+typedef enum { RF_OUT_UPPER = 0, RF_OUT_FULL = 1 } rf_out;
+
+/* Gaussian moments at τ (EQ1 coefficients P:1040; Theorem 1):
+ *   kd[k][d] = E[(√τ ξ)^k σ^(d)(√τ ξ)], ξ ~ N(0,1), k = 0..4, d = 0..2
+ *   e_sigma_sq = E[σ(√τ ξ)²]
+ *   d0 = e_sigma_sq − kd[0][0]² − τ kd[0][1]²,  d1 = kd[0][1]²,  d2 = kd[0][2]²/4
+ * method: 0 = Gauss–Hermite (Golub–Welsch, `nodes` points), 1 = composite trapezoid fallback. */
+typedef struct {
+  double tau;
+  double kd[5][3];
+  double e_sigma_sq;
+  double d0, d1, d2;
+  int32_t nodes;
+  int32_t method;
+  double quad_err_est;   /* |Q_N − Q_{N/2}| max over the table (GH), or the trapezoid h-halving change */
+} rf_moments_t;
+
+/* Thread-local text of the last error on this thread ("" after success). */
+const char* rf_last_error(void);
+const char* rf_version(void);
+
+/* 1 if `device` is an sm_100 part this library's kernels run on, else 0 (no error text). */
+int rf_device_supported(int device);
+
+/* ---------------------------------------------------------------------------------------------
+ * rf_moments — host, synchronous.  Gauss–Hermite quadrature (probabilists' weight) by Golub–Welsch;
+ * nodes = 0 → adaptive (N = 64, 128, 256, 512 until the table changes by < 1e-13, else trapezoid on
+ * [−40, 40], h = 0.05).  nodes > 0 → exactly that many GH nodes (2 ≤ nodes ≤ 1024).
+ * Errors: tau <= 0 or not finite → RF_E_INVALID; out == NULL → RF_E_INVALID; non-finite σ → RF_E_NONFINITE.
+ */
+rf_status rf_moments(rf_act act, double tau, int32_t nodes, rf_moments_t* out);
+
+/* ---------------------------------------------------------------------------------------------
+ * rf_estimate_tau — Lemma 1: *tau_out = (1/n) Σ_i ‖x_i‖², fp64 accumulation, deterministic
+ * order.  Device X (layout above, dtype x_dt), device workspace of rf_tau_workspace_size(n) bytes.
+ * Synchronizes `stream` (8-byte D2H copy into *tau_out, a host pointer).
+ */
+rf_status rf_tau_workspace_size(int64_t n, size_t* bytes);
+rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n,
+                          double* tau_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * rf_gram — G = (1/m_total) Σ_{k < m_local} σ(w_kᵀx_i) σ(w_kᵀx_j)   (Eq. def_Gram)
+ *   X       device, n × p (ldx), dtype per `prec`
+ *   W_local device, m_local × p (ldw): this rank's rows of W (m_local = m_total on one GPU).  The
+ *           sum over the rank's features is scaled by 1/m_total so that summing the partial G of all
+ *           ranks (reduce-scatter / all-reduce) gives G.
+ *   G       device, n × n (ldg), f64 in RF_PREC_FP64 else f32; `out` selects UPPER or FULL.
+ *   ws      device workspace ≥ rf_gram_workspace_size(p, n, m_local, prec) bytes, 256-B aligned
+ *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode).
+ * Pipeline: [3XTF32: K2 split X, W] → K3 fused Σᵀ = σ(X·Wᵀ) (tcgen05 GEMM, σ in the epilogue)
+ *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 128×256 tiles with j ≥ i.
+ * Alignment: X, W, G, ws 16-B aligned; ldx·esize, ldw·esize, ldg·esize multiples of 16 B (TMA).
+ */
+rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec prec, size_t* bytes);
+rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
+                  int64_t p, int64_t n, int64_t m_local, int64_t m_total,
+                  rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * rf_phi_closed_form — Φ(x_i, x_j) by EQ1 for every pair i ≤ j with i in the row range
+ * [row_begin, row_end) (row_begin a multiple of 128, row_end ≤ n; pass 0, n for all rows).
+ *   Gram–Schmidt with x_i (the row) as pivot: u_a = ‖x_i‖, v_b = x_iᵀx_j/‖x_i‖,
+ *   u_b = √max(0, ‖x_j‖² − (x_iᵀx_j)²/‖x_i‖²); diagonal: u_b = 0, v_b = u_a exactly.
+ *   α = u_a/√τ − 1, β = u_b/√τ − 1, ν = v_b/√τ;  with ⟨k,d⟩ = mom->kd[k][d]
+ *   Φ = A0(α)C0(β) + ν A1(α) C1(β) + (ν²/2) A2(α) ⟨0,2⟩,
+ *   A_j(α) = ⟨j,0⟩ + α⟨j+1,1⟩ + (α²/2)⟨j+2,2⟩, C0(β) = ⟨0,0⟩ + β⟨1,1⟩ + (β²/2)⟨2,2⟩, C1(β) = ⟨0,1⟩ + β⟨1,2⟩
+ *   (this is EQ1's 18 terms regrouped; DESIGN.md §4 lists the four corrected garbles).
+ *   tau  > 0: used as given.  tau <= 0: τ̂ of Lemma 1 over ALL n rows (one stream sync).
+ *   mom  != NULL: used as given (its tau must equal the τ used).  NULL: rf_moments(act, τ, 0).
+ *   Phi  device, n × n (ldphi), f64 in RF_PREC_FP64 else f32.  UPPER writes j ≥ i of rows in range;
+ *        FULL additionally writes the mirror Φ[j][i] = Φ[i][j] (only rows/cols the range covers).
+ *   ws   ≥ rf_phi_workspace_size(p, n, prec).
+ * Pipeline: K1 row norms (fp64) [+ τ̂] → per-row coefficients → K5 fused XᵀX (tcgen05) + EQ1 epilogue.
+ * A zero-norm sample makes v_b undefined: with tau <= 0 it is detected → RF_E_INVALID;
+ * with tau > 0 the affected row of Φ is non-finite.
+ */
+rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes);
+rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
+                             rf_act act, double tau, const rf_moments_t* mom,
+                             rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * rf_phi_row_split — row-block sharding of Φ over `world` ranks with no collective: returns the
+ * range [*row_begin, *row_end) of rank `rank`, boundaries multiples of 128, balanced by upper-triangle
+ * area (row i carries n − i entries).  Host only.
+ */
+rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end);
+
+/* Number of kernel launches the last successful rf_gram / rf_phi_closed_form call on this thread
+ * enqueued (for bench accounting). */
+int32_t rf_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RF_B200_H */

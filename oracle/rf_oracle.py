@@ -138,8 +138,9 @@ def hermite_rule(N: int) -> Tuple[np.ndarray, np.ndarray]:
         if done:
             break
     x = 0.5 * (x - x[::-1])           # enforce exact symmetry of the rule
-    _, pNm1 = _psi(N, x)
-    w = 1.0 / (N * pNm1 * pNm1)
+    with np.errstate(over="ignore"):
+        _, pNm1 = _psi(N, x)
+        w = 1.0 / (N * pNm1 * pNm1)          # far-tail weights underflow to 0 for large N
     w = 0.5 * (w + w[::-1])
     return x, w
 

@@ -1,0 +1,153 @@
+"""B200-native random-features Gram G and closed-form kernel Φ (arXiv 2110.01899).
+
+Python face of the C ABI in include/rf.h (same names).  The functions below only marshal arguments:
+they allocate outputs/workspace with torch when the caller does not pass them, pass raw device
+pointers and the current CUDA stream, and raise on any non-OK status.  All arithmetic runs in
+librf_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional, Tuple
+
+from . import _lib
+from ._lib import ACT, OUT, PREC, RFError, load, rf_moments_t  # noqa: F401
+
+__all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf_phi_row_split",
+           "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_version", "rf_device_supported",
+           "rf_last_launch_count", "RFError", "PREC", "ACT"]
+
+_TORCH_DT = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_for(prec: str):
+    torch = _torch()
+    return {"fp64": torch.float64, "fp32": torch.float32, "3xtf32": torch.float32, "tf32": torch.float32,
+            "bf16": torch.bfloat16}[prec]
+
+
+def _out_dtype(prec: str):
+    torch = _torch()
+    return torch.float64 if prec == "fp64" else torch.float32
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_tensor(name, t, dtype):
+    if not t.is_cuda:
+        raise RFError(_lib.RF_E_INVALID, f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise RFError(_lib.RF_E_INVALID, f"{name} has dtype {t.dtype}, precision mode needs {dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise RFError(_lib.RF_E_INVALID, f"{name} must be 2-D with unit column stride")
+
+
+def rf_version() -> str:
+    return load().rf_version().decode()
+
+
+def rf_device_supported(device: int = 0) -> bool:
+    return bool(load().rf_device_supported(device))
+
+
+def rf_last_launch_count() -> int:
+    return int(load().rf_last_launch_count())
+
+
+def rf_moments(act: str, tau: float, nodes: int = 0) -> Dict[str, object]:
+    lib = load()
+    m = rf_moments_t()
+    _lib.check(lib.rf_moments(ACT[act], float(tau), int(nodes), ctypes.byref(m)))
+    kd = [[m.kd[k][d] for d in range(3)] for k in range(5)]
+    return {"tau": m.tau, "kd": kd, "e_sigma_sq": m.e_sigma_sq, "d0": m.d0, "d1": m.d1, "d2": m.d2,
+            "nodes": m.nodes, "method": m.method, "quad_err_est": m.quad_err_est, "_struct": m}
+
+
+def rf_estimate_tau(X, ws=None, stream=None) -> float:
+    torch = _torch()
+    lib = load()
+    dt = {torch.float64: 0, torch.float32: 1, torch.bfloat16: 2}[X.dtype]
+    n, p = X.shape
+    need = ctypes.c_size_t()
+    _lib.check(lib.rf_tau_workspace_size(n, ctypes.byref(need)))
+    if ws is None:
+        ws = torch.empty(need.value, dtype=torch.uint8, device=X.device)
+    out = ctypes.c_double()
+    _lib.check(lib.rf_estimate_tau(ctypes.c_void_p(X.data_ptr()), dt, X.stride(0), p, n, ctypes.byref(out),
+                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return out.value
+
+
+def rf_gram_workspace_size(p: int, n: int, m_local: int, prec: str) -> int:
+    need = ctypes.c_size_t()
+    _lib.check(load().rf_gram_workspace_size(p, n, m_local, PREC[prec], ctypes.byref(need)))
+    return need.value
+
+
+def rf_phi_workspace_size(p: int, n: int, prec: str) -> int:
+    need = ctypes.c_size_t()
+    _lib.check(load().rf_phi_workspace_size(p, n, PREC[prec], ctypes.byref(need)))
+    return need.value
+
+
+def rf_gram(X, W, act: str = "tanh", prec: str = "bf16", out: str = "upper", m_total: Optional[int] = None,
+            G=None, ws=None, stream=None):
+    """G = (1/m_total) σ(W X)ᵀ σ(W X) over this rank's rows of W (Eq. def_Gram).
+    X: (n, p) sample-major CUDA tensor; W: (m_local, p).  Returns G (n, n)."""
+    torch = _torch()
+    lib = load()
+    dt = _dtype_for(prec)
+    _check_tensor("X", X, dt)
+    _check_tensor("W", W, dt)
+    n, p = X.shape
+    m_local = W.shape[0]
+    if W.shape[1] != p:
+        raise RFError(_lib.RF_E_INVALID, "X and W disagree on p")
+    m_total = m_local if m_total is None else int(m_total)
+    if G is None:
+        G = torch.zeros((n, n), dtype=_out_dtype(prec), device=X.device)
+    _check_tensor("G", G, _out_dtype(prec))
+    if ws is None:
+        ws = torch.empty(rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=X.device)
+    _lib.check(lib.rf_gram(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(W.data_ptr()), W.stride(0),
+                           p, n, m_local, m_total, ACT[act], PREC[prec], OUT[out], ctypes.c_void_p(G.data_ptr()),
+                           G.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return G
+
+
+def rf_phi_closed_form(X, act: str = "tanh", tau: float = 0.0, mom: Optional[dict] = None, prec: str = "bf16",
+                       out: str = "upper", row_begin: int = 0, row_end: Optional[int] = None, Phi=None, ws=None,
+                       stream=None):
+    """Φ by EQ1 for pairs i ≤ j, rows i in [row_begin, row_end).  tau <= 0 → Lemma 1 τ̂."""
+    torch = _torch()
+    lib = load()
+    dt = _dtype_for(prec)
+    _check_tensor("X", X, dt)
+    n, p = X.shape
+    row_end = n if row_end is None else int(row_end)
+    if Phi is None:
+        Phi = torch.zeros((n, n), dtype=_out_dtype(prec), device=X.device)
+    _check_tensor("Phi", Phi, _out_dtype(prec))
+    if ws is None:
+        ws = torch.empty(rf_phi_workspace_size(p, n, prec), dtype=torch.uint8, device=X.device)
+    mp = ctypes.byref(mom["_struct"]) if mom is not None else None
+    _lib.check(lib.rf_phi_closed_form(ctypes.c_void_p(X.data_ptr()), X.stride(0), p, n, ACT[act], float(tau), mp,
+                                      PREC[prec], OUT[out], int(row_begin), row_end,
+                                      ctypes.c_void_p(Phi.data_ptr()), Phi.stride(0),
+                                      ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return Phi
+
+
+def rf_phi_row_split(n: int, world: int, rank: int) -> Tuple[int, int]:
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(load().rf_phi_row_split(n, world, rank, ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value

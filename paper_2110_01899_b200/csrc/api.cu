@@ -1,0 +1,574 @@
+// C ABI (include/rf.h): validation, workspace planning, TMA descriptor creation and kernel dispatch.
+// Every compute step of the path runs in this library's kernels; there is no CPU fallback.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/rf.h"
+#include "k_aux.cuh"
+#include "k_simt.cuh"
+#include "rf_common.cuh"
+#include "tc_gemm.cuh"
+
+namespace rfh {
+int compute_moments(rf_act act, double tau, int nodes, rf_moments_t* out);
+}
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+rf_status fail(rf_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+rf_status ok() {
+  g_err.clear();
+  return RF_OK;
+}
+
+#define RF_CUDA_CHECK(expr)                                                                     \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess) return fail(RF_E_CUDA, "%s: %s (%s)", #expr, cudaGetErrorName(_e),   \
+                                       cudaGetErrorString(_e));                                 \
+  } while (0)
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+inline size_t align256(size_t a) { return (a + 255) & ~size_t(255); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+size_t esize_of(rf_prec prec) {
+  switch (prec) {
+    case RF_PREC_FP64: return 8;
+    case RF_PREC_BF16: return 2;
+    default: return 4;
+  }
+}
+const char* prec_name(rf_prec p) {
+  switch (p) {
+    case RF_PREC_FP64: return "FP64";
+    case RF_PREC_FP32: return "FP32";
+    case RF_PREC_3XTF32: return "3XTF32";
+    case RF_PREC_TF32: return "TF32";
+    case RF_PREC_BF16: return "BF16";
+  }
+  return "?";
+}
+bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
+bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_SIGMOID_HALF; }
+bool valid_out(int o) { return o == RF_OUT_UPPER || o == RF_OUT_FULL; }
+
+// ---------------------------------------------------------------- device / driver
+struct DevInfo {
+  int sms = 0;
+  int major = 0, minor = 0;
+};
+DevInfo dev_info(int dev) {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && have[dev]) return cache[dev];
+  DevInfo d;
+  cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (dev >= 0 && dev < 64) {
+    cache[dev] = d;
+    have[dev] = true;
+  }
+  return d;
+}
+
+rf_status check_device(DevInfo* out) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(RF_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  DevInfo d = dev_info(dev);
+  if (d.major != 10 || d.minor != 0)
+    return fail(RF_E_UNSUPPORTED, "device %d is sm_%d%d; this library runs only on sm_100 (B200)", dev, d.major,
+                d.minor);
+  if (out) *out = d;
+  return RF_OK;
+}
+
+typedef CUresult (*PFN_encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encode_tiled encode_fn() {
+  static PFN_encode_tiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encode_tiled>(p);
+  });
+  return fn;
+}
+
+// Row-major matrix rows × kext (ld elements), box box_rows × (128 B of K), 128-B swizzle, OOB → 0.
+rf_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t rows, int64_t kext, int64_t ld,
+                    int box_rows) {
+  PFN_encode_tiled enc = encode_fn();
+  if (!enc) return fail(RF_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const int es = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)kext, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RF_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RF_OK;
+}
+
+template <class Cfg, class Epi>
+rf_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo, const CUtensorMap& blo,
+                    const rfk::Sched& s, int num_kb, const Epi& epi, int sms, cudaStream_t st) {
+  if (s.num_tiles <= 0) return RF_OK;
+  auto kern = rfk::tc_gemm_kernel<Cfg, Epi>;
+  RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES));
+  const int grid = std::min(s.num_tiles, sms);
+  kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(a, b, alo, blo, s, num_kb, epi);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  return RF_OK;
+}
+
+template <typename T, class Epi>
+rf_status launch_simt(const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int tri,
+                      int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st) {
+  const int tn = (int)((N + 63) / 64);
+  if (row_tile1 <= row_tile0 || tn == 0) return RF_OK;
+  dim3 grid(tn, row_tile1 - row_tile0);
+  rfk::simt_gemm_nt<T, Epi><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, tri, row_tile0, epi);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  return RF_OK;
+}
+
+rf_status launch_split(const float* src, int64_t lds, int64_t rows, int64_t cols, float* hi, float* lo, int64_t ldd,
+                       int sms, cudaStream_t st) {
+  const int64_t total = rows * cols;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+  if (grid < 1) grid = 1;
+  rfk::k_split_tf32<<<grid, 256, 0, st>>>(src, lds, rows, cols, hi, lo, ldd);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  return RF_OK;
+}
+
+rf_status launch_rownorm(const void* X, rf_prec prec, int64_t ldx, int64_t p, int64_t n, double* nrm2,
+                         cudaStream_t st) {
+  const int grid = (int)((n + 7) / 8);
+  if (prec == RF_PREC_FP64)
+    rfk::k_rownorm<double><<<grid, 256, 0, st>>>((const double*)X, ldx, p, n, nrm2);
+  else if (prec == RF_PREC_BF16)
+    rfk::k_rownorm<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)X, ldx, p, n, nrm2);
+  else
+    rfk::k_rownorm<float><<<grid, 256, 0, st>>>((const float*)X, ldx, p, n, nrm2);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  return RF_OK;
+}
+
+// ---------------------------------------------------------------- workspace plans
+struct GramPlan {
+  int64_t ldS, ldp;
+  size_t off_s0, off_s1, off_xhi, off_xlo, off_whi, off_wlo, total;
+};
+GramPlan gram_plan(int64_t p, int64_t n, int64_t m_local, rf_prec prec) {
+  GramPlan g{};
+  g.ldS = round_up(std::max<int64_t>(m_local, 1), 64);
+  g.ldp = round_up(p, 32);
+  const size_t es = (prec == RF_PREC_FP64) ? 8 : (prec == RF_PREC_BF16 ? 2 : 4);
+  size_t off = 0;
+  g.off_s0 = off;
+  off = align256(off + (size_t)n * g.ldS * es);
+  g.off_s1 = off;
+  if (prec == RF_PREC_3XTF32) {
+    off = align256(off + (size_t)n * g.ldS * 4);
+    g.off_xhi = off; off = align256(off + (size_t)n * g.ldp * 4);
+    g.off_xlo = off; off = align256(off + (size_t)n * g.ldp * 4);
+    g.off_whi = off; off = align256(off + (size_t)m_local * g.ldp * 4);
+    g.off_wlo = off; off = align256(off + (size_t)m_local * g.ldp * 4);
+  }
+  g.total = off;
+  return g;
+}
+
+struct PhiPlan {
+  int64_t ldp;
+  size_t off_nrm2, off_tau, off_rc, off_nrm2o, off_xhi, off_xlo, total;
+};
+PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
+  PhiPlan g{};
+  g.ldp = round_up(p, 32);
+  size_t off = 0;
+  g.off_nrm2 = off; off = align256(off + (size_t)n * 8);
+  g.off_tau = off; off = align256(off + 16);
+  g.off_rc = off; off = align256(off + (size_t)n * (prec == RF_PREC_FP64 ? sizeof(rfk::RowCoefD) : sizeof(rfk::RowCoef)));
+  g.off_nrm2o = off; off = align256(off + (size_t)n * 8);
+  if (prec == RF_PREC_3XTF32) {
+    g.off_xhi = off; off = align256(off + (size_t)n * g.ldp * 4);
+    g.off_xlo = off; off = align256(off + (size_t)n * g.ldp * 4);
+  }
+  g.total = off;
+  return g;
+}
+
+rf_status validate_matrix(const char* name, const void* ptr, int64_t ld, int64_t cols, size_t es) {
+  if (!ptr) return fail(RF_E_INVALID, "%s is NULL", name);
+  if (!aligned16(ptr)) return fail(RF_E_INVALID, "%s is not 16-byte aligned", name);
+  if (ld < cols) return fail(RF_E_INVALID, "ld of %s (%lld) < %lld", name, (long long)ld, (long long)cols);
+  if ((ld * (int64_t)es) % 16 != 0)
+    return fail(RF_E_INVALID, "ld of %s × element size (%lld B) is not a multiple of 16 B (TMA requirement)", name,
+                (long long)(ld * (int64_t)es));
+  return RF_OK;
+}
+
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+const char* rf_last_error(void) { return g_err.c_str(); }
+const char* rf_version(void) { return "rf_b200 0.1 (sm_100a: tcgen05/TMA/TMEM; SIMT fp32/fp64)"; }
+int32_t rf_last_launch_count(void) { return g_launches; }
+
+int rf_device_supported(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    return 0;
+  }
+  DevInfo d = dev_info(device);
+  return (d.major == 10 && d.minor == 0) ? 1 : 0;
+}
+
+rf_status rf_moments(rf_act act, double tau, int32_t nodes, rf_moments_t* out) {
+  if (!out) return fail(RF_E_INVALID, "rf_moments: out is NULL");
+  if (!valid_act(act)) return fail(RF_E_INVALID, "rf_moments: unknown activation %d", (int)act);
+  if (!(tau > 0.0) || !std::isfinite(tau)) return fail(RF_E_INVALID, "rf_moments: tau must be finite and > 0");
+  if (nodes < 0 || nodes == 1 || nodes > 1024) return fail(RF_E_INVALID, "rf_moments: nodes must be 0 or in [2, 1024]");
+  int r = rfh::compute_moments(act, tau, nodes, out);
+  if (r == 1) return fail(RF_E_NONFINITE, "rf_moments: sigma non-finite at a quadrature node");
+  if (r == 2) return fail(RF_E_INVALID, "rf_moments: Golub-Welsch eigen-solver did not converge");
+  return ok();
+}
+
+rf_status rf_tau_workspace_size(int64_t n, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (n <= 0) return fail(RF_E_INVALID, "n must be > 0");
+  *bytes = align256((size_t)n * 8) + 256;
+  return ok();
+}
+
+rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n, double* tau_out, void* ws,
+                          size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_estimate_tau: p, n must be > 0");
+  if (!tau_out) return fail(RF_E_INVALID, "rf_estimate_tau: tau_out is NULL");
+  if (x_dt < RF_DT_F64 || x_dt > RF_DT_BF16) return fail(RF_E_INVALID, "rf_estimate_tau: bad dtype");
+  const rf_prec pr = x_dt == RF_DT_F64 ? RF_PREC_FP64 : (x_dt == RF_DT_BF16 ? RF_PREC_BF16 : RF_PREC_FP32);
+  rf_status s = validate_matrix("X", X, ldx, p, esize_of(pr));
+  if (s) return s;
+  size_t need;
+  rf_tau_workspace_size(n, &need);
+  if (!ws || ws_bytes < need || !aligned16(ws))
+    return fail(RF_E_WORKSPACE, "rf_estimate_tau: workspace needs %zu bytes (16-B aligned)", need);
+  if ((s = check_device(nullptr))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* nrm2 = (double*)ws;
+  double* out = (double*)((char*)ws + align256((size_t)n * 8));
+  if ((s = launch_rownorm(X, pr, ldx, p, n, nrm2, st))) return s;
+  rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, out);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  double h[2];
+  RF_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+  RF_CUDA_CHECK(cudaStreamSynchronize(st));
+  *tau_out = h[0];
+  return ok();
+}
+
+rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec prec, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (p <= 0 || n <= 0 || m_local <= 0) return fail(RF_E_INVALID, "p, n, m_local must be > 0");
+  if (!valid_prec(prec)) return fail(RF_E_INVALID, "unknown precision %d", (int)prec);
+  *bytes = gram_plan(p, n, m_local, prec).total;
+  return ok();
+}
+
+rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n, int64_t m_local,
+                  int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg, void* ws,
+                  size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (p <= 0 || n <= 0 || m_local <= 0) return fail(RF_E_INVALID, "rf_gram: p, n, m_local must be > 0");
+  if (m_total < m_local) return fail(RF_E_INVALID, "rf_gram: m_total (%lld) < m_local (%lld)", (long long)m_total,
+                                     (long long)m_local);
+  if (n > (int64_t)1 << 31 || m_local > (int64_t)1 << 31 || p > (int64_t)1 << 31)
+    return fail(RF_E_INVALID, "rf_gram: sizes must be < 2^31");
+  if (!valid_act(act)) return fail(RF_E_INVALID, "rf_gram: unknown activation %d", (int)act);
+  if (!valid_prec(prec)) return fail(RF_E_INVALID, "rf_gram: unknown precision %d", (int)prec);
+  if (!valid_out(out)) return fail(RF_E_INVALID, "rf_gram: unknown output mode %d", (int)out);
+  const size_t es = esize_of(prec);
+  rf_status s;
+  if ((s = validate_matrix("X", X, ldx, p, es))) return s;
+  if ((s = validate_matrix("W", W, ldw, p, es))) return s;
+  if ((s = validate_matrix("G", G, ldg, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  const GramPlan pl = gram_plan(p, n, m_local, prec);
+  if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(RF_E_WORKSPACE, "rf_gram: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total, ws_bytes);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  const int full = out == RF_OUT_FULL;
+  const int tiles_m = (int)((n + 127) / 128);
+  const int tiles_n = (int)((n + 255) / 256);
+
+  if (prec == RF_PREC_FP64 || prec == RF_PREC_FP32) {
+    if (prec == RF_PREC_FP64) {
+      double* S = (double*)(w + pl.off_s0);
+      rfk::SimtSigma<double> e1{S, pl.ldS, n, m_local, (int)act};
+      if ((s = launch_simt<double>((const double*)X, ldx, (const double*)W, ldw, n, m_local, p, 0, 0,
+                                   (int)((n + 63) / 64), e1, st)))
+        return s;
+      rfk::SimtSyrk<double> e2{(double*)G, ldg, n, 1.0 / (double)m_total, full};
+      if ((s = launch_simt<double>(S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+        return s;
+    } else {
+      float* S = (float*)(w + pl.off_s0);
+      rfk::SimtSigma<float> e1{S, pl.ldS, n, m_local, (int)act};
+      if ((s = launch_simt<float>((const float*)X, ldx, (const float*)W, ldw, n, m_local, p, 0, 0,
+                                  (int)((n + 63) / 64), e1, st)))
+        return s;
+      rfk::SimtSyrk<float> e2{(float*)G, ldg, n, (float)(1.0 / (double)m_total), full};
+      if ((s = launch_simt<float>(S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+        return s;
+    }
+    return ok();
+  }
+
+  CUtensorMap tA, tB, tAl, tBl;
+  const rfk::Sched s3 = rfk::Sched::rect(0, tiles_m, (int)((m_local + 255) / 256));
+  const rfk::Sched s4 = rfk::Sched::triangle(0, tiles_m, tiles_n);
+  rfk::EpiSyrk e4{(float*)G, ldg, n, (float)(1.0 / (double)m_total), full};
+  if (prec == RF_PREC_BF16) {
+    using C = rfk::TcCfg<1, 1>;
+    __nv_bfloat16* S = (__nv_bfloat16*)(w + pl.off_s0);
+    if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
+    if ((s = make_tmap(&tB, W, true, m_local, p, ldw, C::BN))) return s;
+    rfk::EpiSigma<0> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
+    if ((s = launch_tc<C>(tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, S, true, n, m_local, pl.ldS, C::BM))) return s;
+    if ((s = make_tmap(&tB, S, true, n, m_local, pl.ldS, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+  } else if (prec == RF_PREC_TF32) {
+    using C = rfk::TcCfg<2, 1>;
+    float* S = (float*)(w + pl.off_s0);
+    if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
+    if ((s = make_tmap(&tB, W, false, m_local, p, ldw, C::BN))) return s;
+    rfk::EpiSigma<1> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
+    if ((s = launch_tc<C>(tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, S, false, n, m_local, pl.ldS, C::BM))) return s;
+    if ((s = make_tmap(&tB, S, false, n, m_local, pl.ldS, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+  } else {  // 3XTF32
+    using C = rfk::TcCfg<2, 3>;
+    float* Sh = (float*)(w + pl.off_s0);
+    float* Sl = (float*)(w + pl.off_s1);
+    float* Xh = (float*)(w + pl.off_xhi);
+    float* Xl = (float*)(w + pl.off_xlo);
+    float* Wh = (float*)(w + pl.off_whi);
+    float* Wl = (float*)(w + pl.off_wlo);
+    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
+    if ((s = launch_split((const float*)W, ldw, m_local, p, Wh, Wl, pl.ldp, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, C::BM))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, C::BM))) return s;
+    if ((s = make_tmap(&tB, Wh, false, m_local, p, pl.ldp, C::BN))) return s;
+    if ((s = make_tmap(&tBl, Wl, false, m_local, p, pl.ldp, C::BN))) return s;
+    rfk::EpiSigma<2> e3{Sh, Sl, pl.ldS, n, m_local, (int)act};
+    if ((s = launch_tc<C>(tA, tB, tAl, tBl, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Sh, false, n, m_local, pl.ldS, C::BM))) return s;
+    if ((s = make_tmap(&tAl, Sl, false, n, m_local, pl.ldS, C::BM))) return s;
+    if ((s = make_tmap(&tB, Sh, false, n, m_local, pl.ldS, C::BN))) return s;
+    if ((s = make_tmap(&tBl, Sl, false, n, m_local, pl.ldS, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tAl, tBl, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+  }
+  return ok();
+}
+
+rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "p, n must be > 0");
+  if (!valid_prec(prec)) return fail(RF_E_INVALID, "unknown precision %d", (int)prec);
+  *bytes = phi_plan(p, n, prec).total;
+  return ok();
+}
+
+rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end) {
+  if (n <= 0 || world <= 0 || rank < 0 || rank >= world || !row_begin || !row_end)
+    return fail(RF_E_INVALID, "rf_phi_row_split: bad arguments");
+  // rows of 128; boundary b_r = smallest tile boundary with triangle area above ≥ r/world of the total
+  const int64_t T = (n + 127) / 128;
+  auto area_before = [&](int64_t tile) -> double {   // entries j ≥ i in rows [0, 128·tile)
+    const double r = std::min<int64_t>(tile * 128, n);
+    return r * (double)n - r * (r - 1) / 2.0;
+  };
+  const double total = area_before(T);
+  auto boundary = [&](int32_t r) -> int64_t {
+    if (r <= 0) return 0;
+    if (r >= world) return T;
+    const double target = total * r / world;
+    int64_t lo = 0, hi = T;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) / 2;
+      if (area_before(mid) < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  *row_begin = std::min<int64_t>(boundary(rank) * 128, n);
+  *row_end = std::min<int64_t>(boundary(rank + 1) * 128, n);
+  return ok();
+}
+
+rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                             const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_phi_closed_form: p, n must be > 0");
+  if (n > (int64_t)1 << 31 || p > (int64_t)1 << 31) return fail(RF_E_INVALID, "rf_phi_closed_form: sizes must be < 2^31");
+  if (!valid_act(act)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown activation %d", (int)act);
+  if (!valid_prec(prec)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown precision %d", (int)prec);
+  if (!valid_out(out)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown output mode %d", (int)out);
+  if (row_begin < 0 || row_end > n || row_begin > row_end || (row_begin % 128) != 0 ||
+      (row_end != n && (row_end % 128) != 0))
+    return fail(RF_E_INVALID, "rf_phi_closed_form: row range [%lld, %lld) must satisfy 0 <= begin <= end <= n, "
+                "begin %% 128 == 0, end == n or end %% 128 == 0", (long long)row_begin, (long long)row_end);
+  if (!std::isfinite(tau)) return fail(RF_E_INVALID, "rf_phi_closed_form: tau is not finite");
+  const size_t es = esize_of(prec);
+  rf_status s;
+  if ((s = validate_matrix("X", X, ldx, p, es))) return s;
+  if ((s = validate_matrix("Phi", Phi, ldphi, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  const PhiPlan pl = phi_plan(p, n, prec);
+  if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(RF_E_WORKSPACE, "rf_phi_closed_form: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total,
+                ws_bytes);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  double* nrm2 = (double*)(w + pl.off_nrm2);
+  double* tau_dev = (double*)(w + pl.off_tau);
+
+  // Φ1: row norms (all n rows: columns j of every row block need ‖x_j‖²)
+  if ((s = launch_rownorm(X, prec, ldx, p, n, nrm2, st))) return s;
+  if (!(tau > 0.0)) {   // Lemma 1 τ̂
+    rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, tau_dev);
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    double h[2];
+    RF_CUDA_CHECK(cudaMemcpyAsync(h, tau_dev, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RF_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (h[1] != 0.0)
+      return fail(RF_E_INVALID, "rf_phi_closed_form: %lld sample(s) with zero norm (v_b undefined, P:1017)",
+                  (long long)h[1]);
+    tau = h[0];
+    if (!(tau > 0.0)) return fail(RF_E_INVALID, "rf_phi_closed_form: estimated tau is not > 0");
+  }
+  // Φ2: moments
+  rf_moments_t mloc;
+  if (mom) {
+    if (std::fabs(mom->tau - tau) > 1e-12 * std::fabs(tau))
+      return fail(RF_E_INVALID, "rf_phi_closed_form: mom->tau (%.17g) != tau used (%.17g)", mom->tau, tau);
+    mloc = *mom;
+  } else {
+    rf_status ms = rf_moments(act, tau, 0, &mloc);
+    if (ms) return ms;
+  }
+  // Φ3: per-row coefficients
+  rfk::RowMoments rm;
+  std::memcpy(rm.kd, mloc.kd, sizeof(rm.kd));
+  rm.inv_st = 1.0 / std::sqrt(tau);
+  const int cgrid = (int)((n + 255) / 256);
+  const double k22h = 0.5 * mloc.kd[2][2];
+  const int full = out == RF_OUT_FULL;
+  if (prec == RF_PREC_FP64) {
+    rfk::RowCoefD* rc = (rfk::RowCoefD*)(w + pl.off_rc);
+    double* nj = (double*)(w + pl.off_nrm2o);
+    rfk::k_row_coef<rfk::RowCoefD, double><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    rfk::SimtEq1<double, rfk::RowCoefD> e{(double*)Phi, ldphi, n, rc, nj, mloc.kd[0][0], mloc.kd[1][1], k22h,
+                                          mloc.kd[0][1], mloc.kd[1][2], rm.inv_st, full};
+    return (s = launch_simt<double>((const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
+                                    (int)((row_end + 63) / 64), e, st))
+               ? s
+               : ok();
+  }
+  rfk::RowCoef* rc = (rfk::RowCoef*)(w + pl.off_rc);
+  float* nj = (float*)(w + pl.off_nrm2o);
+  rfk::k_row_coef<rfk::RowCoef, float><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  if (row_end <= row_begin) return ok();
+  if (prec == RF_PREC_FP32) {
+    rfk::SimtEq1<float, rfk::RowCoef> e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1],
+                                        (float)k22h, (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st,
+                                        full};
+    return (s = launch_simt<float>((const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
+                                   (int)((row_end + 63) / 64), e, st))
+               ? s
+               : ok();
+  }
+  // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle tiles
+  rfk::EpiEq1 e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1], (float)k22h,
+                (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st, full};
+  const int tiles_n = (int)((n + 255) / 256);
+  const rfk::Sched sc = rfk::Sched::triangle((int)(row_begin / 128), (int)((row_end + 127) / 128), tiles_n);
+  CUtensorMap tA, tB, tAl, tBl;
+  if (prec == RF_PREC_BF16) {
+    using C = rfk::TcCfg<1, 1>;
+    if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
+    if ((s = make_tmap(&tB, X, true, n, p, ldx, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+  } else if (prec == RF_PREC_TF32) {
+    using C = rfk::TcCfg<2, 1>;
+    if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
+    if ((s = make_tmap(&tB, X, false, n, p, ldx, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+  } else {
+    using C = rfk::TcCfg<2, 3>;
+    float* Xh = (float*)(w + pl.off_xhi);
+    float* Xl = (float*)(w + pl.off_xlo);
+    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, C::BM))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, C::BM))) return s;
+    if ((s = make_tmap(&tB, Xh, false, n, p, pl.ldp, C::BN))) return s;
+    if ((s = make_tmap(&tBl, Xl, false, n, p, pl.ldp, C::BN))) return s;
+    if ((s = launch_tc<C>(tA, tB, tAl, tBl, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+  }
+  return ok();
+}
+
+}  // extern "C"

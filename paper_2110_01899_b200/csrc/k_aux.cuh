@@ -1,0 +1,128 @@
+// Small HBM-bound kernels of the path:
+//   K1  row norms ‖x_i‖² (fp64 accumulation, one warp per row, warp-shuffle reduction)
+//       + deterministic τ̂ = (1/n)Σ‖x_i‖² (Lemma 1) + per-row EQ1 coefficients
+//   K2  fp32 → (tf32 hi, fp32 lo) split for the 3×TF32 operands
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "rf_common.cuh"
+
+namespace rfk {
+
+template <typename T> __device__ __forceinline__ double to_d(T v);
+template <> __device__ __forceinline__ double to_d<double>(double v) { return v; }
+template <> __device__ __forceinline__ double to_d<float>(float v) { return (double)v; }
+template <> __device__ __forceinline__ double to_d<__nv_bfloat16>(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+
+// One warp per row; 16-byte vector loads when the row is 16-B aligned (validated ldx), scalar tail.
+template <typename T>
+__global__ void __launch_bounds__(256) k_rownorm(const T* __restrict__ X, int64_t ldx, int64_t p, int64_t n,
+                                                 double* __restrict__ nrm2) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const T* x = X + row * ldx;
+  constexpr int V = 16 / sizeof(T);
+  const int64_t pv = p / V;
+  double s = 0.0;
+  for (int64_t c = lane; c < pv; c += 32) {
+    uint4 raw = __ldg(reinterpret_cast<const uint4*>(x) + c);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      double d = to_d<T>(e[u]);
+      s = fma(d, d, s);
+    }
+  }
+  for (int64_t c = pv * V + lane; c < p; c += 32) {
+    double d = to_d<T>(x[c]);
+    s = fma(d, d, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) nrm2[row] = s;
+}
+
+// Single block, fixed summation order ⇒ bit-reproducible τ̂.  out[0] = τ̂, out[1] = #zero-norm rows.
+__global__ void __launch_bounds__(1024) k_tau_reduce(const double* __restrict__ nrm2, int64_t n,
+                                                     double* __restrict__ out) {
+  __shared__ double sh[32];
+  __shared__ int zc[32];
+  double s = 0.0;
+  int z = 0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) {
+    double v = nrm2[i];
+    s += v;
+    z += (v == 0.0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    z += __shfl_xor_sync(0xffffffffu, z, o);
+  }
+  if ((threadIdx.x & 31) == 0) { sh[threadIdx.x >> 5] = s; zc[threadIdx.x >> 5] = z; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = sh[threadIdx.x];
+    z = zc[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      z += __shfl_xor_sync(0xffffffffu, z, o);
+    }
+    if (threadIdx.x == 0) {
+      out[0] = s / (double)n;
+      out[1] = (double)z;
+    }
+  }
+}
+
+// Moments needed per row: A_j(α) = ⟨j,0⟩ + α⟨j+1,1⟩ + (α²/2)⟨j+2,2⟩, j = 0,1,2.
+struct RowMoments {
+  double kd[5][3];
+  double inv_st;   // 1/√τ
+};
+
+// Per-row coefficients (fp64 arithmetic, stored as RC = RowCoef (f32) or RowCoefD (f64)); also ‖x_j‖²
+// as the output type for the column side of the epilogue.
+template <typename RC, typename NT>
+__global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm2, int64_t n, RowMoments m,
+                                                  RC* __restrict__ rc, NT* __restrict__ nrm2_out) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= n) return;
+  const double r2 = nrm2[i];
+  const double ua = sqrt(r2);
+  const double al = ua * m.inv_st - 1.0;
+  const double h = 0.5 * al * al;
+  const double A0 = m.kd[0][0] + al * m.kd[1][1] + h * m.kd[2][2];
+  const double A1 = m.kd[1][0] + al * m.kd[2][1] + h * m.kd[3][2];
+  const double A2 = m.kd[2][0] + al * m.kd[3][1] + h * m.kd[4][2];
+  RC c;
+  c.a0 = A0;
+  c.a1 = A1;
+  c.a2h = 0.5 * m.kd[0][2] * A2;
+  c.c = m.inv_st / ua;
+  c.inv_ua = 1.0 / ua;
+  c.nrm2 = r2;
+  c.nu_diag = ua * m.inv_st;
+  c.pad = 0;
+  rc[i] = c;
+  nrm2_out[i] = (NT)r2;
+}
+
+// hi = tf32 truncation of x, lo = x − hi (exact).  2-D: rows × cols with independent strides.
+__global__ void __launch_bounds__(256) k_split_tf32(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                                    int64_t cols, float* __restrict__ hi, float* __restrict__ lo,
+                                                    int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const float x = src[r * lds + c];
+    const float h = tf32_hi(x);
+    hi[r * ldd + c] = h;
+    lo[r * ldd + c] = x - h;
+  }
+}
+
+}  // namespace rfk

@@ -1,0 +1,214 @@
+// Φ2 — Gaussian moments at τ by Gauss–Hermite quadrature (host, fp64).
+//   ⟨k,d⟩ = E[(√τ ξ)^k σ^(d)(√τ ξ)], ξ ~ N(0,1)  — the coefficients of EQ1; the paper says
+//   which expectations are needed (draft P:193) but no method; the north star names Gauss–Hermite.
+//   d0, d1, d2 as in Theorem 1.
+// Nodes/weights by Golub–Welsch: the probabilists' Hermite Jacobi matrix (zero diagonal, off-diagonal
+// √k) is diagonalised by implicit-shift QL; nodes = eigenvalues, weights = squared first components of
+// the normalised eigenvectors (they sum to 1 for the N(0,1) density).
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/rf.h"
+
+namespace rfh {
+
+// Implicit QL with Wilkinson-type shifts on a symmetric tridiagonal matrix (diag d, sub-diagonal e,
+// e[n-1] unused); z carries the first row of the accumulated orthogonal transform.
+static bool tridiag_ql_first_row(std::vector<double>& d, std::vector<double>& e, std::vector<double>& z) {
+  const int n = (int)d.size();
+  for (int l = 0; l < n; ++l) {
+    int iter = 0;
+    for (;;) {
+      int m = l;
+      for (; m < n - 1; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 1.1e-16 * dd) break;
+      }
+      if (m == l) break;
+      if (++iter > 200) return false;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = d[m] - d[l] + e[l] / (g + std::copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      int i = m - 1;
+      bool deflated = false;
+      for (; i >= l; --i) {
+        double f = s * e[i];
+        const double b = c * e[i];
+        r = std::hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[m] = 0.0;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        f = z[i + 1];
+        z[i + 1] = s * z[i] + c * f;
+        z[i] = c * z[i] - s * f;
+      }
+      if (deflated) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[m] = 0.0;
+    }
+  }
+  return true;
+}
+
+bool gauss_hermite(int N, std::vector<double>& x, std::vector<double>& w) {
+  std::vector<double> d(N, 0.0), e(N, 0.0), z(N, 0.0);
+  for (int k = 0; k < N - 1; ++k) e[k] = std::sqrt((double)(k + 1));
+  z[0] = 1.0;
+  if (!tridiag_ql_first_row(d, e, z)) return false;
+  std::vector<int> idx(N);
+  for (int i = 0; i < N; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
+  x.resize(N);
+  w.resize(N);
+  for (int i = 0; i < N; ++i) {
+    x[i] = d[idx[i]];
+    w[i] = z[idx[i]] * z[idx[i]];
+  }
+  // exact symmetry of the rule
+  for (int i = 0; i < N / 2; ++i) {
+    const double xs = 0.5 * (x[N - 1 - i] - x[i]);
+    const double ws = 0.5 * (w[N - 1 - i] + w[i]);
+    x[i] = -xs; x[N - 1 - i] = xs;
+    w[i] = ws; w[N - 1 - i] = ws;
+  }
+  if (N & 1) x[N / 2] = 0.0;
+  return true;
+}
+
+// σ, σ', σ'' of the north-star activations (analytic; sigmoid − ½ = ½ tanh(t/2)).
+static inline void act_derivs(rf_act act, double t, double f[3]) {
+  switch (act) {
+    case RF_ACT_TANH: {
+      const double th = std::tanh(t);
+      f[0] = th;
+      f[1] = 1.0 - th * th;
+      f[2] = -2.0 * th * (1.0 - th * th);
+      break;
+    }
+    case RF_ACT_ERF: {
+      const double g = 1.1283791670955126 * std::exp(-t * t);   // 2/√π e^{−t²}
+      f[0] = std::erf(t);
+      f[1] = g;
+      f[2] = -2.0 * t * g;
+      break;
+    }
+    default: {
+      const double th = std::tanh(0.5 * t);
+      f[0] = 0.5 * th;
+      f[1] = 0.25 * (1.0 - th * th);
+      f[2] = -0.25 * th * (1.0 - th * th);
+      break;
+    }
+  }
+}
+
+// table[0..14] = kd[k][d] (k-major), table[15] = E[σ²].  Returns false on a non-finite value.
+static bool quad_table(rf_act act, double tau, const std::vector<double>& x, const std::vector<double>& w,
+                       double table[16]) {
+  std::memset(table, 0, 16 * sizeof(double));
+  const double st = std::sqrt(tau);
+  for (size_t q = 0; q < x.size(); ++q) {
+    const double t = st * x[q];
+    double f[3];
+    act_derivs(act, t, f);
+    if (!std::isfinite(f[0]) || !std::isfinite(f[1]) || !std::isfinite(f[2])) return false;
+    double tk = w[q];
+    for (int k = 0; k < 5; ++k) {
+      for (int dd = 0; dd < 3; ++dd) table[k * 3 + dd] += tk * f[dd];
+      tk *= t;
+    }
+    table[15] += w[q] * f[0] * f[0];
+  }
+  return true;
+}
+
+static bool trapezoid_table(rf_act act, double tau, double h, double table[16]) {
+  const double L = 40.0;
+  const int npts = (int)std::lround(2 * L / h) + 1;
+  std::vector<double> x(npts), w(npts);
+  for (int i = 0; i < npts; ++i) {
+    x[i] = -L + h * i;
+    w[i] = h * std::exp(-0.5 * x[i] * x[i]) * 0.3989422804014327;   // h·φ(x)
+  }
+  return quad_table(act, tau, x, w, table);
+}
+
+static void fill(const double table[16], double tau, rf_moments_t* out) {
+  out->tau = tau;
+  for (int k = 0; k < 5; ++k)
+    for (int dd = 0; dd < 3; ++dd) out->kd[k][dd] = table[k * 3 + dd];
+  out->e_sigma_sq = table[15];
+  out->d0 = table[15] - table[0] * table[0] - tau * table[1] * table[1];
+  out->d1 = table[1] * table[1];
+  out->d2 = 0.25 * table[2] * table[2];
+}
+
+// returns 0 ok, 1 non-finite, 2 eigen-solver failure
+int compute_moments(rf_act act, double tau, int nodes, rf_moments_t* out) {
+  std::vector<double> x, w;
+  double cur[16], prev[16];
+  if (nodes > 0) {
+    if (!gauss_hermite(nodes, x, w)) return 2;
+    if (!quad_table(act, tau, x, w, cur)) return 1;
+    fill(cur, tau, out);
+    out->nodes = nodes;
+    out->method = 0;
+    out->quad_err_est = 0.0;
+    if (nodes >= 4) {
+      std::vector<double> x2, w2;
+      if (gauss_hermite(nodes / 2, x2, w2) && quad_table(act, tau, x2, w2, prev)) {
+        double err = 0.0;
+        for (int i = 0; i < 16; ++i) err = std::max(err, std::fabs(cur[i] - prev[i]));
+        out->quad_err_est = err;
+      }
+    }
+    return 0;
+  }
+  bool have_prev = false;
+  for (int N = 64; N <= 512; N *= 2) {
+    if (!gauss_hermite(N, x, w)) return 2;
+    if (!quad_table(act, tau, x, w, cur)) return 1;
+    if (have_prev) {
+      double err = 0.0;
+      for (int i = 0; i < 16; ++i) err = std::max(err, std::fabs(cur[i] - prev[i]));
+      if (err < 1e-13) {
+        fill(cur, tau, out);
+        out->nodes = N;
+        out->method = 0;
+        out->quad_err_est = err;
+        return 0;
+      }
+    }
+    std::memcpy(prev, cur, sizeof(cur));
+    have_prev = true;
+  }
+  // Gauss–Hermite did not converge (large τ for tanh: poles at ±iπ/(2√τ)) → composite trapezoid,
+  // geometrically convergent for integrands analytic in a strip.
+  double coarse[16];
+  if (!trapezoid_table(act, tau, 0.05, cur)) return 1;
+  if (!trapezoid_table(act, tau, 0.1, coarse)) return 1;
+  double err = 0.0;
+  for (int i = 0; i < 16; ++i) err = std::max(err, std::fabs(cur[i] - coarse[i]));
+  fill(cur, tau, out);
+  out->nodes = 1601;
+  out->method = 1;
+  out->quad_err_est = err;
+  return 0;
+}
+
+}  // namespace rfh

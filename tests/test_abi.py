@@ -1,0 +1,139 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/rf.h declares, its
+host-only entry points (rf_moments, rf_phi_row_split, workspace sizing) are right, and argument
+validation rejects bad calls before touching a device.  No GPU compute here."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2110_01899_b200 as rf
+from paper_2110_01899_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "rf.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rf_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = rf.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 12
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.SYMBOLS)
+    assert "sm_100a" in rf.rf_version()
+
+
+def test_library_has_tcgen05_and_tma_sass():
+    """The shipped .so carries sm_100a tcgen05 MMAs, TMEM loads and TMA loads (SASS names)."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in out and "LDTM" in out and "UTMALDG" in out
+
+
+@pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
+@pytest.mark.parametrize("tau", [0.5, 1.0, 1.0133, 1.0833, 2.0])
+def test_rf_moments_matches_oracle(act, tau):
+    """Library Golub–Welsch quadrature vs the oracle's independent Newton-based rule."""
+    got = rf.rf_moments(act, tau)
+    ref = oracle.moments(act, tau, 512)
+    kd = np.array(got["kd"])
+    assert np.max(np.abs(kd - ref["kd"])) < 5e-13
+    for key in ("e_sigma_sq", "d0", "d1", "d2"):
+        assert abs(got[key] - ref[key]) < 5e-13, key
+    assert got["quad_err_est"] < 1e-13
+
+
+def test_rf_moments_fixed_nodes_and_large_tau_fallback():
+    m = rf.rf_moments("erf", 1.0, nodes=64)
+    assert m["nodes"] == 64
+    c = 2 / math.sqrt(math.pi)
+    assert abs(m["kd"][0][1] - c / math.sqrt(3.0)) < 1e-14
+    big = rf.rf_moments("tanh", 16.0)            # GH cannot reach 1e-13 here → trapezoid
+    tr = oracle.moments_trapezoid("tanh", 16.0)
+    assert np.max(np.abs(np.array(big["kd"]) - tr) / np.maximum(1.0, np.abs(tr))) < 1e-12
+
+
+def test_rf_moments_errors():
+    with pytest.raises(rf.RFError) as e:
+        rf.rf_moments("tanh", -1.0)
+    assert e.value.status == _lib.RF_E_INVALID
+    with pytest.raises(rf.RFError):
+        rf.rf_moments("tanh", float("nan"))
+    with pytest.raises(rf.RFError):
+        rf.rf_moments("tanh", 1.0, nodes=1)
+
+
+def test_phi_row_split_covers_and_balances():
+    for n in (256, 1000, 131072):
+        for world in (1, 2, 3, 8):
+            ranges = [rf.rf_phi_row_split(n, world, r) for r in range(world)]
+            assert ranges[0][0] == 0 and ranges[-1][1] == n
+            for (b0, e0), (b1, e1) in zip(ranges, ranges[1:]):
+                assert e0 == b1
+            for b, e in ranges:
+                assert b % 128 == 0 and (e == n or e % 128 == 0)
+            if n >= 128 * 8 * world:
+                area = [sum(n - i for i in range(b, e)) for b, e in ranges]
+                assert max(area) / min(area) < 1.05
+
+
+def test_workspace_sizes():
+    assert rf.rf_gram_workspace_size(784, 4096, 8192, "bf16") >= 4096 * 8192 * 2
+    assert rf.rf_gram_workspace_size(784, 4096, 8192, "3xtf32") >= 2 * 4096 * 8192 * 4
+    assert rf.rf_phi_workspace_size(512, 131072, "bf16") >= 131072 * 8
+
+
+def test_validation_rejects_before_any_launch():
+    lib = rf.load()
+    g = lib.rf_gram(None, 64, None, 64, 64, 256, 512, 512, 0, 4, 0, None, 256, None, 0, None)
+    assert g == _lib.RF_E_INVALID
+    assert b"NULL" in lib.rf_last_error()
+    buf = (ctypes.c_char * 4096)()
+    addr = ctypes.addressof(buf)
+    addr16 = (addr + 15) // 16 * 16
+    # p = 100 bf16 with ldx = 100 → 200 B rows, not a multiple of 16 B (TMA stride rule)
+    s = lib.rf_gram(ctypes.c_void_p(addr16), 100, ctypes.c_void_p(addr16), 104, 100, 8, 8, 8, 0, 4, 0,
+                    ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"16 B" in lib.rf_last_error()
+    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 4, 0, 4, 0,
+                    ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"m_total" in lib.rf_last_error()
+    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 7, 4, 0,
+                    ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"activation" in lib.rf_last_error()
+    # workspace too small
+    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 0, 4, 0,
+                    ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
+    assert s == _lib.RF_E_WORKSPACE
+    # Φ row range must start on a 128-row boundary
+    s = lib.rf_phi_closed_form(ctypes.c_void_p(addr16), 64, 64, 256, 0, 1.0, None, 4, 0, 64, 256,
+                               ctypes.c_void_p(addr16), 256, ctypes.c_void_p(addr16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"row range" in lib.rf_last_error()
+
+
+def test_no_cpu_fallback_without_gpu():
+    """On a host with no usable sm_100 device a well-formed call fails loudly (never computes on CPU)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = rf.load()
+    assert lib.rf_device_supported(0) == 0
+    size = rf.rf_phi_workspace_size(64, 256, "bf16")
+    ws = (ctypes.c_char * (size + 512))()
+    wsa = (ctypes.addressof(ws) + 255) // 256 * 256
+    x = (ctypes.c_char * (256 * 64 * 2 + 64))()
+    xa = (ctypes.addressof(x) + 15) // 16 * 16
+    out = (ctypes.c_char * (256 * 256 * 4 + 64))()
+    oa = (ctypes.addressof(out) + 15) // 16 * 16
+    s = lib.rf_phi_closed_form(ctypes.c_void_p(xa), 64, 64, 256, 0, 1.0, None, 4, 0, 0, 256,
+                               ctypes.c_void_p(oa), 256, ctypes.c_void_p(wsa), size, None)
+    assert s in (_lib.RF_E_CUDA, _lib.RF_E_UNSUPPORTED)

@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative Frobenius ≤ 1e-5 in fp32-accurate modes (FP32, 3×TF32)
+and ≤ 2e-3 in BF16 mode; 1×TF32 is in the 2e-3 class; FP64 mode ≤ 1e-12.  The oracle always consumes
+exactly the (rounded) tensors the GPU reads, upcast to fp64 (DESIGN.md §4 R11).  Max-abs errors are
+printed for the diagonal and the off-diagonal separately.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import paper_2110_01899_b200 as rf  # noqa: E402
+import synthetic  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp64": 1e-12, "fp32": 1e-5, "3xtf32": 1e-5, "tf32": 2e-3, "bf16": 2e-3}
+DT = {"fp64": torch.float64, "fp32": torch.float32, "3xtf32": torch.float32, "tf32": torch.float32,
+      "bf16": torch.bfloat16}
+SENTINEL = -7.25
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    assert rf.rf_device_supported(0), "device 0 is not sm_100"
+    torch.cuda.set_device(0)
+    yield
+
+
+def dev(a, prec):
+    return torch.tensor(np.ascontiguousarray(a), device="cuda").to(DT[prec])
+
+
+def back(t):
+    return t.double().cpu().numpy()
+
+
+def rel_fro(got, ref):
+    return float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+
+
+def report(name, got, ref, I, J):
+    d = I == J
+    err = np.abs(got - ref)
+    md = float(err[d].max()) if d.any() else 0.0
+    mo = float(err[~d].max()) if (~d).any() else 0.0
+    r = rel_fro(got, ref)
+    print(f"[parity] {name}: rel-Frobenius {r:.3e}  max-abs diag {md:.3e}  off-diag {mo:.3e}")
+    return r
+
+
+def upper_idx(n):
+    return np.triu_indices(n)
+
+
+# ------------------------------------------------------------------------------------------------ G
+def _gram_case(n, p, m, act, prec, out="upper", seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, p)) / math.sqrt(p)
+    W = rng.standard_normal((m, p))
+    Xd, Wd = dev(X, prec), dev(W, prec)
+    G = torch.full((n, n), SENTINEL, dtype=torch.float64 if prec == "fp64" else torch.float32, device="cuda")
+    rf.rf_gram(Xd, Wd, act=act, prec=prec, out=out, G=G)
+    torch.cuda.synchronize()
+    ref = oracle.gram(back(Xd), back(Wd), act)
+    Gc = back(G)
+    I, J = upper_idx(n)
+    r = report(f"G n={n} p={p} m={m} {act} {prec} {out}", Gc[I, J], ref[I, J], I, J)
+    assert r <= TOL[prec]
+    L = np.tril_indices(n, -1)
+    if out == "upper":
+        assert np.all(Gc[L] == SENTINEL), "UPPER mode wrote below the diagonal"
+    else:
+        assert rel_fro(Gc, ref) <= TOL[prec]
+        assert np.array_equal(Gc, Gc.T)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "3xtf32", "tf32", "bf16"])
+@pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
+def test_gram_small_ragged(prec, act):
+    # n=200: one partial 128-row tile + one partial 256-col tile; m=300: ragged K for the SYRK;
+    # p=72: ragged K for the feature GEMM (72 = 64 + 8 bf16).
+    _gram_case(200, 72, 300, act, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "tf32", "bf16"])
+def test_gram_multi_tile_full(prec):
+    _gram_case(1000, 200, 700, "tanh", prec, out="full", seed=1)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "3xtf32", "bf16"])
+def test_gram_degenerate_sizes(prec):
+    _gram_case(1, 8, 1, "erf", prec, out="full", seed=2)    # n = m = 1
+    _gram_case(129, 8, 1, "tanh", prec, seed=3)             # rank-one G, tile edge + 1
+    _gram_case(256, 8, 512, "tanh", prec, seed=4)           # exact tile multiples
+
+
+def test_gram_sharded_partials_sum_to_full():
+    """Data parallel over m (north star (4)): Σ_r rf_gram(W_r, m_total) == rf_gram(W)."""
+    rng = np.random.default_rng(5)
+    n, p, m = 300, 64, 768
+    X = dev(rng.standard_normal((n, p)) / 8, "bf16")
+    W = dev(rng.standard_normal((m, p)), "bf16")
+    full = rf.rf_gram(X, W, act="sigmoid_half", prec="bf16", out="upper")
+    parts = [rf.rf_gram(X, W[r * 256:(r + 1) * 256].contiguous(), act="sigmoid_half", prec="bf16", out="upper",
+                        m_total=m) for r in range(3)]
+    torch.cuda.synchronize()
+    s = sum(back(g) for g in parts)
+    I, J = upper_idx(n)
+    assert np.max(np.abs(s[I, J] - back(full)[I, J])) < 1e-6
+
+
+def test_gram_zero_size_rejected():
+    X = torch.zeros((0, 8), dtype=torch.bfloat16, device="cuda")
+    W = torch.zeros((4, 8), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(rf.RFError):
+        rf.rf_gram(X, W, prec="bf16", G=torch.zeros((1, 4), device="cuda"))
+
+
+# ------------------------------------------------------------------------------------------------ Φ
+def _phi_case(X, act, prec, tau=0.0, out="upper", rows=None):
+    n = X.shape[0]
+    Xd = dev(X, prec)
+    Phi = torch.full((n, n), SENTINEL, dtype=torch.float64 if prec == "fp64" else torch.float32, device="cuda")
+    if rows is None:
+        rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, Phi=Phi)
+    else:
+        for b, e in rows:
+            rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, row_begin=b, row_end=e, Phi=Phi)
+    torch.cuda.synchronize()
+    Xo = back(Xd)
+    ref = oracle.phi_eq1(Xo, act, tau if tau > 0 else None)
+    Pc = back(Phi)
+    I, J = upper_idx(n)
+    r = report(f"Phi n={n} p={X.shape[1]} {act} {prec} {out}", Pc[I, J], ref[I, J], I, J)
+    tol = {"fp64": 1e-12, "fp32": 1e-5, "3xtf32": 1e-5, "tf32": 2e-3, "bf16": 1e-5}[prec]
+    assert r <= tol
+    L = np.tril_indices(n, -1)
+    if out == "upper":
+        assert np.all(Pc[L] == SENTINEL)
+    else:
+        assert np.array_equal(Pc, Pc.T)
+    return Pc, ref
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "3xtf32", "tf32", "bf16"])
+@pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
+def test_phi_small_ragged(prec, act):
+    X = synthetic.make_X(4, n=300, p=72)        # unit-scaled rows with norms in [0.5, 1.5]
+    _phi_case(X, act, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32", "bf16"])
+def test_phi_multi_tile_given_tau_full(prec):
+    X = synthetic.make_X(1, n=1100, p=200)
+    _phi_case(X, "erf", prec, tau=1.05, out="full")
+
+
+def test_phi_row_blocks_assemble_to_full():
+    X = synthetic.make_X(4, n=1000, p=64)
+    ranges = [rf.rf_phi_row_split(1000, 3, r) for r in range(3)]
+    _phi_case(X, "tanh", "bf16", rows=ranges)
+
+
+def test_phi_diagonal_rule_and_zero_norm():
+    X = synthetic.make_X(0, n=256, p=64)
+    Pc, ref = _phi_case(X, "tanh", "fp32")
+    d = np.arange(256)
+    assert np.max(np.abs(Pc[d, d] - ref[d, d])) < 1e-6
+    Xz = X.copy()
+    Xz[5] = 0.0
+    with pytest.raises(rf.RFError):
+        rf.rf_phi_closed_form(dev(Xz, "bf16"), act="tanh", tau=0.0, prec="bf16")
+
+
+def test_estimate_tau_lemma1():
+    X = synthetic.make_X(2, n=4096, p=3072)
+    for prec in ("fp64", "fp32", "bf16"):
+        Xd = dev(X, prec)
+        t = rf.rf_estimate_tau(Xd)
+        assert abs(t - oracle.tau_hat(back(Xd))) < 1e-12 * t
+
+
+# ------------------------------------------------------------------------------------------------ configs
+def _sampled_gram(cfg_idx, prec, count, stride):
+    cfg = synthetic.CONFIGS[cfg_idx]
+    X = synthetic.make_X(cfg)
+    W = synthetic.make_W(cfg)
+    Xd, Wd = dev(X, prec), dev(W, prec)
+    del X, W
+    G = rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="upper")
+    torch.cuda.synchronize()
+    S = synthetic.sample_indices(cfg.n, count=count, tile_stride=stride)
+    St = torch.tensor(S, device="cuda")
+    sub = back(G.index_select(0, St).index_select(1, St))
+    del G
+    Xs = back(Xd.index_select(0, St))
+    Wo = back(Wd)
+    ref = oracle.gram(Xs, Wo, cfg.act)
+    I, J = upper_idx(len(S))
+    r = report(f"G configs[{cfg_idx}] {prec} sampled |S|={len(S)}", sub[I, J], ref[I, J], S[I], S[J])
+    assert r <= TOL[prec]
+
+
+def _sampled_phi(cfg_idx, prec, count, stride):
+    cfg = synthetic.CONFIGS[cfg_idx]
+    X = synthetic.make_X(cfg)
+    Xd = dev(X, prec)
+    tau_ref = oracle.tau_hat(back(Xd))
+    Phi = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="upper")
+    torch.cuda.synchronize()
+    S = synthetic.sample_indices(cfg.n, count=count, tile_stride=stride)
+    St = torch.tensor(S, device="cuda")
+    sub = back(Phi.index_select(0, St).index_select(1, St))
+    del Phi
+    ref = oracle.phi_eq1(back(Xd.index_select(0, St)), cfg.act, tau_ref)
+    I, J = upper_idx(len(S))
+    tol = {"fp32": 1e-5, "3xtf32": 1e-5, "tf32": 2e-3, "bf16": 1e-5}[prec]
+    r = report(f"Phi configs[{cfg_idx}] {prec} sampled |S|={len(S)}", sub[I, J], ref[I, J], S[I], S[J])
+    assert r <= tol
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32", "3xtf32", "tf32", "bf16"])
+def test_config0_tiny_full(prec):
+    cfg = synthetic.CONFIGS[0]
+    X = synthetic.make_X(cfg)
+    W = synthetic.make_W(cfg)
+    Xd, Wd = dev(X, prec), dev(W, prec)
+    G = rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="full")
+    torch.cuda.synchronize()
+    ref = oracle.gram(back(Xd), back(Wd), cfg.act)
+    I, J = upper_idx(cfg.n)
+    assert report(f"G configs[0] {prec}", back(G)[I, J], ref[I, J], I, J) <= TOL[prec]
+    _phi_case(X, cfg.act, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "3xtf32"])
+def test_config1_full_size(prec):
+    _sampled_gram(1, prec, count=512, stride=256)
+    _sampled_phi(1, prec, count=1024, stride=128)
+
+
+def test_config2_full_size_bf16():
+    _sampled_gram(2, "bf16", count=512, stride=512)
+    _sampled_phi(2, "bf16", count=512, stride=512)
+
+
+def test_config3_full_size_bf16():
+    _sampled_gram(3, "bf16", count=256, stride=2048)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "3xtf32"])
+def test_config4_full_size_phi(prec):
+    _sampled_phi(4, prec, count=1024, stride=1024)
