@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one step = the whole path of SURVEY.md §8(a) over one batch:
+  G  : [K2 split] → K3 Σᵀ = σ(X Wᵀ) → K4 upper-triangular SYRK G = ΣᵀΣ/m → (N>1) reduce-scatter of G
+  Φ  : K1 row norms + Lemma-1 τ̂ (one 8-byte D2H) → Gauss–Hermite moments (host) → per-row
+       coefficients → K5 fused XᵀX + EQ1 epilogue over the rank's upper-triangle rows.
+
+Default workload: BASELINE.json configs[3] (p=1024, n=65536, m=65536, σ = sigmoid − ½, BF16) — the
+config the metric's "1/2/4/8 B200" scaling is quoted on — with Φ evaluated on the same X.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config i --prec bf16|3xtf32|tf32|fp32]
+  python bench.py --impl reference ...   (the fp64 CPU oracle as the reference arm)
+
+Prints ONE JSON line on rank 0.  Timing: W untimed warm-ups, then K steps bracketed by barrier +
+synchronize, CUDA events on the launching stream, max over ranks.  Inputs + workspaces are far larger
+than the 126 MB L2 (no flush needed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gram TFLOP/s and kernel entries/s at 1/2/4/8 B200; % of tensor-core peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--prec", default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-phi", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: float(m[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    return p
+
+
+def cores_used():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------------ oracle arm
+def oracle_sample(cfg, size, seed=0):
+    """Time the fp64 oracle on a principal sample S (|S| = size) of the workload: G_SS (needs σ(W x_i) for
+    all m features, i ∈ S) and Φ_SS.  Returns (seconds, algorithmic flops of the sample)."""
+    import numpy as np
+    import oracle
+    import synthetic
+    rng = np.random.default_rng(seed)
+    S = np.sort(rng.choice(cfg.n, size=size, replace=False))
+    Xs = synthetic.make_X(cfg, rows=S)
+    W = synthetic.make_W(cfg) if cfg.m else None
+    t0 = time.perf_counter()
+    flops = 0.0
+    if cfg.m:
+        oracle.gram(Xs, W, cfg.act)
+        flops += 2.0 * cfg.m * size * cfg.p + cfg.m * size * (size + 1.0)
+    oracle.phi_eq1(Xs, cfg.act, oracle.tau_hat(Xs))
+    flops += cfg.p * size * (size + 1.0)
+    return time.perf_counter() - t0, flops
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synthetic
+    cfg = synthetic.CONFIGS[args.config]
+    size = 512
+    for _ in range(max(args.warmup, 0)):
+        oracle_sample(cfg, 128)
+    tot_t, tot_f = 0.0, 0.0
+    for k in range(args.steps):
+        t, f = oracle_sample(cfg, size, seed=k)
+        tot_t += t
+        tot_f += f
+    v = tot_f / tot_t / 1e12
+    sample = (f"|S|={size} random rows of configs[{args.config}] per step: G_SS (σ(W x_i) over all m) + Φ_SS, "
+              f"fp64 NumPy")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE.json configs)",
+            "config": {"workload": f"configs[{args.config}] {cfg.name} (oracle sample)"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ our arm
+class ClockSampler:
+    def __init__(self, gpus):
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rf_clocks_{os.getpid()}.csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(str(g) for g in gpus),
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    s, m = float(f[1]), float(f[2])
+                except ValueError:
+                    continue
+                sm.append(s)
+                mx.append(m)
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        except Exception:
+            return None
+        if not sm:
+            return None
+        sm.sort()
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_01899_b200 as rf
+    import synthetic
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torch.distributed.run")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    assert rf.rf_device_supported(local), "not an sm_100 device"
+
+    cfg = synthetic.CONFIGS[args.config]
+    prec = args.prec or cfg.modes[0]
+    tdt = {"bf16": torch.bfloat16, "fp32": torch.float32, "3xtf32": torch.float32, "tf32": torch.float32,
+           "fp64": torch.float64}[prec]
+    do_gram = cfg.gram
+    do_phi = (not args.no_phi)
+    n, p, m = cfg.n, cfg.p, cfg.m
+    stream = torch.cuda.current_stream()
+
+    # ---------------- inputs (host → pinned → device); W sharded over m (rank r owns rows [m0, m1))
+    X_host = torch.from_numpy(synthetic.make_X(cfg)).to(tdt).pin_memory()
+    Xd = X_host.to(device)
+    if do_gram:
+        if m % world:
+            raise SystemExit("m must be divisible by the number of GPUs")
+        m_local = m // world
+        m0 = rank * m_local
+        W_host = torch.from_numpy(synthetic.make_W(cfg, rows=np.arange(m0, m0 + m_local))).to(tdt).pin_memory()
+        Wd = W_host.to(device)
+        if n % world:
+            raise SystemExit("n must be divisible by the number of GPUs for the G reduce-scatter")
+        G = torch.empty((n, n), dtype=torch.float32, device=device)
+        ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
+        G_own = torch.empty((n // world, n), dtype=torch.float32, device=device) if world > 1 else G
+    if do_phi:
+        rb, re_ = rf.rf_phi_row_split(n, world, rank)
+        Phi = torch.empty((n, n), dtype=torch.float32, device=device)
+        ws_p = torch.empty(rf.rf_phi_workspace_size(p, n, prec), dtype=torch.uint8, device=device)
+    launches = [0]
+
+    def step():
+        if do_gram:
+            rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="upper", m_total=m, G=G, ws=ws_g)
+            launches[0] += rf.rf_last_launch_count()
+            if world > 1:
+                dist.reduce_scatter_tensor(G_own, G, op=dist.ReduceOp.SUM)
+        if do_phi:
+            rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="upper", row_begin=rb, row_end=re_,
+                                  Phi=Phi, ws=ws_p)
+            launches[0] += rf.rf_last_launch_count()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(list(range(world))) if rank == 0 else None
+    time.sleep(0.3 if clocks else 0)
+    rf.rf_profile_read()          # drop warm-up records
+    rf.rf_profile_enable(True)
+    launches[0] = 0
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    rf.rf_profile_enable(False)
+    recs = rf.rf_profile_read()
+    clk = clocks.stop() if clocks else None
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # ---------------- algorithmic work of one step (whole job)
+    g_flops = (2.0 * m * n * p + m * n * (n + 1.0)) if do_gram else 0.0
+    phi_flops = p * n * (n + 1.0) if do_phi else 0.0
+    tri = n * (n + 1) / 2.0
+    value = (g_flops + phi_flops) / (ms_step * 1e-3) / 1e12
+    entries = ((tri if do_gram else 0) + (tri if do_phi else 0)) / (ms_step * 1e-3)
+
+    # ---------------- per-kernel device times (rank-local launches)
+    pk = peaks()
+    kstat = {}
+    for name, t in recs:
+        s = kstat.setdefault(name, [0, 0.0])
+        s[0] += 1
+        s[1] += t
+    rows_local = (re_ - rb) if do_phi else 0
+    phi_entries_local = (sum(n - i for i in range(rb, re_)) if do_phi else 0)
+    per_launch_alg = {
+        "K3_gemm_sigma": ("tensor", 2.0 * (m // world if do_gram else 0) * n * p),
+        "K4_syrk": ("tensor", (m // world if do_gram else 0) * n * (n + 1.0)),
+        "K5_xtx_eq1": ("tensor", 2.0 * p * phi_entries_local),
+    }
+    tf32_like = prec in ("tf32", "3xtf32")
+    peak_tensor = pk["bf16_tflops_sustained"] * (0.5 if tf32_like else 1.0)
+    kernels = {}
+    for name, (cnt, tot) in kstat.items():
+        avg = tot / cnt
+        d = {"launches": cnt, "avg_ms": avg, "share_of_step": tot / ms}
+        if name in per_launch_alg:
+            kind, fl = per_launch_alg[name]
+            d["achieved_tflops"] = fl / (avg * 1e-3) / 1e12
+            d["frac_of_tensor_peak"] = d["achieved_tflops"] / peak_tensor
+        if name == "K5_xtx_eq1":
+            by = 4.0 * phi_entries_local + (2 if prec == "bf16" else 4) * n * p
+            d["achieved_hbm_gbs"] = by / (avg * 1e-3) / 1e9
+            d["frac_of_hbm_peak"] = d["achieved_hbm_gbs"] / pk["hbm_gbs"]
+        kernels[name] = d
+    dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"]) if kernels else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(f"configs[{args.config}]:{prec}:{dom}")
+    except Exception:
+        pass
+    roof = None
+    if dom in per_launch_alg:
+        d = kernels[dom]
+        roof = {"bound": "tensor", "kernel": dom, "achieved": d["achieved_tflops"], "peak": peak_tensor,
+                "unit": "TFLOP/s", "frac": d["achieved_tflops"] / peak_tensor, "traffic": traffic,
+                "peak_source": pk["source"] + (" sustained bf16" + (" × 0.5 (tf32 nominal ratio)" if tf32_like else "")),
+                "frac_of_burst_peak": d["achieved_tflops"] / (pk["bf16_tflops"] * (0.5 if tf32_like else 1.0))}
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = X_host.numel() * X_host.element_size() + ((W_host.numel() * W_host.element_size()) if do_gram else 0)
+        outs = []
+        if do_gram:
+            outs.append(torch.empty(G_own.shape, dtype=torch.float32, pin_memory=True))
+        if do_phi:
+            outs.append(torch.empty((re_ - rb, n), dtype=torch.float32, pin_memory=True))
+        d2h = sum(o.numel() * 4 for o in outs)
+
+        def e2e_step():
+            Xd.copy_(X_host, non_blocking=True)
+            if do_gram:
+                Wd.copy_(W_host, non_blocking=True)
+            step()
+            k = 0
+            if do_gram:
+                outs[k].copy_(G_own, non_blocking=True)
+                k += 1
+            if do_phi:
+                outs[k].copy_(Phi[rb:re_], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = ea.elapsed_time(eb)
+        if world > 1:
+            t = torch.tensor([ems], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": (g_flops + phi_flops) / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": ems / args.steps}
+
+    # ---------------- CPU baseline (oracle, rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        size = 1024
+        t, f = oracle_sample(cfg, size)
+        cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
+               "sample": f"|S|={size} random rows of configs[{args.config}]: G_SS (σ(W x_i) over all m={m}) + "
+                         f"Φ_SS by the 18-term EQ1, fp64 NumPy, {t:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": prec if prec != "3xtf32" else "f32(3xtf32)",
+            "data": "synthetic (seeded PCG64 draws of BASELINE.json configs; no dataset)",
+            "config": {"workload": f"configs[{args.config}] {cfg.name}" + (" + Φ on the same X" if do_phi and do_gram else ""),
+                       "p": p, "n": n, "m": m, "act": cfg.act, "prec": prec,
+                       "parallelism": (f"G: W sharded over m ({world} ranks) + NCCL reduce-scatter of G rows; "
+                                       f"Φ: row blocks, no collective") if world > 1 else "single GPU",
+                       "l2": "no flush: inputs/workspace/outputs per step ≫ 126 MB L2"},
+            "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches[0], "clocks": clk, "peaks": pk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

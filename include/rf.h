@@ -111,7 +111,8 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
  *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode).
  * Pipeline: [3XTF32: K2 split X, W] → K3 fused Σᵀ = σ(X·Wᵀ) (tcgen05 GEMM, σ in the epilogue)
  *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 128×256 tiles with j ≥ i.
- * Alignment: X, W, G, ws 16-B aligned; ldx·esize, ldw·esize, ldg·esize multiples of 16 B (TMA).
+ * Alignment: X, W 16-B aligned with ldx·esize, ldw·esize multiples of 16 B (TMA); G aligned to its element
+ *            size, any ldg ≥ n (16-B vector stores are used where rows allow); ws 256-B aligned.
  */
 rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec prec, size_t* bytes);
 rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
@@ -153,6 +154,14 @@ rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_
 /* Number of kernel launches the last successful rf_gram / rf_phi_closed_form call on this thread
  * enqueued (for bench accounting). */
 int32_t rf_last_launch_count(void);
+
+/* Launch tracing.  rf_profile_enable(1): from now on every kernel launch of this library is bracketed by
+ * two CUDA events recorded on the launching stream (negligible cost; process-wide switch).
+ * rf_profile_read: waits for the recorded events, writes up to max_records entries — names[32*k] is a
+ * NUL-terminated kernel name (e.g. "K4_syrk"), ms[k] its device duration — sets *count to the number of
+ * records taken (may exceed max_records; the excess is dropped) and clears the record list. */
+rf_status rf_profile_enable(int on);
+rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* count);
 
 #ifdef __cplusplus
 }

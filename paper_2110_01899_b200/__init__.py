@@ -147,6 +147,22 @@ def rf_phi_closed_form(X, act: str = "tanh", tau: float = 0.0, mom: Optional[dic
     return Phi
 
 
+def rf_profile_enable(on: bool = True) -> None:
+    _lib.check(load().rf_profile_enable(1 if on else 0))
+
+
+def rf_profile_read(max_records: int = 4096):
+    """[(kernel name, device ms)] of the launches recorded since the last read (waits for them)."""
+    lib = load()
+    names = ctypes.create_string_buffer(32 * max_records)
+    ms = (ctypes.c_float * max_records)()
+    cnt = ctypes.c_int32()
+    _lib.check(lib.rf_profile_read(max_records, names, ms, ctypes.byref(cnt)))
+    k = min(cnt.value, max_records)
+    raw = names.raw
+    return [(raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(k)]
+
+
 def rf_phi_row_split(n: int, world: int, rank: int) -> Tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
     _lib.check(load().rf_phi_row_split(n, world, rank, ctypes.byref(b), ctypes.byref(e)))

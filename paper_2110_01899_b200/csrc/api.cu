@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/rf.h"
 #include "k_aux.cuh"
@@ -46,6 +47,50 @@ rf_status ok() {
     if (_e != cudaSuccess) return fail(RF_E_CUDA, "%s: %s (%s)", #expr, cudaGetErrorName(_e),   \
                                        cudaGetErrorString(_e));                                 \
   } while (0)
+
+// ---------------------------------------------------------------- launch tracing (rf_profile_*)
+// When enabled, every kernel launch is bracketed by two CUDA events recorded on its stream; the
+// records are read back (and the events recycled) by rf_profile_read.
+struct ProfRec {
+  char name[32];
+  cudaEvent_t a, b;
+};
+std::mutex g_pmu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t pool_get() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  bool on = false;
+  ProfRec r{};
+  cudaStream_t st;
+  ProfScope(const char* name, cudaStream_t s) : st(s) {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    if (!g_prof_on) return;
+    on = true;
+    std::snprintf(r.name, sizeof(r.name), "%s", name);
+    r.a = pool_get();
+    r.b = pool_get();
+    cudaEventRecord(r.a, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(r.b, st);
+    std::lock_guard<std::mutex> lk(g_pmu);
+    g_recs.push_back(r);
+  }
+};
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 inline size_t align256(size_t a) { return (a + 255) & ~size_t(255); }
@@ -141,9 +186,10 @@ rf_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t rows, in
 }
 
 template <class Cfg, class Epi>
-rf_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo, const CUtensorMap& blo,
-                    const rfk::Sched& s, int num_kb, const Epi& epi, int sms, cudaStream_t st) {
+rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo,
+                    const CUtensorMap& blo, const rfk::Sched& s, int num_kb, const Epi& epi, int sms, cudaStream_t st) {
   if (s.num_tiles <= 0) return RF_OK;
+  ProfScope ps(name, st);
   auto kern = rfk::tc_gemm_kernel<Cfg, Epi>;
   RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES));
   const int grid = std::min(s.num_tiles, sms);
@@ -154,10 +200,11 @@ rf_status launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMa
 }
 
 template <typename T, class Epi>
-rf_status launch_simt(const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N, int64_t K, int tri,
-                      int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st) {
+rf_status launch_simt(const char* name, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N,
+                      int64_t K, int tri, int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st) {
   const int tn = (int)((N + 63) / 64);
   if (row_tile1 <= row_tile0 || tn == 0) return RF_OK;
+  ProfScope ps(name, st);
   dim3 grid(tn, row_tile1 - row_tile0);
   rfk::simt_gemm_nt<T, Epi><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, tri, row_tile0, epi);
   RF_CUDA_CHECK(cudaGetLastError());
@@ -170,6 +217,7 @@ rf_status launch_split(const float* src, int64_t lds, int64_t rows, int64_t cols
   const int64_t total = rows * cols;
   int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
   if (grid < 1) grid = 1;
+  ProfScope ps("K2_split_tf32", st);
   rfk::k_split_tf32<<<grid, 256, 0, st>>>(src, lds, rows, cols, hi, lo, ldd);
   RF_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
@@ -179,6 +227,7 @@ rf_status launch_split(const float* src, int64_t lds, int64_t rows, int64_t cols
 rf_status launch_rownorm(const void* X, rf_prec prec, int64_t ldx, int64_t p, int64_t n, double* nrm2,
                          cudaStream_t st) {
   const int grid = (int)((n + 7) / 8);
+  ProfScope ps("K1_rownorm", st);
   if (prec == RF_PREC_FP64)
     rfk::k_rownorm<double><<<grid, 256, 0, st>>>((const double*)X, ldx, p, n, nrm2);
   else if (prec == RF_PREC_BF16)
@@ -235,6 +284,13 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   return g;
 }
 
+rf_status validate_output(const char* name, const void* ptr, int64_t ld, int64_t cols, size_t es) {
+  if (!ptr) return fail(RF_E_INVALID, "%s is NULL", name);
+  if ((reinterpret_cast<uintptr_t>(ptr) % es) != 0) return fail(RF_E_INVALID, "%s is not %zu-byte aligned", name, es);
+  if (ld < cols) return fail(RF_E_INVALID, "ld of %s (%lld) < %lld", name, (long long)ld, (long long)cols);
+  return RF_OK;
+}
+
 rf_status validate_matrix(const char* name, const void* ptr, int64_t ld, int64_t cols, size_t es) {
   if (!ptr) return fail(RF_E_INVALID, "%s is NULL", name);
   if (!aligned16(ptr)) return fail(RF_E_INVALID, "%s is not 16-byte aligned", name);
@@ -253,6 +309,43 @@ extern "C" {
 const char* rf_last_error(void) { return g_err.c_str(); }
 const char* rf_version(void) { return "rf_b200 0.1 (sm_100a: tcgen05/TMA/TMEM; SIMT fp32/fp64)"; }
 int32_t rf_last_launch_count(void) { return g_launches; }
+
+rf_status rf_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_pmu);
+  g_prof_on = on != 0;
+  return ok();
+}
+
+rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* count) {
+  if (!count || (max_records > 0 && (!names || !ms))) return fail(RF_E_INVALID, "rf_profile_read: NULL output");
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    recs.swap(g_recs);
+  }
+  int32_t k = 0;
+  rf_status st = RF_OK;
+  for (auto& r : recs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess && st == RF_OK) st = fail(RF_E_CUDA, "rf_profile_read: %s", cudaGetErrorString(e));
+    if (k < max_records) {
+      std::snprintf(names + 32 * k, 32, "%s", r.name);
+      ms[k] = t;
+    }
+    ++k;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    for (auto& r : recs) {
+      g_pool.push_back(r.a);
+      g_pool.push_back(r.b);
+    }
+  }
+  *count = k;
+  return st == RF_OK ? ok() : st;
+}
 
 int rf_device_supported(int device) {
   int n = 0;
@@ -300,7 +393,10 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
   double* nrm2 = (double*)ws;
   double* out = (double*)((char*)ws + align256((size_t)n * 8));
   if ((s = launch_rownorm(X, pr, ldx, p, n, nrm2, st))) return s;
-  rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, out);
+  {
+    ProfScope ps("K1_tau_reduce", st);
+    rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, out);
+  }
   RF_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
   double h[2];
@@ -334,7 +430,7 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
   rf_status s;
   if ((s = validate_matrix("X", X, ldx, p, es))) return s;
   if ((s = validate_matrix("W", W, ldw, p, es))) return s;
-  if ((s = validate_matrix("G", G, ldg, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  if ((s = validate_output("G", G, ldg, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
   const GramPlan pl = gram_plan(p, n, m_local, prec);
   if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(RF_E_WORKSPACE, "rf_gram: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total, ws_bytes);
@@ -350,20 +446,20 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
     if (prec == RF_PREC_FP64) {
       double* S = (double*)(w + pl.off_s0);
       rfk::SimtSigma<double> e1{S, pl.ldS, n, m_local, (int)act};
-      if ((s = launch_simt<double>((const double*)X, ldx, (const double*)W, ldw, n, m_local, p, 0, 0,
+      if ((s = launch_simt<double>("K6_simt_gemm_sigma", (const double*)X, ldx, (const double*)W, ldw, n, m_local, p, 0, 0,
                                    (int)((n + 63) / 64), e1, st)))
         return s;
       rfk::SimtSyrk<double> e2{(double*)G, ldg, n, 1.0 / (double)m_total, full};
-      if ((s = launch_simt<double>(S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+      if ((s = launch_simt<double>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
         return s;
     } else {
       float* S = (float*)(w + pl.off_s0);
       rfk::SimtSigma<float> e1{S, pl.ldS, n, m_local, (int)act};
-      if ((s = launch_simt<float>((const float*)X, ldx, (const float*)W, ldw, n, m_local, p, 0, 0,
+      if ((s = launch_simt<float>("K6_simt_gemm_sigma", (const float*)X, ldx, (const float*)W, ldw, n, m_local, p, 0, 0,
                                   (int)((n + 63) / 64), e1, st)))
         return s;
       rfk::SimtSyrk<float> e2{(float*)G, ldg, n, (float)(1.0 / (double)m_total), full};
-      if ((s = launch_simt<float>(S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+      if ((s = launch_simt<float>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
         return s;
     }
     return ok();
@@ -379,20 +475,20 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
     if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
     if ((s = make_tmap(&tB, W, true, m_local, p, ldw, C::BN))) return s;
     rfk::EpiSigma<0> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>(tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
     if ((s = make_tmap(&tA, S, true, n, m_local, pl.ldS, C::BM))) return s;
     if ((s = make_tmap(&tB, S, true, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K4_syrk", tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
   } else if (prec == RF_PREC_TF32) {
     using C = rfk::TcCfg<2, 1>;
     float* S = (float*)(w + pl.off_s0);
     if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
     if ((s = make_tmap(&tB, W, false, m_local, p, ldw, C::BN))) return s;
     rfk::EpiSigma<1> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>(tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
     if ((s = make_tmap(&tA, S, false, n, m_local, pl.ldS, C::BM))) return s;
     if ((s = make_tmap(&tB, S, false, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K4_syrk", tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
   } else {  // 3XTF32
     using C = rfk::TcCfg<2, 3>;
     float* Sh = (float*)(w + pl.off_s0);
@@ -408,12 +504,12 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
     if ((s = make_tmap(&tB, Wh, false, m_local, p, pl.ldp, C::BN))) return s;
     if ((s = make_tmap(&tBl, Wl, false, m_local, p, pl.ldp, C::BN))) return s;
     rfk::EpiSigma<2> e3{Sh, Sl, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>(tA, tB, tAl, tBl, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tAl, tBl, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
     if ((s = make_tmap(&tA, Sh, false, n, m_local, pl.ldS, C::BM))) return s;
     if ((s = make_tmap(&tAl, Sl, false, n, m_local, pl.ldS, C::BM))) return s;
     if ((s = make_tmap(&tB, Sh, false, n, m_local, pl.ldS, C::BN))) return s;
     if ((s = make_tmap(&tBl, Sl, false, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tAl, tBl, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K4_syrk", tA, tB, tAl, tBl, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
   }
   return ok();
 }
@@ -469,7 +565,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   const size_t es = esize_of(prec);
   rf_status s;
   if ((s = validate_matrix("X", X, ldx, p, es))) return s;
-  if ((s = validate_matrix("Phi", Phi, ldphi, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  if ((s = validate_output("Phi", Phi, ldphi, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
   const PhiPlan pl = phi_plan(p, n, prec);
   if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(RF_E_WORKSPACE, "rf_phi_closed_form: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total,
@@ -484,7 +580,10 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   // Φ1: row norms (all n rows: columns j of every row block need ‖x_j‖²)
   if ((s = launch_rownorm(X, prec, ldx, p, n, nrm2, st))) return s;
   if (!(tau > 0.0)) {   // Lemma 1 τ̂
-    rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, tau_dev);
+    {
+      ProfScope ps("K1_tau_reduce", st);
+      rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, tau_dev);
+    }
     RF_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     double h[2];
@@ -516,19 +615,25 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   if (prec == RF_PREC_FP64) {
     rfk::RowCoefD* rc = (rfk::RowCoefD*)(w + pl.off_rc);
     double* nj = (double*)(w + pl.off_nrm2o);
-    rfk::k_row_coef<rfk::RowCoefD, double><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+    {
+      ProfScope ps("K1_row_coef", st);
+      rfk::k_row_coef<rfk::RowCoefD, double><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+    }
     RF_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     rfk::SimtEq1<double, rfk::RowCoefD> e{(double*)Phi, ldphi, n, rc, nj, mloc.kd[0][0], mloc.kd[1][1], k22h,
                                           mloc.kd[0][1], mloc.kd[1][2], rm.inv_st, full};
-    return (s = launch_simt<double>((const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
+    return (s = launch_simt<double>("K6_simt_xtx_eq1", (const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
                                     (int)((row_end + 63) / 64), e, st))
                ? s
                : ok();
   }
   rfk::RowCoef* rc = (rfk::RowCoef*)(w + pl.off_rc);
   float* nj = (float*)(w + pl.off_nrm2o);
-  rfk::k_row_coef<rfk::RowCoef, float><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+  {
+    ProfScope ps("K1_row_coef", st);
+    rfk::k_row_coef<rfk::RowCoef, float><<<cgrid, 256, 0, st>>>(nrm2, n, rm, rc, nj);
+  }
   RF_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
   if (row_end <= row_begin) return ok();
@@ -536,7 +641,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     rfk::SimtEq1<float, rfk::RowCoef> e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1],
                                         (float)k22h, (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st,
                                         full};
-    return (s = launch_simt<float>((const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
+    return (s = launch_simt<float>("K6_simt_xtx_eq1", (const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
                                    (int)((row_end + 63) / 64), e, st))
                ? s
                : ok();
@@ -551,12 +656,12 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     using C = rfk::TcCfg<1, 1>;
     if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
     if ((s = make_tmap(&tB, X, true, n, p, ldx, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
   } else if (prec == RF_PREC_TF32) {
     using C = rfk::TcCfg<2, 1>;
     if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
     if ((s = make_tmap(&tB, X, false, n, p, ldx, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
   } else {
     using C = rfk::TcCfg<2, 3>;
     float* Xh = (float*)(w + pl.off_xhi);
@@ -566,7 +671,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, C::BM))) return s;
     if ((s = make_tmap(&tB, Xh, false, n, p, pl.ldp, C::BN))) return s;
     if ((s = make_tmap(&tBl, Xl, false, n, p, pl.ldp, C::BN))) return s;
-    if ((s = launch_tc<C>(tA, tB, tAl, tBl, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tAl, tBl, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
   }
   return ok();
 }

@@ -172,7 +172,7 @@ struct EpiSyrk {
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
     float* dst = G + row * ld + col0;
-    if (col0 >= row && col0 + 32 <= n) {
+    if (col0 >= row && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -223,7 +223,7 @@ struct EpiEq1 {
                               k22h, k01, k12, inv_st);
     }
     float* dst = Phi + row * ld + col0;
-    if (col0 >= row && col0 + 32 <= n) {
+    if (col0 >= row && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
