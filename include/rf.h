@@ -110,7 +110,8 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
  *   ws      device workspace ≥ rf_gram_workspace_size(p, n, m_local, prec) bytes, 256-B aligned
  *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode).
  * Pipeline: [3XTF32: K2 split X, W] → K3 fused Σᵀ = σ(X·Wᵀ) (tcgen05 GEMM, σ in the epilogue)
- *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 128×256 tiles with j ≥ i.
+ *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 256×512 CTA-pair tiles with j ≥ i (3XTF32:
+ *           256×256 tiles, K cut into fp32-summed chunks of 256 to bound tensor-pipe accumulation error).
  * Alignment: X, W 16-B aligned with ldx·esize, ldw·esize multiples of 16 B (TMA); G aligned to its element
  *            size, any ldg ≥ n (16-B vector stores are used where rows allow); ws 256-B aligned.
  */
@@ -122,7 +123,7 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
 
 /* ---------------------------------------------------------------------------------------------
  * rf_phi_closed_form — Φ(x_i, x_j) by EQ1 for every pair i ≤ j with i in the row range
- * [row_begin, row_end) (row_begin a multiple of 128, row_end ≤ n; pass 0, n for all rows).
+ * [row_begin, row_end) (row_begin a multiple of 256, row_end = n or a multiple of 256; 0, n = all rows).
  *   Gram–Schmidt with x_i (the row) as pivot: u_a = ‖x_i‖, v_b = x_iᵀx_j/‖x_i‖,
  *   u_b = √max(0, ‖x_j‖² − (x_iᵀx_j)²/‖x_i‖²); diagonal: u_b = 0, v_b = u_a exactly.
  *   α = u_a/√τ − 1, β = u_b/√τ − 1, ν = v_b/√τ;  with ⟨k,d⟩ = mom->kd[k][d]
@@ -134,7 +135,8 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
  *   Phi  device, n × n (ldphi), f64 in RF_PREC_FP64 else f32.  UPPER writes j ≥ i of rows in range;
  *        FULL additionally writes the mirror Φ[j][i] = Φ[i][j] (only rows/cols the range covers).
  *   ws   ≥ rf_phi_workspace_size(p, n, prec).
- * Pipeline: K1 row norms (fp64) [+ τ̂] → per-row coefficients → K5 fused XᵀX (tcgen05) + EQ1 epilogue.
+ * Pipeline: K1 row norms (fp64) [+ τ̂] → per-row coefficients → K5 fused XᵀX (tcgen05 CTA pairs,
+ *           256×256 upper-triangle tiles) + EQ1 epilogue with TMA stores.
  * A zero-norm sample makes v_b undefined: with tau <= 0 it is detected → RF_E_INVALID;
  * with tau > 0 the affected row of Φ is non-finite.
  */
@@ -146,10 +148,22 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
 
 /* ---------------------------------------------------------------------------------------------
  * rf_phi_row_split — row-block sharding of Φ over `world` ranks with no collective: returns the
- * range [*row_begin, *row_end) of rank `rank`, boundaries multiples of 128, balanced by upper-triangle
+ * range [*row_begin, *row_end) of rank `rank`, boundaries multiples of 256, balanced by upper-triangle
  * area (row i carries n − i entries).  Host only.
  */
 rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end);
+
+/* ---------------------------------------------------------------------------------------------
+ * TEST HOOK (not a step of the method): C = A·Bᵀ on the same tcgen05 mainloop the G/Φ kernels use,
+ * raw fp32 accumulator, rectangular pair tiles (256 × 256).  A: M × K (lda), B: N × K (ldb), dtype per
+ * prec ∈ {BF16 (bf16 inputs), TF32, 3XTF32 (f32 inputs)}; C: M × N fp32 (ldc).  kchunk > 0 cuts the K
+ * reduction into chunks of kchunk K-blocks (64 bf16 / 32 fp32 elements each) whose partial sums are added
+ * in fp32 in the epilogue; 0 = one chunk.  ws ≥ rf_debug_gemm_workspace_size() (3XTF32 split operands).
+ */
+rf_status rf_debug_gemm_workspace_size(int64_t M, int64_t N, int64_t K, rf_prec prec, size_t* bytes);
+rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                           rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
+                           void* stream);
 
 /* Number of kernel launches the last successful rf_gram / rf_phi_closed_form call on this thread
  * enqueued (for bench accounting). */

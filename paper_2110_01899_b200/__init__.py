@@ -163,6 +163,26 @@ def rf_profile_read(max_records: int = 4096):
     return [(raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(k)]
 
 
+def rf_debug_gemm_nt(A, B, prec: str = "bf16", kchunk: int = 0, C=None, stream=None):
+    """TEST HOOK: raw C = A·Bᵀ on the tcgen05 mainloop (see include/rf.h)."""
+    torch = _torch()
+    lib = load()
+    dt = _dtype_for(prec)
+    _check_tensor("A", A, dt)
+    _check_tensor("B", B, dt)
+    M, K = A.shape
+    N = B.shape[0]
+    if C is None:
+        C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    need = ctypes.c_size_t()
+    _lib.check(lib.rf_debug_gemm_workspace_size(M, N, K, PREC[prec], ctypes.byref(need)))
+    ws = torch.empty(need.value, dtype=torch.uint8, device=A.device)
+    _lib.check(lib.rf_debug_gemm_nt(ctypes.c_void_p(A.data_ptr()), A.stride(0), ctypes.c_void_p(B.data_ptr()),
+                                    B.stride(0), M, N, K, PREC[prec], int(kchunk), ctypes.c_void_p(C.data_ptr()),
+                                    C.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return C
+
+
 def rf_phi_row_split(n: int, world: int, rank: int) -> Tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
     _lib.check(load().rf_phi_row_split(n, world, rank, ctypes.byref(b), ctypes.byref(e)))

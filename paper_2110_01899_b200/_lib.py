@@ -25,7 +25,7 @@ OUT = {"upper": 0, "full": 1}
 SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "rf_tau_workspace_size",
            "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram", "rf_phi_workspace_size",
            "rf_phi_closed_form", "rf_phi_row_split", "rf_last_launch_count", "rf_profile_enable",
-           "rf_profile_read")
+           "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt")
 
 
 class rf_moments_t(ctypes.Structure):
@@ -68,10 +68,12 @@ def load() -> ctypes.CDLL:
     lib.rf_phi_row_split.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.rf_last_launch_count.restype = i32
     lib.rf_profile_enable.argtypes = [ctypes.c_int]
+    lib.rf_debug_gemm_workspace_size.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
+    lib.rf_debug_gemm_nt.argtypes = [vp, i64, vp, i64, i64, i64, i64, ctypes.c_int, i32, vp, i64, vp, sz, vp]
     lib.rf_profile_read.argtypes = [i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
     for name in ("rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",
-                 "rf_profile_read"):
+                 "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -185,16 +186,50 @@ rf_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t rows, in
   return RF_OK;
 }
 
+// fp32 n_rows × n_cols output map for the epilogue's TMA stores: box 32 × 32, 128-B swizzle.
+// Returns false (no error) when the rows are not 16-B aligned; the epilogue then stores directly.
+bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+  PFN_encode_tiled enc = encode_fn();
+  if (!enc || (reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 4) % 16)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// K-blocks per accumulation chunk (0 = whole K in one chunk).  Env RF_KCHUNK overrides (experiments).
+int kchunk_for(rf_prec prec, int def) {
+  const char* e = std::getenv("RF_KCHUNK");
+  if (e && *e) return std::atoi(e);
+  (void)prec;
+  return def;
+}
+
 template <class Cfg, class Epi>
 rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& alo,
-                    const CUtensorMap& blo, const rfk::Sched& s, int num_kb, const Epi& epi, int sms, cudaStream_t st) {
+                    const CUtensorMap& blo, const CUtensorMap& out, const rfk::Sched& s, const Epi& epi, int sms,
+                    cudaStream_t st) {
   if (s.num_tiles <= 0) return RF_OK;
   ProfScope ps(name, st);
   auto kern = rfk::tc_gemm_kernel<Cfg, Epi>;
   RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES));
-  const int grid = std::min(s.num_tiles, sms);
-  kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(a, b, alo, blo, s, num_kb, epi);
-  RF_CUDA_CHECK(cudaGetLastError());
+  const int clusters = std::max(1, std::min(s.num_tiles, sms / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, alo, blo, out, s, epi));
   ++g_launches;
   return RF_OK;
 }
@@ -282,6 +317,64 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   }
   g.total = off;
   return g;
+}
+
+struct GramTcArgs {
+  const void* X; int64_t ldx; const void* W; int64_t ldw;
+  int64_t p, n, m_local, m_total;
+  rf_act act; int full; float* G; int64_t ldg;
+  char* w; GramPlan pl; int sms; cudaStream_t st;
+};
+
+// kOut: Σ storage (0 bf16, 1 fp32, 2 fp32 hi/lo).  K3 always uses 256-wide pair tiles (σ epilogue
+// overlapped via two TMEM slots); K4 uses kBN4 (512: one slot, a third less L2 traffic per flop than 256).
+template <int kFmt, int kSplit, int kBN4, int kOut>
+rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
+  using C3 = rfk::TcCfg<kFmt, kSplit, 256>;
+  using C4 = rfk::TcCfg<kFmt, kSplit, kBN4>;
+  const bool bf = kFmt == 1;
+  rf_status s;
+  CUtensorMap tA, tB, tAl, tBl, tO;
+  void* S0 = g.w + g.pl.off_s0;
+  void* S1 = g.w + g.pl.off_s1;
+  const void* XA = g.X;
+  const void* WB = g.W;
+  int64_t ldxa = g.ldx, ldwb = g.ldw;
+  if (kSplit == 3) {
+    float* Xh = (float*)(g.w + g.pl.off_xhi);
+    float* Xl = (float*)(g.w + g.pl.off_xlo);
+    float* Wh = (float*)(g.w + g.pl.off_whi);
+    float* Wl = (float*)(g.w + g.pl.off_wlo);
+    if ((s = launch_split((const float*)g.X, g.ldx, g.n, g.p, Xh, Xl, g.pl.ldp, g.sms, g.st))) return s;
+    if ((s = launch_split((const float*)g.W, g.ldw, g.m_local, g.p, Wh, Wl, g.pl.ldp, g.sms, g.st))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, g.n, g.p, g.pl.ldp, 128))) return s;
+    if ((s = make_tmap(&tBl, Wl, false, g.m_local, g.p, g.pl.ldp, 128))) return s;
+    XA = Xh; WB = Wh; ldxa = ldwb = g.pl.ldp;
+  }
+  if ((s = make_tmap(&tA, XA, bf, g.n, g.p, ldxa, 128))) return s;
+  if ((s = make_tmap(&tB, WB, bf, g.m_local, g.p, ldwb, 128))) return s;
+  if (kSplit != 3) { tAl = tA; tBl = tB; }
+  const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
+  const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0);
+  rfk::EpiSigma<kOut> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
+  if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+
+  if ((s = make_tmap(&tA, S0, bf, g.n, g.m_local, g.pl.ldS, 128))) return s;
+  tB = tA;
+  if (kSplit == 3) {
+    if ((s = make_tmap(&tAl, S1, false, g.n, g.m_local, g.pl.ldS, 128))) return s;
+    tBl = tAl;
+  } else {
+    tAl = tA; tBl = tA;
+  }
+  const bool tma_out = make_tmap_out(&tO, g.G, g.n, g.n, g.ldg);
+  if (!tma_out) tO = tA;
+  const int kb4 = (int)((g.m_local + C4::BK - 1) / C4::BK);
+  const rfk::Sched s4 =
+      rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4);
+  rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+  if ((s = launch_tc<C4>("K4_syrk", tA, tB, tAl, tBl, tO, s4, e4, g.sms, g.st))) return s;
+  return ok();
 }
 
 rf_status validate_output(const char* name, const void* ptr, int64_t ld, int64_t cols, size_t es) {
@@ -439,8 +532,6 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
   cudaStream_t st = (cudaStream_t)stream;
   char* w = (char*)ws;
   const int full = out == RF_OUT_FULL;
-  const int tiles_m = (int)((n + 127) / 128);
-  const int tiles_n = (int)((n + 255) / 256);
 
   if (prec == RF_PREC_FP64 || prec == RF_PREC_FP32) {
     if (prec == RF_PREC_FP64) {
@@ -465,51 +556,72 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
     return ok();
   }
 
+  // Tensor-core path: [K2 split] → K3 (pair tiles 256×256, σ epilogue) → K4 (triangle, SYRK epilogue)
+  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, full, (float*)G, ldg, w, pl, dev.sms, st};
+  if (prec == RF_PREC_BF16) return gram_tc<1, 1, 512, 0>(ga, kchunk_for(prec, 0));
+  if (prec == RF_PREC_TF32) return gram_tc<2, 1, 512, 1>(ga, kchunk_for(prec, 0));
+  return gram_tc<2, 3, 256, 2>(ga, kchunk_for(prec, 8));
+  return ok();
+}
+
+rf_status rf_debug_gemm_workspace_size(int64_t M, int64_t N, int64_t K, rf_prec prec, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (M <= 0 || N <= 0 || K <= 0) return fail(RF_E_INVALID, "M, N, K must be > 0");
+  const int64_t ldk = round_up(K, 32);
+  *bytes = prec == RF_PREC_3XTF32 ? align256((size_t)(M + N) * ldk * 4 * 2) + 256 : 256;
+  return ok();
+}
+
+rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+                           rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
+                           void* stream) {
+  g_launches = 0;
+  if (M <= 0 || N <= 0 || K <= 0) return fail(RF_E_INVALID, "rf_debug_gemm_nt: M, N, K must be > 0");
+  if (prec != RF_PREC_BF16 && prec != RF_PREC_TF32 && prec != RF_PREC_3XTF32)
+    return fail(RF_E_INVALID, "rf_debug_gemm_nt: tensor-core precisions only (BF16, TF32, 3XTF32)");
+  const size_t es = esize_of(prec);
+  rf_status s;
+  if ((s = validate_matrix("A", A, lda, K, es))) return s;
+  if ((s = validate_matrix("B", B, ldb, K, es))) return s;
+  if ((s = validate_output("C", C, ldc, N, 4))) return s;
+  size_t need = 0;
+  rf_debug_gemm_workspace_size(M, N, K, prec, &need);
+  if (ws_bytes < need || (need > 256 && (!ws || (reinterpret_cast<uintptr_t>(ws) & 255))))
+    return fail(RF_E_WORKSPACE, "rf_debug_gemm_nt: workspace needs %zu bytes", need);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  rfk::EpiRaw e{C, ldc, M, N};
   CUtensorMap tA, tB, tAl, tBl;
-  const rfk::Sched s3 = rfk::Sched::rect(0, tiles_m, (int)((m_local + 255) / 256));
-  const rfk::Sched s4 = rfk::Sched::triangle(0, tiles_m, tiles_n);
-  rfk::EpiSyrk e4{(float*)G, ldg, n, (float)(1.0 / (double)m_total), full};
-  if (prec == RF_PREC_BF16) {
-    using C = rfk::TcCfg<1, 1>;
-    __nv_bfloat16* S = (__nv_bfloat16*)(w + pl.off_s0);
-    if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
-    if ((s = make_tmap(&tB, W, true, m_local, p, ldw, C::BN))) return s;
-    rfk::EpiSigma<0> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, S, true, n, m_local, pl.ldS, C::BM))) return s;
-    if ((s = make_tmap(&tB, S, true, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>("K4_syrk", tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
-  } else if (prec == RF_PREC_TF32) {
-    using C = rfk::TcCfg<2, 1>;
-    float* S = (float*)(w + pl.off_s0);
-    if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
-    if ((s = make_tmap(&tB, W, false, m_local, p, ldw, C::BN))) return s;
-    rfk::EpiSigma<1> e3{S, nullptr, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tA, tB, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, S, false, n, m_local, pl.ldS, C::BM))) return s;
-    if ((s = make_tmap(&tB, S, false, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>("K4_syrk", tA, tB, tA, tB, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
-  } else {  // 3XTF32
-    using C = rfk::TcCfg<2, 3>;
-    float* Sh = (float*)(w + pl.off_s0);
-    float* Sl = (float*)(w + pl.off_s1);
-    float* Xh = (float*)(w + pl.off_xhi);
-    float* Xl = (float*)(w + pl.off_xlo);
-    float* Wh = (float*)(w + pl.off_whi);
-    float* Wl = (float*)(w + pl.off_wlo);
-    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
-    if ((s = launch_split((const float*)W, ldw, m_local, p, Wh, Wl, pl.ldp, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, C::BM))) return s;
-    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, C::BM))) return s;
-    if ((s = make_tmap(&tB, Wh, false, m_local, p, pl.ldp, C::BN))) return s;
-    if ((s = make_tmap(&tBl, Wl, false, m_local, p, pl.ldp, C::BN))) return s;
-    rfk::EpiSigma<2> e3{Sh, Sl, pl.ldS, n, m_local, (int)act};
-    if ((s = launch_tc<C>("K3_gemm_sigma", tA, tB, tAl, tBl, s3, (int)((p + C::BK - 1) / C::BK), e3, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, Sh, false, n, m_local, pl.ldS, C::BM))) return s;
-    if ((s = make_tmap(&tAl, Sl, false, n, m_local, pl.ldS, C::BM))) return s;
-    if ((s = make_tmap(&tB, Sh, false, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = make_tmap(&tBl, Sl, false, n, m_local, pl.ldS, C::BN))) return s;
-    if ((s = launch_tc<C>("K4_syrk", tA, tB, tAl, tBl, s4, (int)((m_local + C::BK - 1) / C::BK), e4, dev.sms, st))) return s;
+  const int rt = (int)((M + 255) / 256), tn = (int)((N + 255) / 256);
+  if (prec == RF_PREC_3XTF32) {
+    using Cf = rfk::TcCfg<2, 3, 256>;
+    const int64_t ldk = round_up(K, 32);
+    float* Ah = (float*)ws;
+    float* Al = Ah + M * ldk;
+    float* Bh = Al + M * ldk;
+    float* Bl = Bh + N * ldk;
+    if ((s = launch_split((const float*)A, lda, M, K, Ah, Al, ldk, dev.sms, st))) return s;
+    if ((s = launch_split((const float*)B, ldb, N, K, Bh, Bl, ldk, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Ah, false, M, K, ldk, 128))) return s;
+    if ((s = make_tmap(&tAl, Al, false, M, K, ldk, 128))) return s;
+    if ((s = make_tmap(&tB, Bh, false, N, K, ldk, 128))) return s;
+    if ((s = make_tmap(&tBl, Bl, false, N, K, ldk, 128))) return s;
+    const rfk::Sched sc = rfk::Sched::make(0, 256, 0, rt, tn, (int)((K + Cf::BK - 1) / Cf::BK), kchunk);
+    if ((s = launch_tc<Cf>("KD_gemm_nt", tA, tB, tAl, tBl, tA, sc, e, dev.sms, st))) return s;
+  } else {
+    const bool bf = prec == RF_PREC_BF16;
+    if ((s = make_tmap(&tA, A, bf, M, K, lda, 128))) return s;
+    if ((s = make_tmap(&tB, B, bf, N, K, ldb, 128))) return s;
+    if (bf) {
+      using Cf = rfk::TcCfg<1, 1, 256>;
+      const rfk::Sched sc = rfk::Sched::make(0, 256, 0, rt, tn, (int)((K + Cf::BK - 1) / Cf::BK), kchunk);
+      if ((s = launch_tc<Cf>("KD_gemm_nt", tA, tB, tA, tB, tA, sc, e, dev.sms, st))) return s;
+    } else {
+      using Cf = rfk::TcCfg<2, 1, 256>;
+      const rfk::Sched sc = rfk::Sched::make(0, 256, 0, rt, tn, (int)((K + Cf::BK - 1) / Cf::BK), kchunk);
+      if ((s = launch_tc<Cf>("KD_gemm_nt", tA, tB, tA, tB, tA, sc, e, dev.sms, st))) return s;
+    }
   }
   return ok();
 }
@@ -525,10 +637,10 @@ rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* byte
 rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end) {
   if (n <= 0 || world <= 0 || rank < 0 || rank >= world || !row_begin || !row_end)
     return fail(RF_E_INVALID, "rf_phi_row_split: bad arguments");
-  // rows of 128; boundary b_r = smallest tile boundary with triangle area above ≥ r/world of the total
-  const int64_t T = (n + 127) / 128;
-  auto area_before = [&](int64_t tile) -> double {   // entries j ≥ i in rows [0, 128·tile)
-    const double r = std::min<int64_t>(tile * 128, n);
+  // rows of 256 (the pair tile); boundary b_r = smallest tile boundary with triangle area above ≥ r/world
+  const int64_t T = (n + 255) / 256;
+  auto area_before = [&](int64_t tile) -> double {   // entries j ≥ i in rows [0, 256·tile)
+    const double r = std::min<int64_t>(tile * 256, n);
     return r * (double)n - r * (r - 1) / 2.0;
   };
   const double total = area_before(T);
@@ -543,8 +655,8 @@ rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_
     }
     return lo;
   };
-  *row_begin = std::min<int64_t>(boundary(rank) * 128, n);
-  *row_end = std::min<int64_t>(boundary(rank + 1) * 128, n);
+  *row_begin = std::min<int64_t>(boundary(rank) * 256, n);
+  *row_end = std::min<int64_t>(boundary(rank + 1) * 256, n);
   return ok();
 }
 
@@ -557,10 +669,10 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   if (!valid_act(act)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown activation %d", (int)act);
   if (!valid_prec(prec)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown precision %d", (int)prec);
   if (!valid_out(out)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown output mode %d", (int)out);
-  if (row_begin < 0 || row_end > n || row_begin > row_end || (row_begin % 128) != 0 ||
-      (row_end != n && (row_end % 128) != 0))
+  if (row_begin < 0 || row_end > n || row_begin > row_end || (row_begin % 256) != 0 ||
+      (row_end != n && (row_end % 256) != 0))
     return fail(RF_E_INVALID, "rf_phi_closed_form: row range [%lld, %lld) must satisfy 0 <= begin <= end <= n, "
-                "begin %% 128 == 0, end == n or end %% 128 == 0", (long long)row_begin, (long long)row_end);
+                "begin %% 256 == 0, end == n or end %% 256 == 0", (long long)row_begin, (long long)row_end);
   if (!std::isfinite(tau)) return fail(RF_E_INVALID, "rf_phi_closed_form: tau is not finite");
   const size_t es = esize_of(prec);
   rf_status s;
@@ -646,32 +758,36 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
                ? s
                : ok();
   }
-  // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle tiles
+  // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
+  CUtensorMap tA, tAl, tO;
+  const bool tma_out = make_tmap_out(&tO, Phi, n, n, ldphi);
   rfk::EpiEq1 e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1], (float)k22h,
-                (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st, full};
-  const int tiles_n = (int)((n + 255) / 256);
-  const rfk::Sched sc = rfk::Sched::triangle((int)(row_begin / 128), (int)((row_end + 127) / 128), tiles_n);
-  CUtensorMap tA, tB, tAl, tBl;
-  if (prec == RF_PREC_BF16) {
-    using C = rfk::TcCfg<1, 1>;
-    if ((s = make_tmap(&tA, X, true, n, p, ldx, C::BM))) return s;
-    if ((s = make_tmap(&tB, X, true, n, p, ldx, C::BN))) return s;
-    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
-  } else if (prec == RF_PREC_TF32) {
-    using C = rfk::TcCfg<2, 1>;
-    if ((s = make_tmap(&tA, X, false, n, p, ldx, C::BM))) return s;
-    if ((s = make_tmap(&tB, X, false, n, p, ldx, C::BN))) return s;
-    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tA, tB, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+                (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st, full, tma_out ? 1 : 0};
+  const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
+  if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
+    const bool bf = prec == RF_PREC_BF16;
+    if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
+    if (!tma_out) tO = tA;
+    if (bf) {
+      using C = rfk::TcCfg<1, 1, 256>;
+      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0);
+      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    } else {
+      using C = rfk::TcCfg<2, 1, 256>;
+      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0);
+      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    }
   } else {
-    using C = rfk::TcCfg<2, 3>;
+    using C = rfk::TcCfg<2, 3, 256>;
     float* Xh = (float*)(w + pl.off_xhi);
     float* Xl = (float*)(w + pl.off_xlo);
     if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, C::BM))) return s;
-    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, C::BM))) return s;
-    if ((s = make_tmap(&tB, Xh, false, n, p, pl.ldp, C::BN))) return s;
-    if ((s = make_tmap(&tBl, Xl, false, n, p, pl.ldp, C::BN))) return s;
-    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tB, tAl, tBl, sc, (int)((p + C::BK - 1) / C::BK), e, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, 128))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
+    if (!tma_out) tO = tA;
+    const rfk::Sched sc =
+        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), kchunk_for(prec, 0));
+    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
   }
   return ok();
 }

@@ -1,17 +1,29 @@
-// Warp-specialised persistent tcgen05 GEMM for sm_100a, shared by the three tensor-core kernels:
-//   K3  Σᵀ = σ(X·Wᵀ)          rectangular tiles, σ in the epilogue          (Σ = σ(WX))
-//   K4  G  = ΣᵀΣ / m          upper-triangular tiles, scale in the epilogue  (Eq. def_Gram)
-//   K5  Φ  = EQ1(XᵀX, …)      upper-triangular tiles, EQ1 in the epilogue
+// Warp-specialised persistent tcgen05 GEMM for sm_100a on CTA PAIRS (cta_group::2), shared by the three
+// tensor-core kernels of the path:
+//   K3  Σᵀ = σ(X·Wᵀ)          rectangular pair tiles, σ in the epilogue          (Σ = σ(WX))
+//   K4  G  = ΣᵀΣ / m          upper-triangular pair tiles, scale in the epilogue (Eq. def_Gram)
+//   K5  Φ  = EQ1(XᵀX, …)      upper-triangular pair tiles, EQ1 in the epilogue
 // D[i][j] = Σ_k A[i][k]·B[j][k]; A (rows i) and B (rows j) are both K-major in HBM, so
 // both UMMA operands are K-major 128-B-swizzled smem tiles written by TMA.
 //
-// Tile 128 (M) × 256 (N), K-block = one 128-byte swizzle row (64 bf16 / 32 fp32).
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one thread), w2 TMEM allocator,
-// w3 idle, w4..w7 epilogue (warp w4+q owns TMEM lanes / tile rows 32q..32q+31).
-// Pipelines: smem ring (full/empty mbarriers, STAGES deep) TMA→MMA; TMEM double-buffered accumulator
-// (2 × 256 fp32 columns = all 512 columns) MMA→epilogue, so tile t+1's MMAs overlap tile t's epilogue.
-// 3×TF32 (kSplit = 3): each stage holds A_hi, A_lo, B_hi, B_lo; per K-step three MMAs
-// lo·hi, hi·lo, hi·hi accumulate into the same TMEM accumulator (small terms first).
+// Pair tile 256 (M) × BN (N = 256 or 512).  CTA r of the pair loads A rows [M0+128r, +128) and, for each
+// 256-wide N sub-tile s, B rows [N0+256s+128r, +128); the leader (r = 0) issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256) per sub-tile and K-step; CTA r's TMEM receives rows
+// M0+128r.. of the accumulator.  Per SM this moves (16 + 16·BN/256) KB of operands per
+// 256·BN·64 MACs — half (BN=256) or a third (BN=512) of the 1-CTA 128×256 tile's L2 traffic per flop.
+// K-block = one 128-byte swizzle row (64 bf16 / 32 fp32).
+//
+// Warp roles (384 threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA, one thread), w2 TMEM
+// allocator, w3 idle, w4..w11 epilogue (warp w: TMEM lane quarter w%4, column half (w-4)/4).
+// Pipelines: smem ring (full barrier in the leader, empty barriers in both CTAs) TMA→MMA; TMEM
+// accumulator slots (2 × 256 columns for BN = 256, 1 × 512 for BN = 512) MMA→epilogue.
+//
+// K-chunked accumulation (kchunk k-blocks): the K range of a tile is cut into chunks whose partial sums
+// start from zero in TMEM and are added in fp32 (round-to-nearest) in the epilogue.  The tensor pipe's
+// accumulation into TMEM loses up to ~2^-23 relative per MMA (measured: 3×TF32 SYRK error grows
+// linearly with K), so long-K fp32-accurate results need short chunks.
+// 3×TF32 (kSplit = 3): each stage holds A_hi, A_lo, B_hi, B_lo; per K-step three MMAs lo·hi, hi·lo,
+// hi·hi accumulate into the same accumulator (small terms first).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -22,73 +34,135 @@
 
 namespace rfk {
 
-template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32*/, int kSplit /*1 or 3*/>
+template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32*/, int kSplit /*1 or 3*/, int kBN /*256 or 512*/>
 struct TcCfg {
-  static constexpr int BM = 128, BN = 256;
+  static constexpr int BM = 256, BN = kBN;      // pair tile
+  static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
   static constexpr int ESZ = kFmt == 1 ? 2 : 4;
   static constexpr int BK = 128 / ESZ;          // elements per K-block (one 128-B swizzle row)
   static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (16 bf16 / 8 tf32) = 32 bytes
   static constexpr int NOPS = kSplit == 3 ? 2 : 1;
-  static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int STAGES = kSplit == 3 ? 2 : 4;
-  static constexpr int TMEM_COLS = 512;
-  static constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256 /*barriers*/;
-  static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt, BM, BN);
+  static constexpr int A_BYTES = 128 * 128;     // per CTA: 128 rows × 128 B
+  static constexpr int B_BYTES = 128 * 128;     // per CTA per N sub-tile
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + NSUB * B_BYTES);
+  static constexpr int ACC_COLS = kBN;
+  static constexpr int ACC_SLOTS = 512 / kBN;
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int STG_BUFS = (kSplit == 3 || kBN == 512) ? 1 : 2;   // TMA-store staging per epi warp
+  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
+  static constexpr int STAGES = (225 * 1024 - STG_BYTES) / STAGE_BYTES;
+  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + STG_BYTES + 256;
+  static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt, 256, 256);
+  static_assert(STAGES >= 2, "pipeline too shallow");
+  static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
 
-// Tile scheduler.  Rectangular: row tiles [row_tile0, row_tile1) × all column tiles.
-// Triangular (tri = 1): row tile I covers rows [128 I, 128 I + 128) and needs the column tiles
-// J ≥ floor(I/2) (tile columns are 256 wide), i.e. every tile holding some entry j ≥ i.
+// Pair-tile scheduler.  Rows of 256, columns of BN.  Rectangular: row tiles [row_tile0, row_tile1) × all
+// column tiles.  Triangular: row tile I needs the column tiles J ≥ floor(256 I / BN) (every tile holding
+// an entry j ≥ i).  Work item = (tile, K-chunk); a cluster processes all chunks of a tile in order.
 struct Sched {
   int tri;
+  int shift;            // log2(BN/256)
   int tiles_n;
   int row_tile0, row_tile1;
   int num_tiles;
+  int num_kb;           // K-blocks of the whole reduction
+  int kchunk;           // K-blocks per chunk
+  int nchunks;
 
-  // Σ_{r < I} floor(r/2)
-  __host__ __device__ static long long half_sum(long long I) {
+  __host__ __device__ long long jmin_sum(long long I) const {   // Σ_{r < I} (r >> shift)
+    if (shift == 0) return I * (I - 1) / 2;
     long long q = I >> 1;
     return (I & 1) ? q * q : q * (q - 1);
   }
-  __host__ __device__ long long prefix(long long I) const {  // tiles in rows [0, I)
-    return I * (long long)tiles_n - half_sum(I);
-  }
+  __host__ __device__ long long prefix(long long I) const { return I * (long long)tiles_n - jmin_sum(I); }
   __host__ __device__ void tile(int t, int& ti, int& tj) const {
     if (!tri) {
       ti = row_tile0 + t / tiles_n;
       tj = t % tiles_n;
       return;
     }
-    const long long base = prefix(row_tile0);
-    long long target = base + t;
+    const long long target = prefix(row_tile0) + t;
     int lo = row_tile0, hi = row_tile1 - 1;   // largest I with prefix(I) <= target
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
+      const int mid = (lo + hi + 1) >> 1;
       if (prefix(mid) <= target) lo = mid; else hi = mid - 1;
     }
     ti = lo;
-    tj = (lo >> 1) + (int)(target - prefix(lo));
+    tj = (lo >> shift) + (int)(target - prefix(lo));
   }
-  static Sched rect(int row_tile0, int row_tile1, int tiles_n) {
+  static Sched make(int tri, int bn, int row_tile0, int row_tile1, int tiles_n, int num_kb, int kchunk) {
     Sched s;
-    s.tri = 0; s.tiles_n = tiles_n; s.row_tile0 = row_tile0; s.row_tile1 = row_tile1;
-    s.num_tiles = (row_tile1 - row_tile0) * tiles_n;
-    return s;
-  }
-  static Sched triangle(int row_tile0, int row_tile1, int tiles_n) {
-    Sched s;
-    s.tri = 1; s.tiles_n = tiles_n; s.row_tile0 = row_tile0; s.row_tile1 = row_tile1;
-    s.num_tiles = (int)(s.prefix(row_tile1) - s.prefix(row_tile0));
+    s.tri = tri;
+    s.shift = bn == 512 ? 1 : 0;
+    s.tiles_n = tiles_n;
+    s.row_tile0 = row_tile0;
+    s.row_tile1 = row_tile1;
+    s.num_kb = num_kb;
+    s.kchunk = (kchunk <= 0 || kchunk > num_kb) ? (num_kb > 0 ? num_kb : 1) : kchunk;
+    s.nchunks = num_kb > 0 ? (num_kb + s.kchunk - 1) / s.kchunk : 1;
+    s.num_tiles = tri ? (int)(s.prefix(row_tile1) - s.prefix(row_tile0)) : (row_tile1 - row_tile0) * tiles_n;
     return s;
   }
 };
 
 // ------------------------------------------------------------------------------------------
-// Epilogues.  operator()(row, col0, r[32]) receives row `row` (global) and accumulator columns
-// [col0, col0+32) as raw fp32 bits; `chunk_needed(row_lo, row_hi, col0)` lets triangular epilogues
-// skip 32-column chunks entirely below the diagonal for the warp's 32 rows (warp-uniform).
+// Epilogue store helpers.  A warp owns 32 rows (lanes) × 32 columns per call.
+// ------------------------------------------------------------------------------------------
+template <int kBufs>
+struct EpiCtx {
+  const CUtensorMap* tm;   // fp32 output map: box 32 × 32, 128-B swizzle, bounds = the n×n matrix
+  uint8_t* sbuf;           // this warp's staging buffers (kBufs × 4 KB, 1024-B aligned)
+  int cur;
+  uint32_t lane;
+
+  // Whole 32×32 block → smem (128-B swizzle: 16-B chunk c of row r at chunk c ^ (r & 7), conflict-free)
+  // → one TMA store (rows/cols beyond the matrix are clipped by the tensor map).
+  __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
+    uint8_t* b = sbuf + cur * 4096;
+    if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<float4*>(b + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(tm, b, (int32_t)col0, (int32_t)row_lo);
+      ptx::bulk_commit();
+    }
+    cur = (cur + 1 == kBufs) ? 0 : cur + 1;
+  }
+};
+
+// Direct masked stores of row `row`, columns [col0, col0+32) ∩ [lo, n) into a row-major fp32 matrix.
+__device__ __forceinline__ void store_row_masked(float* M, int64_t ld, int64_t n, int64_t row, int64_t col0, int64_t lo,
+                                                 const float (&v)[32]) {
+  float* dst = M + row * ld + col0;
+  if (col0 >= lo && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (col0 + e >= lo && col0 + e < n) dst[e] = v[e];
+  }
+}
+// Mirror (FULL output): M[j][row] = v[j - col0] for j > row; for fixed e the 32 lanes write 32
+// consecutive floats of row col0+e (coalesced).
+__device__ __forceinline__ void store_mirror(float* M, int64_t ld, int64_t n, int64_t row, int64_t col0,
+                                             const float (&v)[32]) {
+  if (row >= n) return;
+#pragma unroll
+  for (int e = 0; e < 32; ++e)
+    if (col0 + e > row && col0 + e < n) M[(col0 + e) * ld + row] = v[e];
+}
+
+// ------------------------------------------------------------------------------------------
+// Epilogue functors: operator()(ctx, row_lo, col0, r[32], chunk, nchunks) for the warp's rows
+// [row_lo, row_lo+32) (row = row_lo + lane) and accumulator columns [col0, col0+32).
 // ------------------------------------------------------------------------------------------
 
 // K3: Σᵀ[i][k] = σ(z), z = x_iᵀw_k.  kOut: 0 = bf16, 1 = fp32, 2 = fp32 hi/lo split (3×TF32).
@@ -99,8 +173,11 @@ struct EpiSigma {
   int64_t ld;       // elements
   int64_t M, N;     // n rows (samples), m_local columns (features)
   int act;
-  __device__ __forceinline__ bool chunk_needed(int64_t, int64_t, int64_t col0) const { return col0 < N; }
-  __device__ __forceinline__ void operator()(int64_t row, int64_t col0, const uint32_t (&r)[32]) const {
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
+                                             int) const {
+    const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float s[32];
 #pragma unroll
@@ -144,7 +221,7 @@ struct EpiSigma {
         for (int e = 0; e < 32; ++e) {
           if (col0 + e < N) {
             if (kOut == 2) {
-              float h = tf32_hi(s[e]);
+              const float h = tf32_hi(s[e]);
               d0[e] = h;
               d1[e] = s[e] - h;
             } else {
@@ -157,36 +234,36 @@ struct EpiSigma {
   }
 };
 
-// K4: G[i][j] = scale · Σᵀ_iᵀΣᵀ_j for j ≥ i (and the mirror for FULL).
+// K4: G[i][j] = scale · Σᵀ_iᵀΣᵀ_j for j ≥ i (and the mirror for FULL); chunked: G += scale·partial.
 struct EpiSyrk {
   float* G;
   int64_t ld, n;
   float scale;
   int full;
-  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t, int64_t col0) const {
-    return col0 < n && col0 + 31 >= row_lo;
+  int use_tma;      // the output tensor map is valid (16-B aligned rows)
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
+    return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
-  __device__ __forceinline__ void operator()(int64_t row, int64_t col0, const uint32_t (&r)[32]) const {
-    if (row >= n) return;
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
+                                             int chunk, int nchunks) const {
+    const int64_t row = row_lo + cx.lane;
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
-    float* dst = G + row * ld + col0;
-    if (col0 >= row && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    if (nchunks == 1 && use_tma && col0 >= row_lo + 31) {
+      cx.store_block(row_lo, col0, v);
     } else {
+      if (row >= n) return;
+      if (chunk > 0) {
+        const float* src = G + row * ld + col0;
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e >= row && col0 + e < n) dst[e] = v[e];
+        for (int e = 0; e < 32; ++e)
+          if (col0 + e >= row && col0 + e < n) v[e] += src[e];
+      }
+      store_row_masked(G, ld, n, row, col0, row, v);
     }
-    if (full) {
-      // mirror: for fixed e the warp's 32 lanes write 32 consecutive floats of row col0+e (coalesced)
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e > row && col0 + e < n) G[(col0 + e) * ld + row] = v[e];
-    }
+    if (full && chunk == nchunks - 1) store_mirror(G, ld, n, row, col0, v);
   }
 };
 
@@ -198,63 +275,83 @@ struct EpiEq1 {
   const float* nrm2;     // ‖x_j‖² per column
   float k00, k11, k22h, k01, k12, inv_st;
   int full;
-  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t, int64_t col0) const {
-    return col0 < n && col0 + 31 >= row_lo;
+  int use_tma;
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
+    return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
-  __device__ __forceinline__ void operator()(int64_t row, int64_t col0, const uint32_t (&r)[32]) const {
-    if (row >= n) return;
-    const RowCoef c = rc[row];
-    float v[32];
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
+                                             int) const {
+    const int64_t row = row_lo + cx.lane;
+    const RowCoef c = rc[row < n ? row : n - 1];
     float nj[32];
     if (col0 + 32 <= n) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        float4 t = __ldg(reinterpret_cast<const float4*>(nrm2 + col0) + q);
+        const float4 t = __ldg(reinterpret_cast<const float4*>(nrm2 + col0) + q);
         nj[4 * q] = t.x; nj[4 * q + 1] = t.y; nj[4 * q + 2] = t.z; nj[4 * q + 3] = t.w;
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 32; ++e) nj[e] = (col0 + e < n) ? __ldg(nrm2 + col0 + e) : 1.f;
     }
+    float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) {
       const float g = __uint_as_float(r[e]);
       v[e] = eq1_entry<float>(g, c.a0, c.a1, c.a2h, c.c, c.inv_ua, nj[e], col0 + e == row, c.nu_diag, k00, k11,
                               k22h, k01, k12, inv_st);
     }
-    float* dst = Phi + row * ld + col0;
-    if (col0 >= row && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    if (use_tma && col0 >= row_lo + 31) {
+      cx.store_block(row_lo, col0, v);
     } else {
+      if (row >= n) return;
+      store_row_masked(Phi, ld, n, row, col0, row, v);
+    }
+    if (full) store_mirror(Phi, ld, n, row, col0, v);
+  }
+};
+
+// Raw accumulator D = A·Bᵀ (rectangular, fp32, chunk-accumulated) — the mainloop test hook behind
+// rf_debug_gemm_nt.
+struct EpiRaw {
+  float* C;
+  int64_t ld, M, N;
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
+                                             int chunk, int) const {
+    const int64_t row = row_lo + cx.lane;
+    if (row >= M) return;
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+    float* dst = C + row * ld + col0;
+    if (chunk > 0) {
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        if (col0 + e >= row && col0 + e < n) dst[e] = v[e];
+        if (col0 + e < N) v[e] += dst[e];
     }
-    if (full) {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e > row && col0 + e < n) Phi[(col0 + e) * ld + row] = v[e];
-    }
+    store_row_masked(C, ld, N, row, col0, 0, v);
   }
 };
 
 // ------------------------------------------------------------------------------------------
-// The kernel.
+// The kernel.  Launch: grid = 2 × (#clusters), cluster dims (2,1,1), 384 threads, Cfg::SMEM_BYTES.
 // ------------------------------------------------------------------------------------------
 template <class Cfg, class Epi>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
-                   const Sched sched, const int num_kb, const Epi epi) {
+                   const __grid_constant__ CUtensorMap tmOut, const Sched sched, const Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  constexpr int STAGES = Cfg::STAGES, NOPS = Cfg::NOPS;
+  constexpr int STAGES = Cfg::STAGES, NOPS = Cfg::NOPS, NSUB = Cfg::NSUB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                                             // [STAGES][NOPS][A_BYTES]
-  uint8_t* sB = smem + (size_t)STAGES * NOPS * Cfg::A_BYTES;       // [STAGES][NOPS][B_BYTES]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)STAGES * NOPS * Cfg::B_BYTES);
+  uint8_t* sA = smem;                                                    // [STAGES][NOPS][A_BYTES]
+  uint8_t* sB = sA + (size_t)STAGES * NOPS * Cfg::A_BYTES;               // [STAGES][NOPS][NSUB][B_BYTES]
+  uint8_t* sStg = sB + (size_t)STAGES * NOPS * NSUB * Cfg::B_BYTES;      // [EPI_WARPS][STG_BUFS][4096]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Cfg::STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -262,6 +359,9 @@ __global__ void __launch_bounds__(256, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int cid = (int)ptx::cluster_id_x();
+  const int ncl = (int)ptx::ncluster_x();
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -276,114 +376,142 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS);
     }
     ptx::fence_mbarrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) ptx::tmem_alloc_cg2(tmem_slot, 512);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
       const uint64_t pol = ptx::policy_evict_normal();
+      const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x) {
+      for (int t = cid; t < sched.num_tiles; t += ncl) {
         int ti, tj;
         sched.tile(t, ti, tj);
-        const int ra = ti * Cfg::BM, rb = tj * Cfg::BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          const int k = kb * Cfg::BK;
-          uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
-          uint8_t* b = sB + (size_t)(stage * NOPS) * Cfg::B_BYTES;
-          ptx::tma_load_2d(a, &tmA, &full[stage], k, ra, pol);
-          ptx::tma_load_2d(b, &tmB, &full[stage], k, rb, pol);
-          if (NOPS == 2) {
-            ptx::tma_load_2d(a + Cfg::A_BYTES, &tmA_lo, &full[stage], k, ra, pol);
-            ptx::tma_load_2d(b + Cfg::B_BYTES, &tmB_lo, &full[stage], k, rb, pol);
+        const int ra = ti * Cfg::BM + (int)rank * 128;
+        const int rb = tj * Cfg::BN + (int)rank * 128;
+        for (int c = 0; c < nchunks; ++c) {
+          const int kb1 = min(num_kb, (c + 1) * kchunk);
+          for (int kb = c * kchunk; kb < kb1; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            const uint32_t fb = full0 + stage * 8;
+            const int k = kb * Cfg::BK;
+            uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
+            uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
+            ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
+#pragma unroll
+            for (int s = 0; s < NSUB; ++s) ptx::tma_load_2d_cg2(b + s * Cfg::B_BYTES, &tmB, fb, k, rb + 256 * s, pol);
+            if (NOPS == 2) {
+              ptx::tma_load_2d_cg2(a + Cfg::A_BYTES, &tmA_lo, fb, k, ra, pol);
+#pragma unroll
+              for (int s = 0; s < NSUB; ++s)
+                ptx::tma_load_2d_cg2(b + (NSUB + s) * Cfg::B_BYTES, &tmB_lo, fb, k, rb + 256 * s, pol);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer (single thread) =====
+    if (rank == 0 && lane == 0) {
+      // ===== MMA issuer (leader CTA, single thread) =====
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d = tmem_base + acc * Cfg::BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+      for (int t = cid; t < sched.num_tiles; t += ncl) {
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
+          const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
+          ptx::mbar_wait(&tempty[slot], acc_phase ^ 1);
           ptx::tc_fence_after();
-          const uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
-          const uint8_t* b = sB + (size_t)(stage * NOPS) * Cfg::B_BYTES;
-          const uint64_t ad = ptx::sdesc_k128(ptx::smem_u32(a));
-          const uint64_t bd = ptx::sdesc_k128(ptx::smem_u32(b));
+          const uint32_t d = tmem_base + slot * Cfg::ACC_COLS;
+          const int kb0 = c * kchunk, kb1 = min(num_kb, (c + 1) * kchunk);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&full[stage], phase);
+            ptx::tc_fence_after();
+            const uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
+            const uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
+            const uint64_t ad = ptx::sdesc_k128(ptx::smem_u32(a));
 #pragma unroll
-          for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
-            const uint64_t off = (uint64_t)((k * 32) >> 4);   // +32 B along K inside the swizzle row
-            const uint32_t accum = (kb | k) != 0;
-            if (NOPS == 2) {
-              const uint64_t adl = ptx::sdesc_k128(ptx::smem_u32(a + Cfg::A_BYTES));
-              const uint64_t bdl = ptx::sdesc_k128(ptx::smem_u32(b + Cfg::B_BYTES));
-              ptx::mma_tf32(d, adl + off, bd + off, Cfg::IDESC, accum);
-              ptx::mma_tf32(d, ad + off, bdl + off, Cfg::IDESC, 1u);
-              ptx::mma_tf32(d, ad + off, bd + off, Cfg::IDESC, 1u);
-            } else if (Cfg::ESZ == 2) {
-              ptx::mma_bf16(d, ad + off, bd + off, Cfg::IDESC, accum);
-            } else {
-              ptx::mma_tf32(d, ad + off, bd + off, Cfg::IDESC, accum);
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint64_t off = (uint64_t)((k * 32) >> 4);   // +32 B along K inside the swizzle row
+              const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+#pragma unroll
+              for (int s = 0; s < NSUB; ++s) {
+                const uint64_t bd = ptx::sdesc_k128(ptx::smem_u32(b + s * Cfg::B_BYTES));
+                const uint32_t ds = d + s * 256;
+                if (NOPS == 2) {
+                  const uint64_t adl = ptx::sdesc_k128(ptx::smem_u32(a + Cfg::A_BYTES));
+                  const uint64_t bdl = ptx::sdesc_k128(ptx::smem_u32(b + (NSUB + s) * Cfg::B_BYTES));
+                  ptx::mma_tf32_cg2(ds, adl + off, bd + off, Cfg::IDESC, accum);
+                  ptx::mma_tf32_cg2(ds, ad + off, bdl + off, Cfg::IDESC, 1u);
+                  ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, 1u);
+                } else if (Cfg::ESZ == 2) {
+                  ptx::mma_bf16_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                } else {
+                  ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                }
+              }
             }
+            ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          ptx::mma_commit_cg2_mc(&tfull[slot], 0x3);
         }
-        ptx::mma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
-    // ===== Epilogue: TMEM → registers → fused op → global =====
-    const uint32_t q = warp - 4;   // == warp % 4: TMEM lane quarter this warp may access
+    // ===== Epilogue: TMEM → registers → fused op → global (8 warps) =====
+    const uint32_t q = warp & 3;               // TMEM lane quarter this warp may access
+    const uint32_t h = (warp - 4) >> 2;        // column half of the accumulator
+    EpiCtx<Cfg::STG_BUFS> cx;
+    cx.tm = &tmOut;
+    cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
+    cx.cur = 0;
+    cx.lane = lane;
+    const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    constexpr int HALF = Cfg::ACC_COLS / 2;
     int it = 0;
-    for (int t = blockIdx.x; t < sched.num_tiles; t += gridDim.x, ++it) {
+    for (int t = cid; t < sched.num_tiles; t += ncl) {
       int ti, tj;
       sched.tile(t, ti, tj);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      const int64_t row_lo = (int64_t)ti * Cfg::BM + q * 32;
-      const int64_t row = row_lo + lane;
+      const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
+      for (int c = 0; c < nchunks; ++c, ++it) {
+        const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
+        const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
+        ptx::mbar_wait(&tfull[slot], acc_phase);
+        ptx::tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < Cfg::BN / 32; ++c) {
-        const int64_t col0 = (int64_t)tj * Cfg::BN + c * 32;
-        if (!epi.chunk_needed(row_lo, row_lo + 31, col0)) continue;
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * Cfg::BN + c * 32, r);
-        ptx::tmem_ld_wait();
-        epi(row, col0, r);
+        for (int cc = 0; cc < HALF / 32; ++cc) {
+          const int64_t col0 = (int64_t)tj * Cfg::BN + h * HALF + cc * 32;
+          if (!epi.chunk_needed(row_lo, col0)) continue;
+          uint32_t r[32];
+          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF + cc * 32, r);
+          ptx::tmem_ld_wait();
+          epi(cx, row_lo, col0, r, c, nchunks);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) ptx::bulk_wait_all();
   }
-  __syncthreads();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    ptx::tmem_dealloc_cg2(tmem_base, 512);
   }
 #endif
 }

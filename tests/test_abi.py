@@ -80,8 +80,8 @@ def test_phi_row_split_covers_and_balances():
             for (b0, e0), (b1, e1) in zip(ranges, ranges[1:]):
                 assert e0 == b1
             for b, e in ranges:
-                assert b % 128 == 0 and (e == n or e % 128 == 0)
-            if n >= 128 * 8 * world:
+                assert b % 256 == 0 and (e == n or e % 256 == 0)
+            if n >= 256 * 8 * world:
                 area = [sum(n - i for i in range(b, e)) for b, e in ranges]
                 assert max(area) / min(area) < 1.05
 
@@ -114,8 +114,8 @@ def test_validation_rejects_before_any_launch():
     s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 0, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_WORKSPACE
-    # Φ row range must start on a 128-row boundary
-    s = lib.rf_phi_closed_form(ctypes.c_void_p(addr16), 64, 64, 256, 0, 1.0, None, 4, 0, 64, 256,
+    # Φ row range must start on a 256-row boundary
+    s = lib.rf_phi_closed_form(ctypes.c_void_p(addr16), 64, 64, 512, 0, 1.0, None, 4, 0, 128, 512,
                                ctypes.c_void_p(addr16), 256, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"row range" in lib.rf_last_error()
 

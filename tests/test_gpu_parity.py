@@ -59,7 +59,7 @@ def upper_idx(n):
 
 
 # ------------------------------------------------------------------------------------------------ G
-def _gram_case(n, p, m, act, prec, out="upper", seed=0):
+def _gram_case(n, p, m, act, prec, out="upper", seed=0, tol=None):
     rng = np.random.default_rng(seed)
     X = rng.standard_normal((n, p)) / math.sqrt(p)
     W = rng.standard_normal((m, p))
@@ -71,7 +71,7 @@ def _gram_case(n, p, m, act, prec, out="upper", seed=0):
     Gc = back(G)
     I, J = upper_idx(n)
     r = report(f"G n={n} p={p} m={m} {act} {prec} {out}", Gc[I, J], ref[I, J], I, J)
-    assert r <= TOL[prec]
+    assert r <= (TOL[prec] if tol is None else tol)
     L = np.tril_indices(n, -1)
     if out == "upper":
         assert np.all(Gc[L] == SENTINEL), "UPPER mode wrote below the diagonal"
@@ -95,8 +95,9 @@ def test_gram_multi_tile_full(prec):
 
 @pytest.mark.parametrize("prec", ["fp64", "fp32", "3xtf32", "bf16"])
 def test_gram_degenerate_sizes(prec):
-    _gram_case(1, 8, 1, "erf", prec, out="full", seed=2)    # n = m = 1
-    _gram_case(129, 8, 1, "tanh", prec, seed=3)             # rank-one G, tile edge + 1
+    # m = 1: no averaging over features, so BF16 Σ rounding (unit 2^-8 per factor) is not diluted
+    _gram_case(1, 8, 1, "erf", prec, out="full", seed=2, tol=2 * 2.0 ** -8 if prec == "bf16" else None)
+    _gram_case(129, 8, 1, "tanh", prec, seed=3, tol=2 * 2.0 ** -8 if prec == "bf16" else None)  # rank one
     _gram_case(256, 8, 512, "tanh", prec, seed=4)           # exact tile multiples
 
 
