@@ -76,7 +76,7 @@ def _gram_case(n, p, m, act, prec, out="upper", seed=0, tol=None):
     if out == "upper":
         assert np.all(Gc[L] == SENTINEL), "UPPER mode wrote below the diagonal"
     else:
-        assert rel_fro(Gc, ref) <= TOL[prec]
+        assert rel_fro(Gc, ref) <= (TOL[prec] if tol is None else tol)
         assert np.array_equal(Gc, Gc.T)
 
 
