@@ -160,8 +160,7 @@ class ClockSampler:
         if not sm:
             return None
         sm.sort()
-        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": busy[len(busy) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+        return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
                 "samples": len(sm)}
 
 

@@ -200,6 +200,13 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Row tiles per L2 raster group (tc_gemm.cuh Sched).  Env RF_GM overrides (experiments).
+int raster_gm(int def) {
+  const char* e = std::getenv("RF_GM");
+  if (e && *e && std::atoi(e) > 0) return std::atoi(e);
+  return def;
+}
+
 // K-blocks per accumulation chunk (0 = whole K in one chunk).  Env RF_KCHUNK overrides (experiments).
 int kchunk_for(rf_prec prec, int def) {
   const char* e = std::getenv("RF_KCHUNK");
@@ -355,7 +362,8 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   if ((s = make_tmap(&tB, WB, bf, g.m_local, g.p, ldwb, 128))) return s;
   if (kSplit != 3) { tAl = tA; tBl = tB; }
   const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
-  const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0);
+  const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
+                                         raster_gm(8));
   rfk::EpiSigma<kOut> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
   if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
 
@@ -371,7 +379,8 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   if (!tma_out) tO = tA;
   const int kb4 = (int)((g.m_local + C4::BK - 1) / C4::BK);
   const rfk::Sched s4 =
-      rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4);
+      rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4,
+                       raster_gm(8));
   rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
   if ((s = launch_tc<C4>("K4_syrk", tA, tB, tAl, tBl, tO, s4, e4, g.sms, g.st))) return s;
   return ok();
@@ -724,7 +733,12 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   std::memcpy(rm.kd, mloc.kd, sizeof(rm.kd));
   rm.inv_st = 1.0 / std::sqrt(tau);
   const int cgrid = (int)((n + 255) / 256);
-  const double k22h = 0.5 * mloc.kd[2][2];
+  // C0(s), C1(s) coefficients of the regrouped EQ1 (rf_common.cuh), s = u_b/√τ
+  const double e0 = mloc.kd[0][0] - mloc.kd[1][1] + 0.5 * mloc.kd[2][2];
+  const double e1 = mloc.kd[1][1] - mloc.kd[2][2];
+  const double e2 = 0.5 * mloc.kd[2][2];
+  const double f0 = mloc.kd[0][1] - mloc.kd[1][2];
+  const double f1 = mloc.kd[1][2];
   const int full = out == RF_OUT_FULL;
   if (prec == RF_PREC_FP64) {
     rfk::RowCoefD* rc = (rfk::RowCoefD*)(w + pl.off_rc);
@@ -735,8 +749,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     }
     RF_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
-    rfk::SimtEq1<double, rfk::RowCoefD> e{(double*)Phi, ldphi, n, rc, nj, mloc.kd[0][0], mloc.kd[1][1], k22h,
-                                          mloc.kd[0][1], mloc.kd[1][2], rm.inv_st, full};
+    rfk::SimtEq1<double, rfk::RowCoefD> e{(double*)Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full};
     return (s = launch_simt<double>("K6_simt_xtx_eq1", (const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
                                     (int)((row_end + 63) / 64), e, st))
                ? s
@@ -752,9 +765,8 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   ++g_launches;
   if (row_end <= row_begin) return ok();
   if (prec == RF_PREC_FP32) {
-    rfk::SimtEq1<float, rfk::RowCoef> e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1],
-                                        (float)k22h, (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st,
-                                        full};
+    rfk::SimtEq1<float, rfk::RowCoef> e{(float*)Phi, ldphi, n, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
+                                        (float)f1, full};
     return (s = launch_simt<float>("K6_simt_xtx_eq1", (const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
                                    (int)((row_end + 63) / 64), e, st))
                ? s
@@ -763,8 +775,8 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
   CUtensorMap tA, tAl, tO;
   const bool tma_out = make_tmap_out(&tO, Phi, n, n, ldphi);
-  rfk::EpiEq1 e{(float*)Phi, ldphi, n, rc, nj, (float)mloc.kd[0][0], (float)mloc.kd[1][1], (float)k22h,
-                (float)mloc.kd[0][1], (float)mloc.kd[1][2], (float)rm.inv_st, full, tma_out ? 1 : 0};
+  rfk::EpiEq1 e{(float*)Phi, ldphi, n, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0, (float)f1, full,
+                tma_out ? 1 : 0};
   const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
   if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
     const bool bf = prec == RF_PREC_BF16;
@@ -772,11 +784,11 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     if (!tma_out) tO = tA;
     if (bf) {
       using C = rfk::TcCfg<1, 1, 256>;
-      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0);
+      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
       if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     } else {
       using C = rfk::TcCfg<2, 1, 256>;
-      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0);
+      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
       if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     }
   } else {
@@ -788,7 +800,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
     if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
     if (!tma_out) tO = tA;
     const rfk::Sched sc =
-        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0);   // EQ1 is nonlinear in g
+        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));   // EQ1 is nonlinear in g
     if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
   }
   return ok();

@@ -84,16 +84,16 @@ struct RowMoments {
   double inv_st;   // 1/√τ
 };
 
-// Per-row coefficients (fp64 arithmetic, stored as RC = RowCoef (f32) or RowCoefD (f64)); also ‖x_j‖²
-// as the output type for the column side of the epilogue.
+// Per-row coefficients of the regrouped EQ1 (rf_common.cuh), fp64 arithmetic, stored as RC = RowCoef
+// (f32) or RowCoefD (f64); the column side gets ‖x_j‖²/τ.
 template <typename RC, typename NT>
 __global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm2, int64_t n, RowMoments m,
-                                                  RC* __restrict__ rc, NT* __restrict__ nrm2_out) {
+                                                  RC* __restrict__ rc, NT* __restrict__ njt_out) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= n) return;
   const double r2 = nrm2[i];
-  const double ua = sqrt(r2);
-  const double al = ua * m.inv_st - 1.0;
+  const double ua = sqrt(r2);                       // u_a = ‖x_i‖
+  const double al = ua * m.inv_st - 1.0;            // α = u_a/√τ − 1
   const double h = 0.5 * al * al;
   const double A0 = m.kd[0][0] + al * m.kd[1][1] + h * m.kd[2][2];
   const double A1 = m.kd[1][0] + al * m.kd[2][1] + h * m.kd[3][2];
@@ -102,13 +102,11 @@ __global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm
   c.a0 = A0;
   c.a1 = A1;
   c.a2h = 0.5 * m.kd[0][2] * A2;
-  c.c = m.inv_st / ua;
-  c.inv_ua = 1.0 / ua;
-  c.nrm2 = r2;
-  c.nu_diag = ua * m.inv_st;
-  c.pad = 0;
+  c.c = m.inv_st / ua;                              // ν = g·c
+  c.nu_diag = ua * m.inv_st;                        // ν on the diagonal (v_b = u_a)
+  c.pad0 = c.pad1 = c.pad2 = 0;
   rc[i] = c;
-  nrm2_out[i] = (NT)r2;
+  njt_out[i] = (NT)(r2 * m.inv_st * m.inv_st);      // ‖x_j‖²/τ
 }
 
 // hi = tf32 truncation of x, lo = x − hi (exact).  2-D: rows × cols with independent strides.

@@ -37,14 +37,13 @@ struct SimtEq1 {
   T* Phi;
   int64_t ld, n;
   const RC* rc;
-  const T* nrm2;
-  T k00, k11, k22h, k01, k12, inv_st;
+  const T* njt;          // ‖x_j‖²/τ
+  T e0, e1, e2, f0, f1;
   int full;
   __device__ __forceinline__ void operator()(int64_t i, int64_t j, T g) const {
     if (i < n && j < n && j >= i) {
       const RC c = rc[i];
-      T v = eq1_entry<T>(g, (T)c.a0, (T)c.a1, (T)c.a2h, (T)c.c, (T)c.inv_ua, nrm2[j], i == j, (T)c.nu_diag, k00,
-                         k11, k22h, k01, k12, inv_st);
+      T v = eq1_entry<T>(g, (T)c.a0, (T)c.a1, (T)c.a2h, (T)c.c, njt[j], i == j, (T)c.nu_diag, e0, e1, e2, f0, f1);
       Phi[i * ld + j] = v;
       if (full && j > i) Phi[j * ld + i] = v;
     }

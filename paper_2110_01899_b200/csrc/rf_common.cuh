@@ -35,38 +35,44 @@ __device__ __forceinline__ float tf32_hi(float x) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Per-row EQ1 data (DESIGN.md §5 "K1/K5"): for row i with α_i = ‖x_i‖/√τ − 1
-//   a0 = A0(α_i), a1 = A1(α_i), a2h = ½⟨0,2⟩A2(α_i), c = 1/(√τ‖x_i‖), inv_ua = 1/‖x_i‖, nrm2 = ‖x_i‖²
+// EQ1 (readings R1-R4) regrouped for the epilogue (K5).  With
+//   α = u_a/√τ − 1, s = u_b/√τ (= β + 1), ν = v_b/√τ:
+//   Φ = A0(α)·C0(s) + ν·(A1(α)·C1(s) + ν·½⟨0,2⟩A2(α))
+//   A_j(α) = ⟨j,0⟩ + α⟨j+1,1⟩ + (α²/2)⟨j+2,2⟩                     — per row (k_row_coef)
+//   C0(s) = e0 + s(e1 + s e2), C1(s) = f0 + s f1                 — the β-polynomials re-expanded in s:
+//   e0 = ⟨0,0⟩ − ⟨1,1⟩ + ½⟨2,2⟩, e1 = ⟨1,1⟩ − ⟨2,2⟩, e2 = ½⟨2,2⟩, f0 = ⟨0,1⟩ − ⟨1,2⟩, f1 = ⟨1,2⟩.
+// Per entry, from g = x_iᵀx_j: ν = g·c_i with c_i = 1/(√τ‖x_i‖); s = √max(0, ‖x_j‖²/τ − ν²)
+// (Gram–Schmidt P:1016-1018 scaled by 1/√τ).  Diagonal (R6): s = 0, ν = ‖x_i‖/√τ.
 // ------------------------------------------------------------------------------------------
 struct __align__(32) RowCoef {
-  float a0, a1, a2h, c, inv_ua, nrm2, nu_diag, pad;
+  float a0, a1, a2h, c, nu_diag, pad0, pad1, pad2;
 };
 struct RowCoefD {
-  double a0, a1, a2h, c, inv_ua, nrm2, nu_diag, pad;
+  double a0, a1, a2h, c, nu_diag, pad0, pad1, pad2;
 };
 
-// β-polynomial coefficients: C0(β) = k00 + β(k11 + β k22h), C1(β) = k01 + β k12; inv_st = 1/√τ.
-struct Eq1Consts {
-  double k00, k11, k22h, k01, k12, inv_st;
-};
+__device__ __forceinline__ float sqrt_fast(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double sqrt_fast(double x) { return sqrt(x); }
 
 template <typename T>
-__device__ __forceinline__ T eq1_entry(T g, T a0, T a1, T a2h, T c, T inv_ua, T nrm2_j, bool diag, T nu_diag,
-                                       T k00, T k11, T k22h, T k01, T k12, T inv_st) {
-  T nu, beta;
+__device__ __forceinline__ T eq1_entry(T g, T a0, T a1, T a2h, T c, T njt, bool diag, T nu_diag, T e0, T e1, T e2,
+                                       T f0, T f1) {
+  T nu = g * c;
+  T r = fma(-nu, nu, njt);
+  r = r > T(0) ? r : T(0);
+  T s = sqrt_fast(r);
   if (diag) {
-    nu = nu_diag;                  // v_b = u_a ⇒ ν = ‖x_i‖/√τ
-    beta = T(-1);                  // u_b = 0
-  } else {
-    T vb = g * inv_ua;             // v_b = x_iᵀx_j/‖x_i‖
-    T r = nrm2_j - vb * vb;        // u_b² = ‖x_j‖² − v_b²
-    r = r > T(0) ? r : T(0);
-    beta = sqrt(r) * inv_st - T(1);
-    nu = g * c;
+    nu = nu_diag;
+    s = T(0);
   }
-  T C0 = k00 + beta * (k11 + beta * k22h);
-  T C1 = k01 + beta * k12;
-  return a0 * C0 + nu * (a1 * C1 + nu * a2h);
+  const T C0 = fma(s, fma(s, e2, e1), e0);
+  const T C1 = fma(s, f1, f0);
+  const T inner = fma(nu, a2h, a1 * C1);
+  return fma(nu, inner, a0 * C0);
 }
 
 }  // namespace rfk

@@ -60,6 +60,12 @@ struct TcCfg {
 // Pair-tile scheduler.  Rows of 256, columns of BN.  Rectangular: row tiles [row_tile0, row_tile1) × all
 // column tiles.  Triangular: row tile I needs the column tiles J ≥ floor(256 I / BN) (every tile holding
 // an entry j ≥ i).  Work item = (tile, K-chunk); a cluster processes all chunks of a tile in order.
+//
+// L2-aware order: row tiles are taken in groups of `gm`; inside a group the walk is column-major (down
+// the gm rows, then the next column), so the ~74 tiles in flight at once cover gm row panels × ~74/gm
+// column panels instead of 1 × 74.  Measured on configs[3] (K4): the row-major walk re-read Σᵀ ≈ 155×
+// from DRAM (1.33 TB per launch); grouping bounds the re-reads to one pass of the column panels per
+// group (and all clusters advance through K in near lockstep, so only K-slices need to stay in L2).
 struct Sched {
   int tri;
   int shift;            // log2(BN/256)
@@ -69,29 +75,51 @@ struct Sched {
   int num_kb;           // K-blocks of the whole reduction
   int kchunk;           // K-blocks per chunk
   int nchunks;
+  int gm;               // row tiles per raster group
 
-  __host__ __device__ long long jmin_sum(long long I) const {   // Σ_{r < I} (r >> shift)
-    if (shift == 0) return I * (I - 1) / 2;
-    long long q = I >> 1;
-    return (I & 1) ? q * q : q * (q - 1);
-  }
-  __host__ __device__ long long prefix(long long I) const { return I * (long long)tiles_n - jmin_sum(I); }
-  __host__ __device__ void tile(int t, int& ti, int& tj) const {
+  struct Group {
+    int I0, I1, J0, Jf;
+    long long P, cnt;
+  };
+  __host__ __device__ Group group(int I0) const {
+    Group g;
+    g.I0 = I0;
+    g.I1 = I0 + gm < row_tile1 ? I0 + gm : row_tile1;
+    const long long rows = g.I1 - g.I0;
     if (!tri) {
-      ti = row_tile0 + t / tiles_n;
-      tj = t % tiles_n;
+      g.J0 = g.Jf = 0;
+      g.P = 0;
+      g.cnt = rows * tiles_n;
+      return g;
+    }
+    g.J0 = I0 >> shift;
+    const int jf = (g.I1 - 1) >> shift;     // first column where every row of the group is needed
+    g.Jf = jf < tiles_n ? jf : tiles_n;
+    const long long a = g.J0, b = g.Jf;
+    g.P = ((b * (b + 1) - a * (a + 1)) / 2 << shift) - (b - a) * (long long)I0;   // partial columns [J0, Jf)
+    g.cnt = g.P + (tiles_n - g.Jf) * rows;
+    return g;
+  }
+  // tile (ti, tj) of index u inside group g
+  __host__ __device__ void in_group(const Group& g, long long u, int& ti, int& tj) const {
+    if (u < g.P) {
+      int J = g.J0;
+      for (;;) {
+        const long long rv = ((long long)(J + 1) << shift) - g.I0;
+        if (u < rv) break;
+        u -= rv;
+        ++J;
+      }
+      ti = g.I0 + (int)u;
+      tj = J;
       return;
     }
-    const long long target = prefix(row_tile0) + t;
-    int lo = row_tile0, hi = row_tile1 - 1;   // largest I with prefix(I) <= target
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix(mid) <= target) lo = mid; else hi = mid - 1;
-    }
-    ti = lo;
-    tj = (lo >> shift) + (int)(target - prefix(lo));
+    u -= g.P;
+    const int rows = g.I1 - g.I0;
+    tj = g.Jf + (int)(u / rows);
+    ti = g.I0 + (int)(u % rows);
   }
-  static Sched make(int tri, int bn, int row_tile0, int row_tile1, int tiles_n, int num_kb, int kchunk) {
+  static Sched make(int tri, int bn, int row_tile0, int row_tile1, int tiles_n, int num_kb, int kchunk, int gm = 8) {
     Sched s;
     s.tri = tri;
     s.shift = bn == 512 ? 1 : 0;
@@ -101,8 +129,31 @@ struct Sched {
     s.num_kb = num_kb;
     s.kchunk = (kchunk <= 0 || kchunk > num_kb) ? (num_kb > 0 ? num_kb : 1) : kchunk;
     s.nchunks = num_kb > 0 ? (num_kb + s.kchunk - 1) / s.kchunk : 1;
-    s.num_tiles = tri ? (int)(s.prefix(row_tile1) - s.prefix(row_tile0)) : (row_tile1 - row_tile0) * tiles_n;
+    s.gm = gm > 0 ? gm : 1;
+    long long tot = 0;
+    for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
+    s.num_tiles = (int)tot;
     return s;
+  }
+};
+
+// Monotone cursor over the tile order (each cluster visits t = cid, cid + ncl, … in increasing order, so
+// advancing group by group is amortised O(1)).
+struct TileCursor {
+  const Sched* s;
+  Sched::Group g;
+  long long base;
+  __device__ __forceinline__ void init(const Sched* sp) {
+    s = sp;
+    base = 0;
+    g = s->group(s->row_tile0);
+  }
+  __device__ __forceinline__ void get(long long t, int& ti, int& tj) {
+    while (t >= base + g.cnt) {
+      base += g.cnt;
+      g = s->group(g.I1);
+    }
+    s->in_group(g, t - base, ti, tj);
   }
 };
 
@@ -272,8 +323,8 @@ struct EpiEq1 {
   float* Phi;
   int64_t ld, n;
   const RowCoef* rc;     // per row
-  const float* nrm2;     // ‖x_j‖² per column
-  float k00, k11, k22h, k01, k12, inv_st;
+  const float* njt;      // ‖x_j‖²/τ per column
+  float e0, e1, e2, f0, f1;
   int full;
   int use_tma;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
@@ -288,19 +339,24 @@ struct EpiEq1 {
     if (col0 + 32 <= n) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(nrm2 + col0) + q);
+        const float4 t = __ldg(reinterpret_cast<const float4*>(njt + col0) + q);
         nj[4 * q] = t.x; nj[4 * q + 1] = t.y; nj[4 * q + 2] = t.z; nj[4 * q + 3] = t.w;
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) nj[e] = (col0 + e < n) ? __ldg(nrm2 + col0 + e) : 1.f;
+      for (int e = 0; e < 32; ++e) nj[e] = (col0 + e < n) ? __ldg(njt + col0 + e) : 1.f;
     }
     float v[32];
+    if (col0 + 31 >= row_lo && col0 <= row_lo + 31) {   // chunk holds diagonal entries (warp-uniform)
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      const float g = __uint_as_float(r[e]);
-      v[e] = eq1_entry<float>(g, c.a0, c.a1, c.a2h, c.c, c.inv_ua, nj[e], col0 + e == row, c.nu_diag, k00, k11,
-                              k22h, k01, k12, inv_st);
+      for (int e = 0; e < 32; ++e)
+        v[e] = eq1_entry<float>(__uint_as_float(r[e]), c.a0, c.a1, c.a2h, c.c, nj[e], col0 + e == row, c.nu_diag, e0,
+                                e1, e2, f0, f1);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        v[e] = eq1_entry<float>(__uint_as_float(r[e]), c.a0, c.a1, c.a2h, c.c, nj[e], false, c.nu_diag, e0, e1, e2,
+                                f0, f1);
     }
     if (use_tma && col0 >= row_lo + 31) {
       cx.store_block(row_lo, col0, v);
@@ -394,9 +450,11 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
       int stage = 0;
       uint32_t phase = 0;
+      TileCursor cur;
+      cur.init(&sched);
       for (int t = cid; t < sched.num_tiles; t += ncl) {
         int ti, tj;
-        sched.tile(t, ti, tj);
+        cur.get(t, ti, tj);
         const int ra = ti * Cfg::BM + (int)rank * 128;
         const int rb = tj * Cfg::BN + (int)rank * 128;
         for (int c = 0; c < nchunks; ++c) {
@@ -482,9 +540,11 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     constexpr int HALF = Cfg::ACC_COLS / 2;
     int it = 0;
+    TileCursor cur;
+    cur.init(&sched);
     for (int t = cid; t < sched.num_tiles; t += ncl) {
       int ti, tj;
-      sched.tile(t, ti, tj);
+      cur.get(t, ti, tj);
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
