@@ -76,6 +76,15 @@ struct Sched {
   int kchunk;           // K-blocks per chunk
   int nchunks;
   int gm;               // row tiles per raster group
+  // Soft lockstep (K4): every `lock_ks` K-blocks the leader CTA's producer publishes its cluster's
+  // K-block count in prog[cluster] and waits (bounded, ≤ 50 µs per check) until the slowest cluster is
+  // within `lock_w` K-blocks.  Tiles of one raster wave share Σᵀ panels, but a K-block row slice stays in
+  // L2 only ~25 µs at the kernel's fill rate; unsynchronised clusters drift further apart than that and
+  // re-read the shared panels from DRAM (measured: 1.16 TB of DRAM reads per configs[3] launch for 8.6 GB
+  // of Σᵀ).  prog == nullptr disables it.  The wait is bounded, so co-residency of all clusters is not
+  // required for progress.
+  uint32_t* prog;
+  int lock_w, lock_ks;
 
   struct Group {
     int I0, I1, J0, Jf;
@@ -130,6 +139,9 @@ struct Sched {
     s.kchunk = (kchunk <= 0 || kchunk > num_kb) ? (num_kb > 0 ? num_kb : 1) : kchunk;
     s.nchunks = num_kb > 0 ? (num_kb + s.kchunk - 1) / s.kchunk : 1;
     s.gm = gm > 0 ? gm : 1;
+    s.prog = nullptr;
+    s.lock_w = 0;
+    s.lock_ks = 8;
     long long tot = 0;
     for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
     s.num_tiles = (int)tot;
@@ -444,22 +456,37 @@ __global__ void __launch_bounds__(384, 1)
   const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
-      const uint64_t pol = ptx::policy_evict_normal();
-      const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      TileCursor cur;
-      cur.init(&sched);
-      for (int t = cid; t < sched.num_tiles; t += ncl) {
-        int ti, tj;
-        cur.get(t, ti, tj);
-        const int ra = ti * Cfg::BM + (int)rank * 128;
-        const int rb = tj * Cfg::BN + (int)rank * 128;
-        for (int c = 0; c < nchunks; ++c) {
-          const int kb1 = min(num_kb, (c + 1) * kchunk);
-          for (int kb = c * kchunk; kb < kb1; ++kb) {
+    // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
+    // The whole warp walks the loop (lane 0 issues); the leader's warp also runs the lockstep check.
+    const bool lock = sched.prog != nullptr && rank == 0;
+    const uint64_t pol = ptx::policy_evict_normal();
+    const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t step = 0;
+    TileCursor cur;
+    cur.init(&sched);
+    for (int t = cid; t < sched.num_tiles; t += ncl) {
+      int ti, tj;
+      cur.get(t, ti, tj);
+      const int ra = ti * Cfg::BM + (int)rank * 128;
+      const int rb = tj * Cfg::BN + (int)rank * 128;
+      for (int c = 0; c < nchunks; ++c) {
+        const int kb1 = min(num_kb, (c + 1) * kchunk);
+        for (int kb = c * kchunk; kb < kb1; ++kb, ++step) {
+          if (lock && (step % (uint32_t)sched.lock_ks) == 0) {
+            if (lane == 0) ptx::st_relaxed_gpu(sched.prog + cid, step);
+            const uint32_t need = step > (uint32_t)sched.lock_w ? step - (uint32_t)sched.lock_w : 0u;
+            const uint64_t t0 = ptx::globaltimer_ns();
+            for (;;) {
+              uint32_t mn = 0xFFFFFFFFu;
+              for (int q = (int)lane; q < ncl; q += 32) mn = min(mn, ptx::ld_relaxed_gpu(sched.prog + q));
+              mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+              if (mn >= need || ptx::globaltimer_ns() - t0 > 50000ull) break;
+              __nanosleep(256);
+            }
+          }
+          if (lane == 0) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
             const uint32_t fb = full0 + stage * 8;
@@ -475,11 +502,13 @@ __global__ void __launch_bounds__(384, 1)
               for (int s = 0; s < NSUB; ++s)
                 ptx::tma_load_2d_cg2(b + (NSUB + s) * Cfg::B_BYTES, &tmB_lo, fb, k, rb + 256 * s, pol);
             }
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
+    if (lock && lane == 0) ptx::st_relaxed_gpu(sched.prog + cid, 0xFFFFFFFFu);   // done: never the minimum
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       // ===== MMA issuer (leader CTA, single thread) =====
