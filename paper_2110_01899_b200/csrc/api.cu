@@ -381,8 +381,16 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
   const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
                                          raster_gm(8));
-  rfk::EpiSigma<kOut> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
-  if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+  if (g.act == RF_ACT_TANH) {
+    rfk::EpiSigma<kOut, RF_ACT_TANH> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+  } else if (g.act == RF_ACT_ERF) {
+    rfk::EpiSigma<kOut, RF_ACT_ERF> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+  } else {
+    rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+  }
 
   if ((s = make_tmap(&tA, S0, bf, g.n, g.m_local, g.pl.ldS, 128))) return s;
   tB = tA;

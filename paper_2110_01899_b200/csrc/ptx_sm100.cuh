@@ -179,8 +179,13 @@ __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Arrive on a barrier of another CTA of the cluster.  Default (.release.cta) semantics: the only thing the
+// arrive publishes is the completion of this warp's tcgen05.ld reads (ordered by tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync), so no generic-proxy store fence is needed.  (.release.cluster here
+// compiled to MEMBAR.ALL.GPU + ERRBAR: every epilogue warp waited for its global stores to drain before
+// handing the accumulator back — the top stall of K3 in ncu.)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load by either CTA of a pair; completion bytes are signalled on the LEADER's barrier (cluster addr).
 __device__ __forceinline__ void tma_load_2d_cg2(void* smem_dst, const CUtensorMap* m, uint32_t bar_cluster,

@@ -24,6 +24,35 @@ __device__ __forceinline__ double act_f64(int act, double x) {
   if (act == RF_ACT_ERF) return erf(x);
   return 0.5 * tanh(0.5 * x);
 }
+// Compile-time σ for the tensor-core K3 epilogue.
+template <int kAct>
+__device__ __forceinline__ float act_fixed(float x) {
+  if (kAct == RF_ACT_TANH) return tanhf(x);
+  if (kAct == RF_ACT_ERF) return erff(x);
+  return 0.5f * tanhf(0.5f * x);
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// σ for BF16-stored Σ (K3, RF_PREC_BF16): sigmoid(x) − ½ = 1/(1 + 2^(−x·log2 e)) − ½ and
+// tanh(x) = 2/(1 + 2^(−2x·log2 e)) − 1 on the MUFU pipe (one EX2 + one RCP).  Absolute error ≲ 3e-7
+// (ex2/rcp.approx are within ~2 ulp), i.e. ≥ 30× below half an ulp of the bf16 value it is rounded to for
+// |σ| ≥ 2^-6; both limits saturate correctly (2^+∞ → rcp → 0).  erf keeps the library erff.
+template <int kAct>
+__device__ __forceinline__ float act_bf16out(float x) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  if (kAct == RF_ACT_SIGMOID_HALF) return rcp_approx(1.0f + ex2_approx(-kLog2e * x)) - 0.5f;
+  if (kAct == RF_ACT_TANH) return fmaf(2.0f, rcp_approx(1.0f + ex2_approx(-2.0f * kLog2e * x)), -1.0f);
+  return erff(x);
+}
+
 template <typename T> __device__ __forceinline__ T act_t(int act, T x);
 template <> __device__ __forceinline__ float act_t<float>(int act, float x) { return act_f32(act, x); }
 template <> __device__ __forceinline__ double act_t<double>(int act, double x) { return act_f64(act, x); }

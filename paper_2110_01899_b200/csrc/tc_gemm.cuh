@@ -229,13 +229,13 @@ __device__ __forceinline__ void store_mirror(float* M, int64_t ld, int64_t n, in
 // ------------------------------------------------------------------------------------------
 
 // K3: Σᵀ[i][k] = σ(z), z = x_iᵀw_k.  kOut: 0 = bf16, 1 = fp32, 2 = fp32 hi/lo split (3×TF32).
-template <int kOut>
+// kAct = rf_act (compile time).
+template <int kOut, int kAct>
 struct EpiSigma {
   void* out0;
   void* out1;
   int64_t ld;       // elements
   int64_t M, N;     // n rows (samples), m_local columns (features)
-  int act;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
@@ -244,7 +244,8 @@ struct EpiSigma {
     if (row >= M) return;
     float s[32];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) s[e] = act_f32(act, __uint_as_float(r[e]));
+    for (int e = 0; e < 32; ++e)
+      s[e] = kOut == 0 ? act_bf16out<kAct>(__uint_as_float(r[e])) : act_fixed<kAct>(__uint_as_float(r[e]));
     const bool full = col0 + 32 <= N;
     if (kOut == 0) {
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(out0) + row * ld + col0;
@@ -510,8 +511,10 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (lock && lane == 0) ptx::st_relaxed_gpu(sched.prog + cid, 0xFFFFFFFFu);   // done: never the minimum
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
-      // ===== MMA issuer (leader CTA, single thread) =====
+    if (rank == 0) {
+      // ===== MMA issuer (leader CTA).  The whole warp walks the loop so that stage addresses and UMMA
+      // descriptors stay warp-uniform (uniform datapath, no per-MMA R2UR broadcasts); one elected lane
+      // issues the k-block's MMAs and commits.
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -526,34 +529,38 @@ __global__ void __launch_bounds__(384, 1)
           for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
-            const uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
-            const uint64_t ad = ptx::sdesc_k128(ptx::smem_u32(a));
+            const uint32_t a_s = ptx::smem_u32(sA + (size_t)(stage * NOPS) * Cfg::A_BYTES);
+            const uint32_t b_s = ptx::smem_u32(sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES);
+            const uint64_t ad = ptx::sdesc_k128(a_s);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
-              const uint64_t off = (uint64_t)((k * 32) >> 4);   // +32 B along K inside the swizzle row
-              const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+              for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+                const uint64_t off = (uint64_t)((k * 32) >> 4);   // +32 B along K inside the swizzle row
+                const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
 #pragma unroll
-              for (int s = 0; s < NSUB; ++s) {
-                const uint64_t bd = ptx::sdesc_k128(ptx::smem_u32(b + s * Cfg::B_BYTES));
-                const uint32_t ds = d + s * 256;
-                if (NOPS == 2) {
-                  const uint64_t adl = ptx::sdesc_k128(ptx::smem_u32(a + Cfg::A_BYTES));
-                  const uint64_t bdl = ptx::sdesc_k128(ptx::smem_u32(b + (NSUB + s) * Cfg::B_BYTES));
-                  ptx::mma_tf32_cg2(ds, adl + off, bd + off, Cfg::IDESC, accum);
-                  ptx::mma_tf32_cg2(ds, ad + off, bdl + off, Cfg::IDESC, 1u);
-                  ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, 1u);
-                } else if (Cfg::ESZ == 2) {
-                  ptx::mma_bf16_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
-                } else {
-                  ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                for (int s = 0; s < NSUB; ++s) {
+                  const uint64_t bd = ptx::sdesc_k128(b_s + s * Cfg::B_BYTES);
+                  const uint32_t ds = d + s * 256;
+                  if (NOPS == 2) {
+                    const uint64_t adl = ptx::sdesc_k128(a_s + Cfg::A_BYTES);
+                    const uint64_t bdl = ptx::sdesc_k128(b_s + (NSUB + s) * Cfg::B_BYTES);
+                    ptx::mma_tf32_cg2(ds, adl + off, bd + off, Cfg::IDESC, accum);
+                    ptx::mma_tf32_cg2(ds, ad + off, bdl + off, Cfg::IDESC, 1u);
+                    ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, 1u);
+                  } else if (Cfg::ESZ == 2) {
+                    ptx::mma_bf16_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                  } else {
+                    ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                  }
                 }
               }
+              ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
             }
-            ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+            __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          ptx::mma_commit_cg2_mc(&tfull[slot], 0x3);
+          if (ptx::elect_one()) ptx::mma_commit_cg2_mc(&tfull[slot], 0x3);
+          __syncwarp();
         }
       }
     }
