@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phi", action="store_true")
+    ap.add_argument("--comm-sms", type=int, default=8,
+                    help="N>1: SMs left free during K4 for the overlapped reduce-scatter kernels")
     return ap.parse_args()
 
 
@@ -175,6 +177,7 @@ def main():
 
     import paper_2110_01899_b200 as rf
     import synthetic
+    from paper_2110_01899_b200 import collective
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -206,11 +209,16 @@ def main():
         m0 = rank * m_local
         W_host = torch.from_numpy(synthetic.make_W(cfg, rows=np.arange(m0, m0 + m_local))).to(tdt).pin_memory()
         Wd = W_host.to(device)
-        if n % world:
-            raise SystemExit("n must be divisible by the number of GPUs for the G reduce-scatter")
-        G = torch.empty((n, n), dtype=torch.float32, device=device)
-        ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
-        G_own = torch.empty((n // world, n), dtype=torch.float32, device=device) if world > 1 else G
+        if world == 1:
+            G = torch.empty((n, n), dtype=torch.float32, device=device)
+            ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
+            G_own = G
+        else:
+            # G5: K4 writes packed triangle tiles; chunked NCCL reduce-scatter overlapped on a comm stream
+            rs = collective.GramReduceScatter(n, p, m_local, m, cfg.act, prec, nchunks=16,
+                                              max_sms=torch.cuda.get_device_properties(device).multi_processor_count
+                                              - args.comm_sms)
+            G_own = rs.recv
     if do_phi:
         rb, re_ = rf.rf_phi_row_split(n, world, rank)
         Phi = torch.empty((n, n), dtype=torch.float32, device=device)
@@ -219,10 +227,11 @@ def main():
 
     def step():
         if do_gram:
-            rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="upper", m_total=m, G=G, ws=ws_g)
+            if world == 1:
+                rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="upper", m_total=m, G=G, ws=ws_g)
+            else:
+                rs(Xd, Wd)
             launches[0] += rf.rf_last_launch_count()
-            if world > 1:
-                dist.reduce_scatter_tensor(G_own, G, op=dist.ReduceOp.SUM)
         if do_phi:
             rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="upper", row_begin=rb, row_end=re_,
                                   Phi=Phi, ws=ws_p)
@@ -371,7 +380,8 @@ def main():
             "data": "synthetic (seeded PCG64 draws of BASELINE.json configs; no dataset)",
             "config": {"workload": f"configs[{args.config}] {cfg.name}" + (" + Φ on the same X" if do_phi and do_gram else ""),
                        "p": p, "n": n, "m": m, "act": cfg.act, "prec": prec,
-                       "parallelism": (f"G: W sharded over m ({world} ranks) + NCCL reduce-scatter of G rows; "
+                       "parallelism": (f"G: W sharded over m ({world} ranks) + chunked NCCL reduce-scatter of "
+                                       f"packed triangle tiles overlapped with K4; "
                                        f"Φ: row blocks, no collective") if world > 1 else "single GPU",
                        "l2": "no flush: inputs/workspace/outputs per step ≫ 126 MB L2"},
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),

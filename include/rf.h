@@ -153,6 +153,70 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
  */
 rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end);
 
+/* =============================================================================================
+ * G5 — multi-GPU G: feature sharding + reduce-scatter of PACKED TRIANGLE TILES.
+ * G is a sum over the m features (Eq. def_Gram), so rank r computes the partial
+ * G_r = (1/m_total) Σ_{k ∈ its W rows} σ(Xᵀw_k)σ(w_kᵀX) and G = Σ_r G_r.  Instead of a dense n×n partial,
+ * rf_gram_packed has K4 write each 256×256 tile (I, J ≥ I … see below) of the partial straight into a
+ * SEND buffer laid out for ncclReduceScatter:
+ *
+ *   chunk-major:  send = [chunk 0 | chunk 1 | …],  chunk c = [owner 0 | owner 1 | … | owner R−1],
+ *                 owner block = chunk_slots[c] tiles of 256×256 fp32, row-major inside a tile (ld 256).
+ *
+ * Chunks are runs of K4's 256-row raster groups in schedule order, so chunk c is complete early in the
+ * launch; within a chunk, the tiles (in K4's schedule order, u = 0, 1, …) are dealt round-robin to owners
+ * (owner = u mod R, slot = u div R), which balances the ownership to ±1 tile per chunk.  A reduce-scatter of
+ * chunk c (count = chunk_slots[c]·65536 per rank) leaves rank r with the SUMMED tiles of its slots, at
+ * chunk_recv_off[c] of its receive buffer.  rf_pack_tile_map says which tile each received slot is.
+ * Every tile K4 computes is stored whole, so a slot holds valid G entries everywhere (tiles that straddle
+ * the diagonal hold both G[i][j] and its mirror; entries with i or j ≥ n are 0).  The set of tiles covers
+ * every entry (i, j) with j ≥ i at least once.
+ *
+ * Overlap: K4 counts finished tiles per chunk in `chunk_sync` (device uint32[nchunks], zeroed by the caller
+ * before the first epoch); rf_stream_wait_chunk enqueues on a (communication) stream a wait until chunk c of
+ * call `epoch` (1, 2, … per rf_gram_packed call with the same chunk_sync) is complete, after which that
+ * stream may run the reduce-scatter of chunk c while K4 continues with chunk c+1.  Launch K4 on max_sms < all
+ * SMs so the collective's kernels have SMs to run on.
+ * ============================================================================================= */
+#define RF_PACK_TILE 256
+#define RF_PACK_MAX_CHUNKS 64
+typedef struct {
+  int64_t n;
+  int32_t world, nchunks;
+  int32_t prec;                                   /* rf_prec the plan was made for (K4 tile width) */
+  int32_t tiles_per_pair;                         /* 256×256 tiles per K4 pair tile (2 = 256×512 pair tiles) */
+  int64_t pair_tiles;                             /* K4 pair tiles in the triangle schedule */
+  int64_t send_elems;                             /* fp32 elements of the send buffer */
+  int64_t recv_elems;                             /* fp32 elements each rank receives */
+  int64_t chunk_tile0[RF_PACK_MAX_CHUNKS + 1];    /* first pair tile (schedule index) of chunk c */
+  int64_t chunk_slots[RF_PACK_MAX_CHUNKS];        /* 256×256 slots per owner in chunk c */
+  int64_t chunk_send_off[RF_PACK_MAX_CHUNKS + 1]; /* element offset of chunk c in the send buffer */
+  int64_t chunk_recv_off[RF_PACK_MAX_CHUNKS + 1]; /* element offset of chunk c in a receive buffer */
+} rf_pack_plan_t;
+
+/* Host.  nchunks ≤ RF_PACK_MAX_CHUNKS (clamped to the number of raster groups); prec ∈ {BF16, TF32, 3XTF32}. */
+rf_status rf_pack_plan(int64_t n, int32_t world, int32_t nchunks, rf_prec prec, rf_pack_plan_t* out);
+/* Host.  rc[2·s], rc[2·s+1] = (row tile I, column tile J) of receive slot s of `rank` (256-row/col tiles;
+ * entry (i, j) of G is element ((i − 256 I)·256 + (j − 256 J)) of the slot), or (−1, −1) for padding slots.
+ * rc holds 2 · recv_elems / 65536 int32. */
+rf_status rf_pack_tile_map(const rf_pack_plan_t* plan, int32_t rank, int32_t* rc);
+/* rf_gram's K3 + K4 with packed output (plan->prec must equal prec, plan->n must equal n).
+ *   send        device fp32[plan->send_elems]; every slot that holds a tile is written whole; padding
+ *               slots (rf_pack_tile_map gives (−1, −1)) are left untouched (their reduced value is garbage
+ *               and must be ignored).
+ *   chunk_sync  device uint32[plan->nchunks]; K4 adds 16 per finished pair tile (8 epilogue warps × 2 CTAs).
+ *   epoch       1-based count of calls made with this chunk_sync.
+ *   max_sms     ≤ 0: all SMs; else K4/K3 use at most this many SMs (rounded down to CTA pairs).
+ * ws as rf_gram (rf_gram_workspace_size). */
+rf_status rf_gram_packed(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
+                         int64_t p, int64_t n, int64_t m_local, int64_t m_total, rf_act act, rf_prec prec,
+                         const rf_pack_plan_t* plan, int32_t max_sms, float* send, uint32_t* chunk_sync,
+                         uint32_t epoch, void* ws, size_t ws_bytes, void* stream);
+/* Enqueue on `stream` a wait until chunk_sync[chunk] ≥ 16 · epoch · (pair tiles of chunk) (driver
+ * stream-memory wait; wrap-safe comparison).  Returns immediately on the host. */
+rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk_sync, int32_t chunk,
+                               uint32_t epoch, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * TEST HOOK (not a step of the method): C = A·Bᵀ on the same tcgen05 mainloop the G/Φ kernels use,
  * raw fp32 accumulator, rectangular pair tiles (256 × 256).  A: M × K (lda), B: N × K (ldb), dtype per

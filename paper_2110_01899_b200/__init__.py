@@ -11,11 +11,12 @@ import ctypes
 from typing import Dict, Optional, Tuple
 
 from . import _lib
-from ._lib import ACT, OUT, PREC, RFError, load, rf_moments_t  # noqa: F401
+from ._lib import ACT, OUT, PREC, RF_PACK_TILE, RFError, load, rf_moments_t, rf_pack_plan_t  # noqa: F401
 
 __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf_phi_row_split",
            "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_version", "rf_device_supported",
-           "rf_last_launch_count", "RFError", "PREC", "ACT"]
+           "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
+           "RFError", "PREC", "ACT"]
 
 _TORCH_DT = None
 
@@ -187,3 +188,50 @@ def rf_phi_row_split(n: int, world: int, rank: int) -> Tuple[int, int]:
     b, e = ctypes.c_int64(), ctypes.c_int64()
     _lib.check(load().rf_phi_row_split(n, world, rank, ctypes.byref(b), ctypes.byref(e)))
     return b.value, e.value
+
+
+# ------------------------------------------------------------------------------------------ G5 (packed tiles)
+def rf_pack_plan(n: int, world: int, nchunks: int, prec: str) -> rf_pack_plan_t:
+    """Layout of the packed-triangle send/receive buffers of the multi-GPU G (include/rf.h, G5)."""
+    plan = rf_pack_plan_t()
+    _lib.check(load().rf_pack_plan(n, world, nchunks, PREC[prec], ctypes.byref(plan)))
+    return plan
+
+
+def rf_pack_tile_map(plan: rf_pack_plan_t, rank: int):
+    """(row tile, col tile) of every receive slot of `rank` as an int32 numpy array (slots, 2); −1 = padding."""
+    import numpy as np
+    nslots = plan.recv_elems // (RF_PACK_TILE * RF_PACK_TILE)
+    rc = np.empty((max(nslots, 1), 2), dtype=np.int32)
+    _lib.check(load().rf_pack_tile_map(ctypes.byref(plan), rank,
+                                       rc.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+    return rc[:nslots]
+
+
+def rf_gram_packed(X, W, plan: rf_pack_plan_t, send, sync, epoch: int, act: str = "tanh", prec: str = "bf16",
+                   m_total: Optional[int] = None, max_sms: int = 0, ws=None, stream=None):
+    """K3 + K4 of this rank's features with K4 writing the packed send buffer (include/rf.h, G5)."""
+    torch = _torch()
+    lib = load()
+    dt = _dtype_for(prec)
+    _check_tensor("X", X, dt)
+    _check_tensor("W", W, dt)
+    n, p = X.shape
+    m_local = W.shape[0]
+    m_total = m_local if m_total is None else int(m_total)
+    if send.dtype != torch.float32 or not send.is_contiguous() or send.numel() < plan.send_elems:
+        raise RFError(_lib.RF_E_INVALID, f"send must be a contiguous float32 tensor of >= {plan.send_elems} elements")
+    if sync.dtype != torch.int32 or not sync.is_contiguous() or sync.numel() < plan.nchunks:
+        raise RFError(_lib.RF_E_INVALID, "sync must be a contiguous int32 tensor of >= nchunks elements")
+    if ws is None:
+        ws = torch.empty(rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=X.device)
+    _lib.check(lib.rf_gram_packed(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(W.data_ptr()),
+                                  W.stride(0), p, n, m_local, m_total, ACT[act], PREC[prec], ctypes.byref(plan),
+                                  int(max_sms), ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(sync.data_ptr()),
+                                  int(epoch), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return send
+
+
+def rf_stream_wait_chunk(plan: rf_pack_plan_t, sync, chunk: int, epoch: int, stream=None) -> None:
+    _lib.check(load().rf_stream_wait_chunk(ctypes.byref(plan), ctypes.c_void_p(sync.data_ptr()), int(chunk),
+                                           int(epoch), _stream_ptr(stream)))

@@ -25,13 +25,27 @@ OUT = {"upper": 0, "full": 1}
 SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "rf_tau_workspace_size",
            "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram", "rf_phi_workspace_size",
            "rf_phi_closed_form", "rf_phi_row_split", "rf_last_launch_count", "rf_profile_enable",
-           "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt")
+           "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt", "rf_pack_plan",
+           "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk")
+
+RF_PACK_TILE = 256
+RF_PACK_MAX_CHUNKS = 64
 
 
 class rf_moments_t(ctypes.Structure):
     _fields_ = [("tau", ctypes.c_double), ("kd", (ctypes.c_double * 3) * 5), ("e_sigma_sq", ctypes.c_double),
                 ("d0", ctypes.c_double), ("d1", ctypes.c_double), ("d2", ctypes.c_double),
                 ("nodes", ctypes.c_int32), ("method", ctypes.c_int32), ("quad_err_est", ctypes.c_double)]
+
+
+class rf_pack_plan_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("world", ctypes.c_int32), ("nchunks", ctypes.c_int32),
+                ("prec", ctypes.c_int32), ("tiles_per_pair", ctypes.c_int32), ("pair_tiles", ctypes.c_int64),
+                ("send_elems", ctypes.c_int64), ("recv_elems", ctypes.c_int64),
+                ("chunk_tile0", ctypes.c_int64 * (RF_PACK_MAX_CHUNKS + 1)),
+                ("chunk_slots", ctypes.c_int64 * RF_PACK_MAX_CHUNKS),
+                ("chunk_send_off", ctypes.c_int64 * (RF_PACK_MAX_CHUNKS + 1)),
+                ("chunk_recv_off", ctypes.c_int64 * (RF_PACK_MAX_CHUNKS + 1))]
 
 
 class RFError(RuntimeError):
@@ -71,7 +85,14 @@ def load() -> ctypes.CDLL:
     lib.rf_debug_gemm_workspace_size.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_debug_gemm_nt.argtypes = [vp, i64, vp, i64, i64, i64, i64, ctypes.c_int, i32, vp, i64, vp, sz, vp]
     lib.rf_profile_read.argtypes = [i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
-    for name in ("rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
+    PP = ctypes.POINTER(rf_pack_plan_t)
+    lib.rf_pack_plan.argtypes = [i64, i32, i32, ctypes.c_int, PP]
+    lib.rf_pack_tile_map.argtypes = [PP, i32, ctypes.POINTER(i32)]
+    lib.rf_gram_packed.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, PP, i32, vp, vp,
+                                   ctypes.c_uint32, vp, sz, vp]
+    lib.rf_stream_wait_chunk.argtypes = [PP, vp, i32, ctypes.c_uint32, vp]
+    for name in ("rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
+                 "rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",
                  "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt"):
         getattr(lib, name).restype = ctypes.c_int

@@ -224,7 +224,7 @@ __device__ __forceinline__ void store_mirror(float* M, int64_t ld, int64_t n, in
 }
 
 // ------------------------------------------------------------------------------------------
-// Epilogue functors: operator()(ctx, row_lo, col0, r[32], chunk, nchunks) for the warp's rows
+// Epilogue functors: operator()(ctx, row_lo, col0, r[32], chunk, nchunks, t) for the warp's rows
 // [row_lo, row_lo+32) (row = row_lo + lane) and accumulator columns [col0, col0+32).
 // ------------------------------------------------------------------------------------------
 
@@ -237,9 +237,10 @@ struct EpiSigma {
   int64_t ld;       // elements
   int64_t M, N;     // n rows (samples), m_local columns (features)
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
-                                             int) const {
+                                             int, long long) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float s[32];
@@ -308,9 +309,10 @@ struct EpiSyrk {
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int nchunks) const {
+                                             int chunk, int nchunks, long long) const {
     const int64_t row = row_lo + cx.lane;
     float v[32];
 #pragma unroll
@@ -331,6 +333,66 @@ struct EpiSyrk {
   }
 };
 
+// K4 with PACKED output for the multi-GPU reduce-scatter (include/rf.h, G5).  The pair tile t (schedule
+// index; row tile ti) belongs to the chunk whose row-tile range holds ti; its 256×256 sub-tile sub goes to
+// position u = tiles_per_pair·(t − tile0[c]) + sub of the chunk: owner u mod R, slot u div R.  Whole tiles are
+// stored (no triangle mask).  K-chunked accumulation (3×TF32) re-reads the partial from the slot.
+struct PackDev {
+  int64_t tile0[RF_PACK_MAX_CHUNKS + 1];
+  int64_t slots[RF_PACK_MAX_CHUNKS];
+  int64_t soff[RF_PACK_MAX_CHUNKS + 1];
+  int32_t rt0[RF_PACK_MAX_CHUNKS + 1];      // first 256-row tile of chunk c
+};
+struct EpiSyrkPacked {
+  float* send;
+  uint32_t* sync;
+  float scale;
+  int world, nchunks, bn;
+  PackDev pk;
+  __device__ __forceinline__ bool chunk_needed(int64_t, int64_t) const { return true; }
+  __device__ __forceinline__ int chunk_of(int ti) const {
+    int c = 0;
+    while (c + 1 < nchunks && ti >= pk.rt0[c + 1]) ++c;
+    return c;
+  }
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
+                                             int chunk, int, long long t) const {
+    const int ti = (int)(row_lo >> 8);
+    const int c = chunk_of(ti);
+    const int64_t tj0 = (col0 / bn) * bn;                          // first column of the pair tile
+    const int sub = (int)((col0 - tj0) >> 8);
+    const int64_t u = (int64_t)(bn >> 8) * (t - pk.tile0[c]) + sub;
+    const int64_t owner = u % world, slot = u / world;
+    float* tile = send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
+    const int64_t lrow = (row_lo & 255) + cx.lane;
+    float* dst = tile + lrow * RF_PACK_TILE + ((col0 - tj0) & 255);
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
+    if (chunk > 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 o = reinterpret_cast<const float4*>(dst)[q];
+        v[4 * q] += o.x; v[4 * q + 1] += o.y; v[4 * q + 2] += o.z; v[4 * q + 3] += o.w;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+  // After the warp's last store of pair tile t: publish it (system-scope release) to the chunk counter.
+  __device__ __forceinline__ void tile_done(long long t, uint32_t lane) const {
+    __syncwarp();
+    if (lane == 0) {
+      int c = 0;
+      while (c + 1 < nchunks && t >= pk.tile0[c + 1]) ++c;
+      __threadfence_system();
+      atomicAdd(sync + c, 1u);
+    }
+  }
+};
+
 // K5: Φ[i][j] = EQ1 with x_i as pivot (DESIGN.md §4 R6), j ≥ i.
 struct EpiEq1 {
   float* Phi;
@@ -343,9 +405,10 @@ struct EpiEq1 {
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
-                                             int) const {
+                                             int, long long) const {
     const int64_t row = row_lo + cx.lane;
     const RowCoef c = rc[row < n ? row : n - 1];
     float nj[32];
@@ -387,9 +450,10 @@ struct EpiRaw {
   float* C;
   int64_t ld, M, N;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int) const {
+                                             int chunk, int, long long) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float v[32];
@@ -594,12 +658,13 @@ __global__ void __launch_bounds__(384, 1)
           uint32_t r[32];
           ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF + cc * 32, r);
           ptx::tmem_ld_wait();
-          epi(cx, row_lo, col0, r, c, nchunks);
+          epi(cx, row_lo, col0, r, c, nchunks, (long long)t);
         }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
       }
+      epi.tile_done((long long)t, lane);
     }
     if (lane == 0) ptx::bulk_wait_all();
   }

@@ -137,3 +137,52 @@ def test_no_cpu_fallback_without_gpu():
     s = lib.rf_phi_closed_form(ctypes.c_void_p(xa), 64, 64, 256, 0, 1.0, None, 4, 0, 0, 256,
                                ctypes.c_void_p(oa), 256, ctypes.c_void_p(wsa), size, None)
     assert s in (_lib.RF_E_CUDA, _lib.RF_E_UNSUPPORTED)
+
+
+# ------------------------------------------------------------------------------------------ G5 plan (host)
+@pytest.mark.parametrize("n", [1, 255, 256, 600, 4096, 65536])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("prec", ["bf16", "3xtf32"])
+def test_pack_plan_layout_and_coverage(n, world, prec):
+    """Chunk offsets are consistent, every pair tile of K4's triangle schedule is owned by exactly one slot
+    of exactly one rank, and the owned tiles cover the upper triangle (256-tile granularity)."""
+    plan = rf.rf_pack_plan(n, world, 16, prec)
+    T2 = 256 * 256
+    assert 1 <= plan.nchunks <= 16
+    assert plan.chunk_tile0[0] == 0 and plan.chunk_tile0[plan.nchunks] == plan.pair_tiles
+    for c in range(plan.nchunks):
+        tiles = (plan.chunk_tile0[c + 1] - plan.chunk_tile0[c]) * plan.tiles_per_pair
+        assert tiles > 0
+        assert plan.chunk_slots[c] == -(-tiles // world)
+        assert plan.chunk_send_off[c + 1] - plan.chunk_send_off[c] == world * plan.chunk_slots[c] * T2
+        assert plan.chunk_recv_off[c + 1] - plan.chunk_recv_off[c] == plan.chunk_slots[c] * T2
+    assert plan.send_elems == plan.chunk_send_off[plan.nchunks] == world * plan.recv_elems
+    nt = -(-n // 256)
+    seen = {}
+    for r in range(world):
+        for I, J in rf.rf_pack_tile_map(plan, r):
+            if I < 0:
+                continue
+            assert (I, J) not in seen
+            seen[(I, J)] = r
+    assert len(seen) == plan.pair_tiles * plan.tiles_per_pair
+    for I in range(nt):
+        for J in range(I, nt):
+            assert (I, J) in seen, (I, J)
+    counts = np.bincount(np.array(list(seen.values())), minlength=world)
+    assert counts.max() - counts.min() <= plan.nchunks
+
+
+def test_pack_plan_rejects_bad_arguments():
+    with pytest.raises(rf.RFError):
+        rf.rf_pack_plan(0, 2, 4, "bf16")
+    with pytest.raises(rf.RFError):
+        rf.rf_pack_plan(1024, 0, 4, "bf16")
+    with pytest.raises(rf.RFError):
+        rf.rf_pack_plan(1024, 2, 4, "fp32")      # SIMT modes have no packed output
+    plan = rf.rf_pack_plan(1024, 2, 4, "bf16")
+    with pytest.raises(rf.RFError):
+        rf.rf_pack_tile_map(plan, 2)
+    plan.chunk_slots[0] += 1                     # a plan not made by rf_pack_plan is refused
+    with pytest.raises(rf.RFError):
+        rf.rf_pack_tile_map(plan, 0)
