@@ -364,7 +364,7 @@ constexpr int kPackGm = 8;  // raster group of rf_gram_packed's K4 (chunks are r
 // overlapped via two TMEM slots); K4 uses kBN4 (512: one slot, a third less L2 traffic per flop than 256).
 template <int kFmt, int kSplit, int kBN4, int kOut>
 rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
-  using C3 = rfk::TcCfg<kFmt, kSplit, 256>;
+  using C3 = rfk::TcCfg<kFmt, kSplit, 256, 0>;     // K3 stores Σᵀ from registers: no staging buffers
   using C4 = rfk::TcCfg<kFmt, kSplit, kBN4>;
   const bool bf = kFmt == 1;
   rf_status s;
@@ -437,6 +437,72 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   }
   rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
   if ((s = launch_tc<C4>("K4_syrk", tA, tB, tAl, tBl, tO, s4l, e4, g.sms, g.st))) return s;
+  return ok();
+}
+
+struct K5Args {
+  const void* X; int64_t ldx, p, n; rf_prec prec;
+  float* Phi; int64_t ldphi; int full;
+  const rfk::RowCoef* rc; const float* nj;
+  float e0, e1, e2, f0, f1;
+  int64_t row_begin, row_end;
+  char* w; PhiPlan pl; int sms; cudaStream_t st;
+};
+
+#ifndef K5_STG
+#define K5_STG 2
+#endif
+// Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
+template <bool kOdd>
+rf_status launch_k5(const K5Args& a) {
+  const void* X = a.X;
+  const int64_t ldx = a.ldx, p = a.p, n = a.n, ldphi = a.ldphi, row_begin = a.row_begin, row_end = a.row_end;
+  const rf_prec prec = a.prec;
+  float* Phi = a.Phi;
+  const int full = a.full;
+  const rfk::RowCoef* rc = a.rc;
+  const float* nj = a.nj;
+  const float e0 = a.e0, e1 = a.e1, e2 = a.e2, f0 = a.f0, f1 = a.f1;
+  char* w = a.w;
+  const PhiPlan& pl = a.pl;
+  cudaStream_t st = a.st;
+  struct { int sms; } dev{a.sms};
+  rf_status s;
+  CUtensorMap tA, tAl, tO;
+  const bool tma_out = make_tmap_out(&tO, Phi, n, n, ldphi);
+  rfk::EpiEq1<kOdd> e{Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full, tma_out ? 1 : 0};
+  const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
+  if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
+    const bool bf = prec == RF_PREC_BF16;
+    if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
+    if (!tma_out) tO = tA;
+    if (bf) {
+      using C = rfk::TcCfg<1, 1, 256, K5_STG>;
+      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
+      sc.load_pol = env_int("RF_K5_LOADPOL", 1);
+      sc.store_pol = env_int("RF_K5_STOREPOL", 1);
+      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    } else {
+      using C = rfk::TcCfg<2, 1, 256, K5_STG>;
+      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
+      sc.load_pol = env_int("RF_K5_LOADPOL", 1);
+      sc.store_pol = env_int("RF_K5_STOREPOL", 1);
+      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    }
+  } else {
+    using C = rfk::TcCfg<2, 3, 256>;
+    float* Xh = (float*)(w + pl.off_xhi);
+    float* Xl = (float*)(w + pl.off_xlo);
+    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, 128))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
+    if (!tma_out) tO = tA;
+    rfk::Sched sc =
+        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));   // EQ1 is nonlinear in g
+    sc.load_pol = env_int("RF_K5_LOADPOL", 1);
+    sc.store_pol = env_int("RF_K5_STOREPOL", 1);
+    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
+  }
   return ok();
 }
 
@@ -1024,38 +1090,13 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
                ? s
                : ok();
   }
-  // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
-  CUtensorMap tA, tAl, tO;
-  const bool tma_out = make_tmap_out(&tO, Phi, n, n, ldphi);
-  rfk::EpiEq1 e{(float*)Phi, ldphi, n, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0, (float)f1, full,
-                tma_out ? 1 : 0};
-  const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
-  if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
-    const bool bf = prec == RF_PREC_BF16;
-    if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
-    if (!tma_out) tO = tA;
-    if (bf) {
-      using C = rfk::TcCfg<1, 1, 256>;
-      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
-      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
-    } else {
-      using C = rfk::TcCfg<2, 1, 256>;
-      const rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
-      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
-    }
-  } else {
-    using C = rfk::TcCfg<2, 3, 256>;
-    float* Xh = (float*)(w + pl.off_xhi);
-    float* Xl = (float*)(w + pl.off_xlo);
-    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
-    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, 128))) return s;
-    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
-    if (!tma_out) tO = tA;
-    const rfk::Sched sc =
-        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));   // EQ1 is nonlinear in g
-    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
-  }
-  return ok();
+  // σ odd (tanh, erf, sigmoid − ½: all north-star activations) ⇒ ⟨k,d⟩ = 0 for k + d even ⇒ A0 = A2 = 0;
+  // the general form stays available (RF_EQ1_GENERAL=1, tested) for non-odd σ.
+  const bool odd_act = act == RF_ACT_TANH || act == RF_ACT_ERF || act == RF_ACT_SIGMOID_HALF;
+  K5Args ka{X, ldx, p, n, prec, (float*)Phi, ldphi, full, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
+            (float)f1, row_begin, row_end, w, pl, dev.sms, st};
+  if (odd_act && env_int("RF_EQ1_GENERAL", 0) == 0) return launch_k5<true>(ka);
+  return launch_k5<false>(ka);
 }
 
 }  // extern "C"

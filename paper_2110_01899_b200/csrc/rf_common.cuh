@@ -87,6 +87,54 @@ __device__ __forceinline__ float sqrt_fast(float x) {
 }
 __device__ __forceinline__ double sqrt_fast(double x) { return sqrt(x); }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FMUL2: two fp32 lanes per instruction, each rounded as the scalar op).
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Two off-diagonal EQ1 entries at once (same row i, columns j, j+1): the arithmetic of eq1_entry below,
+// op for op, on fp32 pairs.  kOdd: σ odd ⇒ ⟨k,d⟩ = 0 for k + d even ⇒ A0 = A2 = 0 and Φ = ν·A1·C1(s).
+template <bool kOdd>
+__device__ __forceinline__ void eq1_pair(float g0, float g1, float nj0, float nj1, uint64_t c2, uint64_t a0_2,
+                                         uint64_t a1_2, uint64_t a2h_2, uint64_t e0_2, uint64_t e1_2, uint64_t e2_2,
+                                         uint64_t f0_2, uint64_t f1_2, float& out0, float& out1) {
+  const uint64_t nu = mul2(pk2(g0, g1), c2);
+  const uint64_t r = sub2(pk2(nj0, nj1), mul2(nu, nu));
+  float r0, r1;
+  up2(r, r0, r1);
+  const uint64_t s = pk2(sqrt_fast(fmaxf(r0, 0.f)), sqrt_fast(fmaxf(r1, 0.f)));
+  const uint64_t C1 = fma2(s, f1_2, f0_2);
+  uint64_t o;
+  if (kOdd) {
+    o = mul2(nu, mul2(a1_2, C1));
+  } else {
+    const uint64_t C0 = fma2(s, fma2(s, e2_2, e1_2), e0_2);
+    const uint64_t inner = fma2(nu, a2h_2, mul2(a1_2, C1));
+    o = fma2(nu, inner, mul2(a0_2, C0));
+  }
+  up2(o, out0, out1);
+}
+
 template <typename T>
 __device__ __forceinline__ T eq1_entry(T g, T a0, T a1, T a2h, T c, T njt, bool diag, T nu_diag, T e0, T e1, T e2,
                                        T f0, T f1) {

@@ -34,7 +34,9 @@
 
 namespace rfk {
 
-template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32*/, int kSplit /*1 or 3*/, int kBN /*256 or 512*/>
+// kStg: 4-KB TMA-store staging buffers per epilogue warp (-1 = default: 1 if stages are large, else 2;
+// 0 for epilogues that store directly from registers, e.g. K3).
+template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32*/, int kSplit /*1 or 3*/, int kBN /*256 or 512*/, int kStg = -1>
 struct TcCfg {
   static constexpr int BM = 256, BN = kBN;      // pair tile
   static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
@@ -48,7 +50,7 @@ struct TcCfg {
   static constexpr int ACC_COLS = kBN;
   static constexpr int ACC_SLOTS = 512 / kBN;
   static constexpr int EPI_WARPS = 8;
-  static constexpr int STG_BUFS = (kSplit == 3 || kBN == 512) ? 1 : 2;   // TMA-store staging per epi warp
+  static constexpr int STG_BUFS = kStg >= 0 ? kStg : ((kSplit == 3 || kBN == 512) ? 1 : 2);   // per epi warp
   static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
   static constexpr int STAGES = (225 * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + STG_BYTES + 256;
@@ -85,6 +87,9 @@ struct Sched {
   // required for progress.
   uint32_t* prog;
   int lock_w, lock_ks;
+  // L2 policies: operand loads (0 = evict_normal, 1 = evict_last: operands re-read by many tiles, e.g. X in
+  // K5) and epilogue TMA stores (0 = normal, 1 = evict_first: a streamed output must not evict them).
+  int load_pol, store_pol;
 
   struct Group {
     int I0, I1, J0, Jf;
@@ -142,6 +147,8 @@ struct Sched {
     s.prog = nullptr;
     s.lock_w = 0;
     s.lock_ks = 8;
+    s.load_pol = 0;
+    s.store_pol = 0;
     long long tot = 0;
     for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
     s.num_tiles = (int)tot;
@@ -178,10 +185,13 @@ struct EpiCtx {
   uint8_t* sbuf;           // this warp's staging buffers (kBufs × 4 KB, 1024-B aligned)
   int cur;
   uint32_t lane;
+  int hint;                // 1: stores carry the L2 evict_first hint `pol`
+  uint64_t pol;
 
   // Whole 32×32 block → smem (128-B swizzle: 16-B chunk c of row r at chunk c ^ (r & 7), conflict-free)
   // → one TMA store (rows/cols beyond the matrix are clipped by the tensor map).
   __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
+    static_assert(kBufs >= 1, "store_block needs staging buffers");
     uint8_t* b = sbuf + cur * 4096;
     if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
     __syncwarp();
@@ -192,7 +202,10 @@ struct EpiCtx {
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      ptx::tma_store_2d(tm, b, (int32_t)col0, (int32_t)row_lo);
+      if (hint)
+        ptx::tma_store_2d_hint(tm, b, (int32_t)col0, (int32_t)row_lo, pol);
+      else
+        ptx::tma_store_2d(tm, b, (int32_t)col0, (int32_t)row_lo);
       ptx::bulk_commit();
     }
     cur = (cur + 1 == kBufs) ? 0 : cur + 1;
@@ -238,9 +251,11 @@ struct EpiSigma {
   int64_t M, N;     // n rows (samples), m_local columns (features)
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
   __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
-                                             int, long long) const {
+                                             int, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float s[32];
@@ -310,9 +325,11 @@ struct EpiSyrk {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
   __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int nchunks, long long) const {
+                                             int chunk, int nchunks, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     float v[32];
 #pragma unroll
@@ -350,6 +367,8 @@ struct EpiSyrkPacked {
   int world, nchunks, bn;
   PackDev pk;
   __device__ __forceinline__ bool chunk_needed(int64_t, int64_t) const { return true; }
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   __device__ __forceinline__ int chunk_of(int ti) const {
     int c = 0;
     while (c + 1 < nchunks && ti >= pk.rt0[c + 1]) ++c;
@@ -357,7 +376,7 @@ struct EpiSyrkPacked {
   }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int, long long t) const {
+                                             int chunk, int, long long t, const Pre&) const {
     const int ti = (int)(row_lo >> 8);
     const int c = chunk_of(ti);
     const int64_t tj0 = (col0 / bn) * bn;                          // first column of the pair tile
@@ -393,7 +412,9 @@ struct EpiSyrkPacked {
   }
 };
 
-// K5: Φ[i][j] = EQ1 with x_i as pivot (DESIGN.md §4 R6), j ≥ i.
+// K5: Φ[i][j] = EQ1 with x_i as pivot (DESIGN.md §4 R6), j ≥ i.  Off-diagonal chunks evaluate EQ1 on fp32
+// pairs (eq1_pair); kOdd selects the odd-σ form Φ = ν·A1(α)·C1(s) (A0 = A2 = 0 for odd σ).
+template <bool kOdd>
 struct EpiEq1 {
   float* Phi;
   int64_t ld, n;
@@ -406,11 +427,19 @@ struct EpiEq1 {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
   __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  // The row's coefficient record does not depend on the accumulator: loaded before the TMEM wait.
+  struct Pre {
+    RowCoef c;
+  };
+  __device__ __forceinline__ Pre prefetch(int64_t row_lo, int64_t, uint32_t lane) const {
+    const int64_t row = row_lo + lane;
+    return Pre{rc[row < n ? row : n - 1]};
+  }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
-                                             int, long long) const {
+                                             int, long long, const Pre& pf) const {
     const int64_t row = row_lo + cx.lane;
-    const RowCoef c = rc[row < n ? row : n - 1];
+    const RowCoef& c = pf.c;
     float nj[32];
     if (col0 + 32 <= n) {
 #pragma unroll
@@ -429,10 +458,12 @@ struct EpiEq1 {
         v[e] = eq1_entry<float>(__uint_as_float(r[e]), c.a0, c.a1, c.a2h, c.c, nj[e], col0 + e == row, c.nu_diag, e0,
                                 e1, e2, f0, f1);
     } else {
+      const uint64_t c2 = pk2(c.c, c.c), a0_2 = pk2(c.a0, c.a0), a1_2 = pk2(c.a1, c.a1), a2h_2 = pk2(c.a2h, c.a2h);
+      const uint64_t e0_2 = pk2(e0, e0), e1_2 = pk2(e1, e1), e2_2 = pk2(e2, e2), f0_2 = pk2(f0, f0), f1_2 = pk2(f1, f1);
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        v[e] = eq1_entry<float>(__uint_as_float(r[e]), c.a0, c.a1, c.a2h, c.c, nj[e], false, c.nu_diag, e0, e1, e2,
-                                f0, f1);
+      for (int e = 0; e < 32; e += 2)
+        eq1_pair<kOdd>(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, a0_2, a1_2, a2h_2, e0_2,
+                       e1_2, e2_2, f0_2, f1_2, v[e], v[e + 1]);
     }
     if (use_tma && col0 >= row_lo + 31) {
       cx.store_block(row_lo, col0, v);
@@ -451,9 +482,11 @@ struct EpiRaw {
   int64_t ld, M, N;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
   __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int, long long) const {
+                                             int chunk, int, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float v[32];
@@ -524,7 +557,7 @@ __global__ void __launch_bounds__(384, 1)
     // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
     // The whole warp walks the loop (lane 0 issues); the leader's warp also runs the lockstep check.
     const bool lock = sched.prog != nullptr && rank == 0;
-    const uint64_t pol = ptx::policy_evict_normal();
+    const uint64_t pol = sched.load_pol ? ptx::policy_evict_last() : ptx::policy_evict_normal();
     const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -637,6 +670,8 @@ __global__ void __launch_bounds__(384, 1)
     cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
     cx.cur = 0;
     cx.lane = lane;
+    cx.hint = sched.store_pol;
+    cx.pol = ptx::policy_evict_first();
     const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     constexpr int HALF = Cfg::ACC_COLS / 2;
     int it = 0;
@@ -646,19 +681,31 @@ __global__ void __launch_bounds__(384, 1)
       int ti, tj;
       cur.get(t, ti, tj);
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
+      const int64_t colb = (int64_t)tj * Cfg::BN + h * HALF;
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
+        const uint32_t tbase = tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF;
+        const typename Epi::Pre pf = epi.prefetch(row_lo, colb, lane);   // per-row inputs: before the wait
         ptx::mbar_wait(&tfull[slot], acc_phase);
         ptx::tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < HALF / 32; ++cc) {
-          const int64_t col0 = (int64_t)tj * Cfg::BN + h * HALF + cc * 32;
-          if (!epi.chunk_needed(row_lo, col0)) continue;
-          uint32_t r[32];
-          ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF + cc * 32, r);
+        // Software pipeline over the warp's 32-column chunks: the TMEM load of chunk cc+1 is in flight while
+        // chunk cc is transformed and stored (tcgen05.wait::ld waits for all of a thread's loads, so the
+        // next load is issued only after the current one has been waited for).
+        constexpr int NCH = HALF / 32;
+        static_assert(NCH % 2 == 0, "even number of 32-column chunks");
+        uint32_t ra[32], rb[32];
+        auto step = [&](int cc, uint32_t(&cur)[32], uint32_t(&nxt)[32]) __attribute__((always_inline)) {
+          const int64_t col0 = colb + cc * 32;
           ptx::tmem_ld_wait();
-          epi(cx, row_lo, col0, r, c, nchunks, (long long)t);
+          if (cc + 1 < NCH) ptx::tmem_ld_32x32b_x32(tbase + (cc + 1) * 32, nxt);
+          if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, cur, c, nchunks, (long long)t, pf);
+        };
+        ptx::tmem_ld_32x32b_x32(tbase, ra);
+#pragma unroll 1
+        for (int cc = 0; cc < NCH; cc += 2) {
+          step(cc, ra, rb);
+          step(cc + 1, rb, ra);
         }
         ptx::tc_fence_before();
         __syncwarp();

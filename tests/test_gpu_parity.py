@@ -162,6 +162,18 @@ def test_phi_multi_tile_given_tau_full(prec):
     _phi_case(X, "erf", prec, tau=1.05, out="full")
 
 
+@pytest.mark.parametrize("prec", ["3xtf32", "bf16"])
+def test_phi_general_epilogue_matches_odd_form(prec, monkeypatch):
+    """The general EQ1 epilogue (A0, A2 terms kept, used for non-odd σ) on an odd σ: same parity, and within
+    a few fp32 ulps of the odd-σ form the library selects by default."""
+    X = synthetic.make_X(4, n=700, p=96)
+    P_odd, _ = _phi_case(X, "tanh", prec)
+    monkeypatch.setenv("RF_EQ1_GENERAL", "1")
+    P_gen, _ = _phi_case(X, "tanh", prec)
+    I, J = upper_idx(X.shape[0])
+    assert np.max(np.abs(P_gen[I, J] - P_odd[I, J])) <= 1e-6 * np.max(np.abs(P_odd[I, J]))
+
+
 def test_phi_row_blocks_assemble_to_full():
     X = synthetic.make_X(4, n=1000, p=64)
     ranges = [rf.rf_phi_row_split(1000, 3, r) for r in range(3)]
