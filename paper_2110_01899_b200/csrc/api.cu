@@ -200,9 +200,13 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Row tiles per L2 raster group (tc_gemm.cuh Sched).  Env RF_GM overrides (experiments).
-int raster_gm(int def) {
-  const char* e = std::getenv("RF_GM");
+// Row tiles per L2 raster group (tc_gemm.cuh Sched).  Env RF_GM<k> (kernel k = 3, 4, 5) or RF_GM overrides
+// (experiments).
+int raster_gm(int def, int kernel = 0) {
+  char name[16];
+  std::snprintf(name, sizeof(name), "RF_GM%d", kernel);
+  const char* e = kernel ? std::getenv(name) : nullptr;
+  if (!(e && *e && std::atoi(e) > 0)) e = std::getenv("RF_GM");
   if (e && *e && std::atoi(e) > 0) return std::atoi(e);
   return def;
 }
@@ -390,7 +394,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   if (kSplit != 3) { tAl = tA; tBl = tB; }
   const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
   const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
-                                         raster_gm(8));
+                                         raster_gm(8, 3));
   if (g.act == RF_ACT_TANH) {
     rfk::EpiSigma<kOut, RF_ACT_TANH> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
     if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
@@ -415,7 +419,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   const int kb4 = (int)((g.m_local + C4::BK - 1) / C4::BK);
   const rfk::Sched s4 =
       rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4,
-                       raster_gm(8));
+                       raster_gm(8, 4));
   rfk::Sched s4l = s4;
   const int lockw = env_int("RF_LOCKW", 24);
   if (lockw > 0) {
@@ -478,13 +482,13 @@ rf_status launch_k5(const K5Args& a) {
     if (!tma_out) tO = tA;
     if (bf) {
       using C = rfk::TcCfg<1, 1, 256, K5_STG>;
-      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
+      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       sc.load_pol = env_int("RF_K5_LOADPOL", 1);
       sc.store_pol = env_int("RF_K5_STOREPOL", 1);
       if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     } else {
       using C = rfk::TcCfg<2, 1, 256, K5_STG>;
-      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));
+      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       sc.load_pol = env_int("RF_K5_LOADPOL", 1);
       sc.store_pol = env_int("RF_K5_STOREPOL", 1);
       if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
@@ -498,7 +502,7 @@ rf_status launch_k5(const K5Args& a) {
     if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
     if (!tma_out) tO = tA;
     rfk::Sched sc =
-        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16));   // EQ1 is nonlinear in g
+        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));   // EQ1 is nonlinear in g
     sc.load_pol = env_int("RF_K5_LOADPOL", 1);
     sc.store_pol = env_int("RF_K5_STOREPOL", 1);
     if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
