@@ -172,3 +172,31 @@ def sample_indices(n: int, count: int = 1024, seed: int = 7, tile_stride: int = 
             if 0 <= t + d < n:
                 s.add(t + d)
     return np.array(sorted(s), dtype=np.int64)
+
+
+def make_T(cfg: Config | int, eps: float, rows: Optional[np.ndarray] = None, *, m: Optional[int] = None,
+           p: Optional[int] = None) -> np.ndarray:
+    """Sign/sparsity pattern T ∈ {−1, 0, +1}^{len(rows)×p} of the ternary projection (Eq. (4)):
+    entry 0 with probability ε, −1 or +1 each with probability (1−ε)/2.  W^ter = (1−ε)^{-1/2}·T; the scale
+    belongs to the method and is applied by each implementation, not here.  Returned as float64 (exact).
+    Seed t = 4 of the config; blockwise substreams as make_W."""
+    if isinstance(cfg, int):
+        cfg = CONFIGS[cfg]
+    if not (0.0 <= eps < 1.0):
+        raise ValueError("eps must be in [0, 1)")
+    m = cfg.m if m is None else m
+    p = cfg.p if p is None else p
+    if rows is None:
+        rows = np.arange(m, dtype=np.int64)
+    rows = np.asarray(rows, dtype=np.int64)
+    out = np.empty((len(rows), p), dtype=np.float64)
+    blocks = rows // BLOCK
+    seed = seed_of(cfg.idx, 4)
+    for b in np.unique(blocks):
+        b = int(b)
+        nb = min(BLOCK, m - b * BLOCK)
+        u = _block_rng(seed, b).random((nb, p))
+        full = np.where(u < eps, 0.0, np.where(u < eps + (1.0 - eps) / 2.0, -1.0, 1.0))
+        sel = blocks == b
+        out[sel] = full[rows[sel] - b * BLOCK]
+    return out
