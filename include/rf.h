@@ -217,6 +217,42 @@ rf_status rf_gram_packed(const void* X, int64_t ldx, const void* W_local, int64_
 rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk_sync, int32_t chunk,
                                uint32_t epoch, void* stream);
 
+/* =============================================================================================
+ * NEXT-1 — Ternary Random Features (TRF): Eq. (3)-(5), Corollary 1 + Eq. (8),
+ * Algorithm 1.  W^ter = c·T with T ∈ {−1, 0, +1} (P(0) = ε, P(±1) = (1−ε)/2) and c = (1−ε)^{-1/2};
+ * σ^ter(t) = −1 if t < s−, +1 if t > s+, 0 otherwise; Σ^ter = σ^ter(W^ter X); G^ter = (1/m) Σ^terᵀ Σ^ter.
+ * ============================================================================================= */
+
+/* rf_trf_thresholds — host.  Algorithm 1 step 2: (s−, s+) whose ternary moments match Theorem 1's d1, d2
+ * (P:539-541), from Eq. (5) with weak derivatives (Remark 2) — NOT Eq. (8) as printed, which contradicts Table 2's
+ * sign(t) row (reading R15): E[σ^ter'] = (φ(a)+φ(b))/√τ, E[σ^ter''] = (aφ(a)+bφ(b))/τ, a = s−/√τ,
+ * b = s+/√τ.  sign2 (±1) picks the sign of E[σ^ter''] (the mirror solution (−s+, −s−) has the same d1, d2).
+ * Errors: tau <= 0, negative / non-finite d → RF_E_INVALID; unreachable targets (√(τd1) > 2φ(0), i.e. more than
+ * sign(t), or 2τ√d2 > 2φ(1)) → RF_E_INVALID with the residual in rf_last_error(). */
+rf_status rf_trf_thresholds(double d1, double d2, double tau, int32_t sign2, double* s_minus, double* s_plus);
+/* The same for the d1, d2 of a north-star σ at τ (rf_moments, sign2 = sign of E[σ'']; odd σ → s− = −s+). */
+rf_status rf_trf_thresholds_for(rf_act act, double tau, double* s_minus, double* s_plus);
+
+/* rf_ter_features — Algorithm 1 step 4, features only (also the test hook for the decisions):
+ *   features[i*ldf + k] = FP8 E4M3 code of σ^ter(c·x_iᵀt_k): 0x38 (+1), 0xB8 (−1), 0x00 (0).
+ *   X device bf16 n × p (ldx); T device bf16 m_local × p (ldt) with entries exactly −1, 0, +1 (not checked).
+ *   The projection z = x_iᵀt_k is accumulated in fp32 on the tensor cores (bf16 × {−1,0,1} products are
+ *   exact) and compared with t± = s±/c rounded to fp32; an entry whose exact z lies within the fp32 rounding
+ *   of z of a threshold may decide either way (the tests bound that band).
+ *   features: device, 16-B aligned, ldf ≥ m_local bytes, ldf % 16 == 0.  Async on `stream`. */
+rf_status rf_ter_features(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
+                          int64_t m_local, double eps, double s_minus, double s_plus, void* features, int64_t ldf,
+                          void* stream);
+/* rf_gram_ter — G^ter = (1/m_total) Σ^terᵀ Σ^ter over this rank's m_local features (UPPER / FULL like rf_gram).
+ * Pipeline: K3^ter (bf16 tcgen05 GEMM X·Tᵀ, σ^ter in the epilogue → fp8 codes, 1 byte per feature instead of the
+ * paper's 32 bits) → K4^ter (fp8 kind::f8f6f4 SYRK, 256×512 CTA-pair tiles, soft lockstep): the ±1
+ * products and their sums are exact in fp32 (m_local ≤ 2^24), so m_total·G^ter is an exact integer count of the
+ * decided features.  ws ≥ rf_gram_ter_workspace_size(p, n, m_local). */
+rf_status rf_gram_ter_workspace_size(int64_t p, int64_t n, int64_t m_local, size_t* bytes);
+rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n, int64_t m_local,
+                      int64_t m_total, double eps, double s_minus, double s_plus, rf_out out, float* G, int64_t ldg,
+                      void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * TEST HOOK (not a step of the method): C = A·Bᵀ on the same tcgen05 mainloop the G/Φ kernels use,
  * raw fp32 accumulator, rectangular pair tiles (256 × 256).  A: M × K (lda), B: N × K (ldb), dtype per

@@ -16,7 +16,8 @@ from ._lib import ACT, OUT, PREC, RF_PACK_TILE, RFError, load, rf_moments_t, rf_
 __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf_phi_row_split",
            "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_version", "rf_device_supported",
            "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
-           "RFError", "PREC", "ACT"]
+           "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter",
+           "rf_gram_ter_workspace_size", "RFError", "PREC", "ACT"]
 
 _TORCH_DT = None
 
@@ -235,3 +236,61 @@ def rf_gram_packed(X, W, plan: rf_pack_plan_t, send, sync, epoch: int, act: str 
 def rf_stream_wait_chunk(plan: rf_pack_plan_t, sync, chunk: int, epoch: int, stream=None) -> None:
     _lib.check(load().rf_stream_wait_chunk(ctypes.byref(plan), ctypes.c_void_p(sync.data_ptr()), int(chunk),
                                            int(epoch), _stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------------------------------ NEXT-1 (TRF)
+def rf_trf_thresholds(d1: float, d2: float, tau: float, sign2: int = 1) -> Tuple[float, float]:
+    """(s−, s+) of σ^ter matching Theorem 1's d1, d2 at τ (Algorithm 1 step 2; include/rf.h)."""
+    sm, sp = ctypes.c_double(), ctypes.c_double()
+    _lib.check(load().rf_trf_thresholds(float(d1), float(d2), float(tau), int(sign2), ctypes.byref(sm),
+                                        ctypes.byref(sp)))
+    return sm.value, sp.value
+
+
+def rf_trf_thresholds_for(act: str, tau: float) -> Tuple[float, float]:
+    sm, sp = ctypes.c_double(), ctypes.c_double()
+    _lib.check(load().rf_trf_thresholds_for(ACT[act], float(tau), ctypes.byref(sm), ctypes.byref(sp)))
+    return sm.value, sp.value
+
+
+def rf_gram_ter_workspace_size(p: int, n: int, m_local: int) -> int:
+    need = ctypes.c_size_t()
+    _lib.check(load().rf_gram_ter_workspace_size(p, n, m_local, ctypes.byref(need)))
+    return need.value
+
+
+def rf_ter_features(X, T, eps: float, s_minus: float, s_plus: float, out=None, stream=None):
+    """Σ^terᵀ as fp8 E4M3 codes (uint8 n × m_local; 0x38 = +1, 0xB8 = −1, 0 = 0).  X, T: bf16 CUDA tensors."""
+    torch = _torch()
+    _check_tensor("X", X, torch.bfloat16)
+    _check_tensor("T", T, torch.bfloat16)
+    n, p = X.shape
+    m_local = T.shape[0]
+    if out is None:
+        ld = (m_local + 15) // 16 * 16
+        out = torch.empty((n, ld), dtype=torch.uint8, device=X.device)[:, :m_local]
+    _lib.check(load().rf_ter_features(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(T.data_ptr()),
+                                      T.stride(0), p, n, m_local, float(eps), float(s_minus), float(s_plus),
+                                      ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_ptr(stream)))
+    return out
+
+
+def rf_gram_ter(X, T, eps: float, s_minus: float, s_plus: float, out: str = "upper", m_total: Optional[int] = None,
+                G=None, ws=None, stream=None):
+    """G^ter = (1/m_total) Σ^terᵀ Σ^ter (Algorithm 1 step 4) over this rank's rows of T."""
+    torch = _torch()
+    _check_tensor("X", X, torch.bfloat16)
+    _check_tensor("T", T, torch.bfloat16)
+    n, p = X.shape
+    m_local = T.shape[0]
+    m_total = m_local if m_total is None else int(m_total)
+    if G is None:
+        G = torch.zeros((n, n), dtype=torch.float32, device=X.device)
+    _check_tensor("G", G, torch.float32)
+    if ws is None:
+        ws = torch.empty(rf_gram_ter_workspace_size(p, n, m_local), dtype=torch.uint8, device=X.device)
+    _lib.check(load().rf_gram_ter(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(T.data_ptr()),
+                                  T.stride(0), p, n, m_local, m_total, float(eps), float(s_minus), float(s_plus),
+                                  OUT[out], ctypes.c_void_p(G.data_ptr()), G.stride(0), ctypes.c_void_p(ws.data_ptr()),
+                                  ws.numel(), _stream_ptr(stream)))
+    return G

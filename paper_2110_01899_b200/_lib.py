@@ -26,7 +26,8 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram", "rf_phi_workspace_size",
            "rf_phi_closed_form", "rf_phi_row_split", "rf_last_launch_count", "rf_profile_enable",
            "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt", "rf_pack_plan",
-           "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk")
+           "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
+           "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -91,7 +92,13 @@ def load() -> ctypes.CDLL:
     lib.rf_gram_packed.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, PP, i32, vp, vp,
                                    ctypes.c_uint32, vp, sz, vp]
     lib.rf_stream_wait_chunk.argtypes = [PP, vp, i32, ctypes.c_uint32, vp]
-    for name in ("rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
+    lib.rf_trf_thresholds.argtypes = [dbl, dbl, dbl, i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+    lib.rf_trf_thresholds_for.argtypes = [ctypes.c_int, dbl, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+    lib.rf_ter_features.argtypes = [vp, i64, vp, i64, i64, i64, i64, dbl, dbl, dbl, vp, i64, vp]
+    lib.rf_gram_ter_workspace_size.argtypes = [i64, i64, i64, ctypes.POINTER(sz)]
+    lib.rf_gram_ter.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, dbl, dbl, dbl, ctypes.c_int, vp, i64, vp, sz, vp]
+    for name in ("rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
+                 "rf_gram_ter", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
                  "rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",
                  "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt"):

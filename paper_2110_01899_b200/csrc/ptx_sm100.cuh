@@ -229,6 +229,16 @@ __device__ __forceinline__ void mma_tf32_cg2(uint32_t tmem_d, uint64_t adesc, ui
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// FP8 pair MMA (kind::f8f6f4; both operands E4M3 per the instruction descriptor), fp32 accumulate.
+__device__ __forceinline__ void mma_f8_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on the barrier at the same smem offset in every CTA of `mask` once the leader's MMAs complete.
 __device__ __forceinline__ void mma_commit_cg2_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -283,8 +293,8 @@ __device__ __forceinline__ uint64_t sdesc_k128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor (kind::f16 / kind::tf32, fp32 accumulate, both operands K-major).
-// fmt: 1 = BF16, 2 = TF32.  Bits: [4,6) D fmt (1 = F32), [7,10) A fmt, [10,13) B fmt, 15/16 major,
+// Instruction descriptor (kind::f16 / kind::tf32 / kind::f8f6f4, fp32 accumulate, both operands K-major).
+// fmt (a_format = b_format, bits [7,10) / [10,13)): kind::f16 1 = BF16; kind::tf32 2 = TF32; kind::f8f6f4 0 = E4M3.  Bits: [4,6) D fmt (1 = F32), [7,10) A fmt, [10,13) B fmt, 15/16 major,
 // [17,23) N>>3, [24,29) M>>4.
 __host__ __device__ constexpr uint32_t idesc_f32acc(uint32_t fmt, uint32_t M, uint32_t N) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);

@@ -36,13 +36,14 @@ namespace rfk {
 
 // kStg: 4-KB TMA-store staging buffers per epilogue warp (-1 = default: 1 if stages are large, else 2;
 // 0 for epilogues that store directly from registers, e.g. K3).
-template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32*/, int kSplit /*1 or 3*/, int kBN /*256 or 512*/, int kStg = -1>
+template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
+          int kBN /*256 or 512*/, int kStg = -1>
 struct TcCfg {
   static constexpr int BM = 256, BN = kBN;      // pair tile
   static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
-  static constexpr int ESZ = kFmt == 1 ? 2 : 4;
+  static constexpr int ESZ = kFmt == 1 ? 2 : (kFmt == 3 ? 1 : 4);
   static constexpr int BK = 128 / ESZ;          // elements per K-block (one 128-B swizzle row)
-  static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (16 bf16 / 8 tf32) = 32 bytes
+  static constexpr int UK = 32 / ESZ;           // K per tcgen05.mma (16 bf16 / 8 tf32 / 32 fp8) = 32 bytes
   static constexpr int NOPS = kSplit == 3 ? 2 : 1;
   static constexpr int A_BYTES = 128 * 128;     // per CTA: 128 rows × 128 B
   static constexpr int B_BYTES = 128 * 128;     // per CTA per N sub-tile
@@ -54,7 +55,7 @@ struct TcCfg {
   static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
   static constexpr int STAGES = (225 * 1024 - STG_BYTES) / STAGE_BYTES;
   static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + STG_BYTES + 256;
-  static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt, 256, 256);
+  static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt == 3 ? 0u : (uint32_t)kFmt, 256, 256);
   static_assert(STAGES >= 2, "pipeline too shallow");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
 };
@@ -310,6 +311,47 @@ struct EpiSigma {
           }
         }
       }
+    }
+  }
+};
+
+// K3^ter (NEXT-1, Algorithm 1 step 4): Σ^terᵀ[i][k] = σ^ter(c·z), z = x_iᵀt_k, W^ter = c·T, c = (1−ε)^{-1/2}
+// (Eq. (4)); σ^ter(v) = −1 if v < s−, +1 if v > s+, else 0 (Eq. (5)).  The comparison is made on z against
+// t± = s±/c (rounded once on the host), so no product is formed per entry.  Stored as FP8 E4M3 codes
+// (+1 = 0x38, −1 = 0xB8, 0 = 0x00): exact operands for the fp8 SYRK that forms G^ter.
+struct EpiSigmaTer {
+  uint8_t* out;
+  int64_t ld;       // bytes
+  int64_t M, N;     // n rows (samples), m_local columns (features)
+  float t_minus, t_plus;
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  struct Pre {};
+  __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
+                                             int, long long, const Pre&) const {
+    const int64_t row = row_lo + cx.lane;
+    if (row >= M) return;
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float z = __uint_as_float(r[4 * q + b]);
+        const uint32_t code = z > t_plus ? 0x38u : (z < t_minus ? 0xB8u : 0u);
+        word |= code << (8 * b);
+      }
+      w[q] = word;
+    }
+    uint8_t* dst = out + row * ld + col0;
+    if (col0 + 32 <= N) {
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+      for (int e = 0; e < 32; ++e)
+        if (col0 + e < N) dst[e] = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
     }
   }
 };
@@ -646,6 +688,8 @@ __global__ void __launch_bounds__(384, 1)
                     ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, 1u);
                   } else if (Cfg::ESZ == 2) {
                     ptx::mma_bf16_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
+                  } else if (Cfg::ESZ == 1) {
+                    ptx::mma_f8_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
                   } else {
                     ptx::mma_tf32_cg2(ds, ad + off, bd + off, Cfg::IDESC, accum);
                   }

@@ -186,3 +186,38 @@ def test_pack_plan_rejects_bad_arguments():
     plan.chunk_slots[0] += 1                     # a plan not made by rf_pack_plan is refused
     with pytest.raises(rf.RFError):
         rf.rf_pack_tile_map(plan, 0)
+
+
+# ------------------------------------------------------------------------------------------ TRF thresholds (host)
+@pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
+@pytest.mark.parametrize("tau", [0.5, 1.0, 1.0133, 1.0833])
+def test_trf_thresholds_for_match_oracle(act, tau):
+    from oracle import trf
+    sm, sp = rf.rf_trf_thresholds_for(act, tau)
+    mo = oracle.moments(act, tau)
+    osm, osp = trf.solve_thresholds(mo["d1"], mo["d2"], tau)
+    assert abs(sm - osm) < 1e-9 and abs(sp - osp) < 1e-9
+    t = trf.ternary_moments(sm, sp, tau)
+    assert abs(t["d1"] - mo["d1"]) < 1e-13 and abs(t["d2"] - mo["d2"]) < 1e-13
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.0])
+@pytest.mark.parametrize("sign2", [1, -1])
+def test_trf_thresholds_relu_targets(tau, sign2):
+    """Table 2 ReLU row as the target; the mirror solution for the other sign of E[σ'']."""
+    from oracle import trf
+    d1, d2 = 0.25, 1 / (8 * math.pi * tau)
+    sm, sp = rf.rf_trf_thresholds(d1, d2, tau, sign2)
+    osm, osp = trf.solve_thresholds(d1, d2, tau, sign2=sign2)
+    assert abs(sm - osm) < 1e-9 and abs(sp - osp) < 1e-9
+    t = trf.ternary_moments(sm, sp, tau)
+    assert abs(t["d1"] - d1) < 1e-13 and abs(t["d2"] - d2) < 1e-13
+    assert (t["E_s2"] > 0) == (sign2 > 0)
+
+
+def test_trf_thresholds_sign_function_and_errors():
+    sm, sp = rf.rf_trf_thresholds(2 / math.pi, 0.0, 1.0, 1)        # Table 2 sign(t) row: s± = 0
+    assert abs(sm) < 1e-7 and abs(sp) < 1e-7
+    for bad in [(0.7, 0.0, 1.0), (0.25, 1 / (16 * math.pi), 2.0), (0.1, 0.0, 0.0), (-0.1, 0.0, 1.0)]:
+        with pytest.raises(rf.RFError):
+            rf.rf_trf_thresholds(*bad, 1)
