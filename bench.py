@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phi", action="store_true")
+    ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
     ap.add_argument("--comm-sms", type=int, default=8,
                     help="N>1: SMs left free during K4 for the overlapped reduce-scatter kernels")
     return ap.parse_args()
@@ -363,6 +364,53 @@ def main():
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "ms_per_step": ems / args.steps}
 
+    # ---------------- NEXT-1 (Ternary Random Features) on the same shapes: reported beside the headline
+    trf_line = None
+    if do_gram and not args.no_trf:
+        eps = 0.9
+        T_host = torch.from_numpy(synthetic.make_T(cfg, eps, rows=np.arange(m0, m0 + m_local))).to(torch.bfloat16)
+        Td = T_host.to(device)
+        tau_t = rf.rf_estimate_tau(Xd)
+        sm, sp = rf.rf_trf_thresholds_for(cfg.act, tau_t)
+        G_t = G if world == 1 else torch.empty((n, n), dtype=torch.float32, device=device)
+        ws_t = torch.empty(rf.rf_gram_ter_workspace_size(p, n, m_local), dtype=torch.uint8, device=device)
+        for _ in range(args.warmup):
+            rf.rf_gram_ter(Xd, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
+        torch.cuda.synchronize()
+        barrier()
+        rf.rf_profile_read()
+        rf.rf_profile_enable(True)
+        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ta.record(stream)
+        for _ in range(args.steps):
+            rf.rf_gram_ter(Xd, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
+        tb.record(stream)
+        torch.cuda.synchronize()
+        rf.rf_profile_enable(False)
+        trec = rf.rf_profile_read()
+        tms = ta.elapsed_time(tb) / args.steps
+        tk = {}
+        for name, t in trec:
+            tk.setdefault(name, []).append(t)
+        k3t = sum(tk.get("K3_ter_features", [0])) / max(1, len(tk.get("K3_ter_features", [])))
+        k4t = sum(tk.get("K4_ter_syrk", [0])) / max(1, len(tk.get("K4_ter_syrk", [])))
+        fl_t = 2.0 * m_local * n * p + m_local * n * (n + 1.0)
+        fp8_peak = 2.0 * pk["bf16_tflops"]
+        trf_line = {"what": "G^ter (Algorithm 1 step 4) on the same X, W^ter sparsity eps=0.9, σ^ter matched to "
+                            f"{cfg.act} at the Lemma-1 tau (s-={sm:.4f}, s+={sp:.4f}); per rank",
+                    "ms_per_step": tms, "tflops": fl_t / (tms * 1e-3) / 1e12,
+                    "K3_ter_ms": k3t, "K3_ter_tflops_bf16": 2.0 * m_local * n * p / (k3t * 1e-3) / 1e12 if k3t else None,
+                    "K4_ter_ms": k4t, "K4_ter_tflops_fp8": m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12 if k4t else None,
+                    "K4_ter_frac_fp8_peak": (m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12) / fp8_peak if k4t else None,
+                    "fp8_peak": fp8_peak, "fp8_peak_source": "2 × measured burst bf16 (nominal fp8/bf16 ratio); "
+                                                              "ternary operands toggle few bits, so the power cap "
+                                                              "bites less than for the random-bf16 measurement",
+                    "K4_ter_frac_fp8_nominal_4500": (m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12) / 4500.0 if k4t else None,
+                    "speedup_vs_gaussian_G": ((kernels.get("K3_gemm_sigma", {}).get("avg_ms", 0.0) +
+                                               kernels.get("K4_syrk", {}).get("avg_ms", 0.0)) / (k3t + k4t)
+                                              if (k3t + k4t) > 0 else None)}
+        del Td, ws_t
+
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -386,7 +434,7 @@ def main():
                        "l2": "no flush: inputs/workspace/outputs per step ≫ 126 MB L2"},
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches[0], "clocks": clk, "peaks": pk,
+            "gpu_launches": launches[0], "clocks": clk, "peaks": pk, "trf": trf_line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
