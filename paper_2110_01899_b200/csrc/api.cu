@@ -241,19 +241,30 @@ rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b
   ProfScope ps(name, st);
   auto kern = rfk::tc_gemm_kernel<Cfg, Epi>;
   RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES));
-  const int clusters = std::max(1, std::min(s.num_tiles, sms / 2));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * clusters);
   cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = Cfg::CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  int max_cl = sms / Cfg::CL;
+  if (Cfg::CL > 2) {   // clusters of 4 must fit inside a GPC: ask the occupancy calculator
+    cfg.gridDim = dim3(Cfg::CL * max_cl);
+    int q = 0;
+    RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0) max_cl = std::min(max_cl, q);
+    cudaGetLastError();
+  }
+  const int clusters = std::max(1, std::min(s.num_tiles, max_cl));
+  cfg.gridDim = dim3(Cfg::CL * clusters);
+  if (env_int("RF_DEBUG_LAUNCH", 0))
+    std::fprintf(stderr, "[rf] %s: %d clusters of %d CTAs (%d SMs), %d tiles\n", name, clusters, Cfg::CL,
+                 clusters * Cfg::CL, s.num_tiles);
   RF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, alo, blo, out, s, epi));
   ++g_launches;
   return RF_OK;
@@ -435,6 +446,21 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     s4l.lock_w = lockw;
     s4l.lock_ks = std::max(1, env_int("RF_LOCKKS", 8));
     RF_CUDA_CHECK(cudaMemsetAsync(s4l.prog, 0, 1024, g.st));
+  }
+  if constexpr (kBN4 == 512 && kSplit == 1) {
+  if (!g.pack && env_int("RF_K4_MC", 0)) {
+    // 4-CTA clusters with B multicast: the scheduler walks 512-row super tiles (super-row I2 covers row tiles
+    // 2·I2 and 2·I2 + 1; both need column tiles J ≥ I2 of width 512).
+    using C4m = rfk::TcCfg<kFmt, kSplit, 512, -1, 4>;
+    rfk::Sched sm = rfk::Sched::make(1, 256, 0, (int)((g.n + 511) / 512), (int)((g.n + 511) / 512), kb4, kchunk4,
+                                     raster_gm(4, 4));
+    sm.prog = s4l.prog;
+    sm.lock_w = s4l.lock_w;
+    sm.lock_ks = s4l.lock_ks;
+    rfk::EpiSyrk em{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+    if ((s = launch_tc<C4m>("K4_syrk", tA, tB, tAl, tBl, tO, sm, em, g.sms, g.st))) return s;
+    return ok();
+  }
   }
   if (g.pack) {
     rfk::Sched sp = rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4,

@@ -36,9 +36,15 @@ namespace rfk {
 
 // kStg: 4-KB TMA-store staging buffers per epilogue warp (-1 = default: 1 if stages are large, else 2;
 // 0 for epilogues that store directly from registers, e.g. K3).
+// kCl: CTAs per cluster.  2 = one CTA pair per cluster.  4 = two pairs computing vertically adjacent tiles
+// (row tiles 2I, 2I+1, same column tile): each CTA loads its own A half and ONE of the NSUB B sub-tiles for its
+// rank-in-pair and TMA-multicasts it to the same rank of both pairs, so a B sub-tile leaves L2 once per cluster
+// instead of once per pair (a third less L2 → SM traffic per flop for BN = 512).  Requires NSUB == 2, kSplit == 1.
 template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
-          int kBN /*256 or 512*/, int kStg = -1>
+          int kBN /*256 or 512*/, int kStg = -1, int kCl = 2>
 struct TcCfg {
+  static constexpr int CL = kCl;
+  static_assert(kCl == 2 || (kCl == 4 && kBN == 512 && kSplit == 1), "4-CTA clusters: BN = 512, one operand split");
   static constexpr int BM = 256, BN = kBN;      // pair tile
   static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
   static constexpr int ESZ = kFmt == 1 ? 2 : (kFmt == 3 ? 1 : 4);
@@ -567,7 +573,10 @@ __global__ void __launch_bounds__(384, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
-  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t rank = crank & 1u;                    // rank inside the CTA pair
+  const uint32_t pi = crank >> 1;                      // pair index inside the cluster (kCl = 4)
+  const uint32_t leader = crank & ~1u;                 // cluster rank of this pair's MMA-issuing CTA
   const int cid = (int)ptx::cluster_id_x();
   const int ncl = (int)ptx::ncluster_x();
 
@@ -580,7 +589,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], Cfg::CL / 2);         // released by the MMA commit of every pair reading it
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -598,9 +607,13 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
     // The whole warp walks the loop (lane 0 issues); the leader's warp also runs the lockstep check.
-    const bool lock = sched.prog != nullptr && rank == 0;
+    const bool lock = sched.prog != nullptr && crank == 0;
     const uint64_t pol = sched.load_pol ? ptx::policy_evict_last() : ptx::policy_evict_normal();
-    const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), 0);
+    const uint32_t full0 = ptx::mapa(ptx::smem_u32(&full[0]), leader);
+    // kCl = 4: barrier operand of the multicast B load in the CTA-relative form with the pair bit cleared,
+    // so each destination's bytes are counted on its own pair leader's full barrier.
+    const uint32_t full_rel0 = ptx::smem_u32(&full[0]) & 0xFEFFFFFFu;
+    const uint16_t mc_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
     int stage = 0;
     uint32_t phase = 0;
     uint32_t step = 0;
@@ -609,6 +622,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = cid; t < sched.num_tiles; t += ncl) {
       int ti, tj;
       cur.get(t, ti, tj);
+      if (Cfg::CL == 4) ti = 2 * ti + (int)pi;       // the scheduler walks 512-row super tiles
       const int ra = ti * Cfg::BM + (int)rank * 128;
       const int rb = tj * Cfg::BN + (int)rank * 128;
       for (int c = 0; c < nchunks; ++c) {
@@ -628,14 +642,20 @@ __global__ void __launch_bounds__(384, 1)
           }
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);   // both CTAs' bytes
             const uint32_t fb = full0 + stage * 8;
             const int k = kb * Cfg::BK;
             uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
             uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
             ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
+            if (Cfg::CL == 4) {
+              ptx::tma_load_2d_cg2_mc(b + pi * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)pi, mc_mask,
+                                      pol);
+            } else {
 #pragma unroll
-            for (int s = 0; s < NSUB; ++s) ptx::tma_load_2d_cg2(b + s * Cfg::B_BYTES, &tmB, fb, k, rb + 256 * s, pol);
+              for (int s = 0; s < NSUB; ++s)
+                ptx::tma_load_2d_cg2(b + s * Cfg::B_BYTES, &tmB, fb, k, rb + 256 * s, pol);
+            }
             if (NOPS == 2) {
               ptx::tma_load_2d_cg2(a + Cfg::A_BYTES, &tmA_lo, fb, k, ra, pol);
 #pragma unroll
@@ -695,12 +715,12 @@ __global__ void __launch_bounds__(384, 1)
                   }
                 }
               }
-              ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+              ptx::mma_commit_cg2_mc(&empty[stage], Cfg::CL == 4 ? 0xF : 0x3);   // every CTA that fed the stage
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          if (ptx::elect_one()) ptx::mma_commit_cg2_mc(&tfull[slot], 0x3);
+          if (ptx::elect_one()) ptx::mma_commit_cg2_mc(&tfull[slot], (uint16_t)(0x3u << (2 * pi)));
           __syncwarp();
         }
       }
@@ -716,7 +736,7 @@ __global__ void __launch_bounds__(384, 1)
     cx.lane = lane;
     cx.hint = sched.store_pol;
     cx.pol = ptx::policy_evict_first();
-    const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), leader);
     constexpr int HALF = Cfg::ACC_COLS / 2;
     int it = 0;
     TileCursor cur;
@@ -724,6 +744,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = cid; t < sched.num_tiles; t += ncl) {
       int ti, tj;
       cur.get(t, ti, tj);
+      if (Cfg::CL == 4) ti = 2 * ti + (int)pi;
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
       const int64_t colb = (int64_t)tj * Cfg::BN + h * HALF;
       for (int c = 0; c < nchunks; ++c, ++it) {
