@@ -58,8 +58,12 @@ typedef enum { RF_ACT_TANH = 0, RF_ACT_ERF = 1, RF_ACT_SIGMOID_HALF = 2 } rf_act
 typedef enum { RF_DT_F64 = 0, RF_DT_F32 = 1, RF_DT_BF16 = 2 } rf_dtype;
 typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_TF32 = 3, RF_PREC_BF16 = 4 } rf_prec;
 /* UPPER: write only entries j >= i (the rest of the buffer is untouched).
- * FULL : write all n×n entries; the lower triangle mirrors the upper one (Φ: pivot = row, see below). */
-typedef enum { RF_OUT_UPPER = 0, RF_OUT_FULL = 1 } rf_out;
+ * FULL : write all n×n entries; the lower triangle mirrors the upper one (Φ: pivot = row, see below).
+ * *_CENTERED (NEXT-2): the result is centered in place, K = P·A·P with P = I − (1/n)11ᵀ (Eq. (2)),
+ *   as a post-pass (row sums of the symmetric matrix in fp64, then A_ij − r_i − r_j + s); it is linear, so per-rank
+ *   partial G can each be centered.  Φ: only for the full row range. */
+typedef enum { RF_OUT_UPPER = 0, RF_OUT_FULL = 1, RF_OUT_UPPER_CENTERED = 2, RF_OUT_FULL_CENTERED = 3 } rf_out;
+#define RF_OUT_CENTER 2
 
 /* Gaussian moments at τ (EQ1 coefficients P:1040; Theorem 1):
  *   kd[k][d] = E[(√τ ξ)^k σ^(d)(√τ ξ)], ξ ~ N(0,1), k = 0..4, d = 0..2
@@ -216,6 +220,23 @@ rf_status rf_gram_packed(const void* X, int64_t ldx, const void* W_local, int64_
  * stream-memory wait; wrap-safe comparison).  Returns immediately on the host. */
 rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk_sync, int32_t chunk,
                                uint32_t epoch, void* stream);
+
+/* =============================================================================================
+ * NEXT-2 — Theorem 1's asymptotic equivalent K̃ (EQ6):
+ *   K̃ = P (d1·XᵀX + d2·V A Vᵀ + d0·I_n) P,   P = I_n − (1/n)11ᵀ,
+ * for GMM data x_i = μ_a/√p + z_i (so Z + M Jᵀ/√p = X), V = [J/√p, φ] ∈ R^{n×(K+1)}, A = [[ttᵀ + 2T, t], [tᵀ, 1]]
+ * (the caller forms V and A from its class statistics; d0, d1, d2 from rf_moments).  One tcgen05 pass: the XᵀX
+ * mainloop of K5 with an epilogue d1·g + d2·u_iᵀv_j + d0·δ_ij − r'_i − r'_j, where u_i = A v_i and r'_i = r_i − s/2
+ * come from the exact row means of the uncentred matrix (r_i = (d1·x_iᵀx̄ + d2·u_iᵀv̄ + d0)/n, s = mean r), so the
+ * centring costs no extra pass over the n × n output.
+ *   X   device n × p (ldx): bf16 for RF_PREC_BF16, f32 for RF_PREC_TF32 / RF_PREC_3XTF32.
+ *   V   device f32 n × kv (ldv ≥ kv), 0 ≤ kv ≤ 8 (NULL if kv = 0);  A host f64 kv × kv row-major.
+ *   out RF_OUT_UPPER or RF_OUT_FULL;  Kt device f32 n × n (ldk).  ws ≥ rf_ktilde_workspace_size(p, n, prec).
+ * Async on `stream`. */
+rf_status rf_ktilde_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes);
+rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv, int32_t kv,
+                    const double* A, double d0, double d1, double d2, rf_prec prec, rf_out out, float* Kt, int64_t ldk,
+                    void* ws, size_t ws_bytes, void* stream);
 
 /* =============================================================================================
  * NEXT-1 — Ternary Random Features (TRF): Eq. (3)-(5), Corollary 1 + Eq. (8),

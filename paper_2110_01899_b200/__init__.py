@@ -17,7 +17,7 @@ __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf
            "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_version", "rf_device_supported",
            "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
            "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter",
-           "rf_gram_ter_workspace_size", "RFError", "PREC", "ACT"]
+           "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "RFError", "PREC", "ACT"]
 
 _TORCH_DT = None
 
@@ -294,3 +294,35 @@ def rf_gram_ter(X, T, eps: float, s_minus: float, s_plus: float, out: str = "upp
                                   OUT[out], ctypes.c_void_p(G.data_ptr()), G.stride(0), ctypes.c_void_p(ws.data_ptr()),
                                   ws.numel(), _stream_ptr(stream)))
     return G
+
+
+# ------------------------------------------------------------------------------------------ NEXT-2 (K̃)
+def rf_ktilde_workspace_size(p: int, n: int, prec: str) -> int:
+    need = ctypes.c_size_t()
+    _lib.check(load().rf_ktilde_workspace_size(p, n, PREC[prec], ctypes.byref(need)))
+    return need.value
+
+
+def rf_ktilde(X, V, A, d0: float, d1: float, d2: float, prec: str = "bf16", out: str = "upper", Kt=None, ws=None,
+              stream=None):
+    """Theorem 1's K̃ = P(d1·XᵀX + d2·V A Vᵀ + d0·I)P (EQ6).  X: CUDA (n, p) bf16 (prec bf16) or f32 (tf32/3xtf32);
+    V: CUDA f32 (n, kv) or None; A: host (kv, kv) array-like."""
+    import numpy as np
+    torch = _torch()
+    _check_tensor("X", X, _dtype_for(prec))
+    n, p = X.shape
+    kv = 0 if V is None else V.shape[1]
+    if V is not None:
+        _check_tensor("V", V, torch.float32)
+    Ah = np.ascontiguousarray(np.asarray(A if A is not None else np.zeros((0, 0)), dtype=np.float64).reshape(kv, kv))
+    if Kt is None:
+        Kt = torch.zeros((n, n), dtype=torch.float32, device=X.device)
+    _check_tensor("Kt", Kt, torch.float32)
+    if ws is None:
+        ws = torch.empty(rf_ktilde_workspace_size(p, n, prec), dtype=torch.uint8, device=X.device)
+    _lib.check(load().rf_ktilde(ctypes.c_void_p(X.data_ptr()), X.stride(0), p, n,
+                                ctypes.c_void_p(V.data_ptr() if V is not None else 0), V.stride(0) if V is not None else 1,
+                                kv, Ah.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(d0), float(d1), float(d2),
+                                PREC[prec], OUT[out], ctypes.c_void_p(Kt.data_ptr()), Kt.stride(0),
+                                ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return Kt

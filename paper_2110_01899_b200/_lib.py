@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "RF_OK", 1: "RF_E_INVALID", 2: "RF_E_UNSUPPORTED", 3: "RF_E_N
 ACT = {"tanh": 0, "erf": 1, "sigmoid_half": 2}
 DT = {"f64": 0, "f32": 1, "bf16": 2}
 PREC = {"fp64": 0, "fp32": 1, "3xtf32": 2, "tf32": 3, "bf16": 4}
-OUT = {"upper": 0, "full": 1}
+OUT = {"upper": 0, "full": 1, "upper_centered": 2, "full_centered": 3}
 
 # exported symbols declared in include/rf.h
 SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "rf_tau_workspace_size",
@@ -27,7 +27,8 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_phi_closed_form", "rf_phi_row_split", "rf_last_launch_count", "rf_profile_enable",
            "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt", "rf_pack_plan",
            "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
-           "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter")
+           "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
+           "rf_ktilde_workspace_size", "rf_ktilde")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -97,7 +98,10 @@ def load() -> ctypes.CDLL:
     lib.rf_ter_features.argtypes = [vp, i64, vp, i64, i64, i64, i64, dbl, dbl, dbl, vp, i64, vp]
     lib.rf_gram_ter_workspace_size.argtypes = [i64, i64, i64, ctypes.POINTER(sz)]
     lib.rf_gram_ter.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, dbl, dbl, dbl, ctypes.c_int, vp, i64, vp, sz, vp]
-    for name in ("rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
+    lib.rf_ktilde_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
+    lib.rf_ktilde.argtypes = [vp, i64, i64, i64, vp, i64, i32, ctypes.POINTER(dbl), dbl, dbl, dbl, ctypes.c_int,
+                              ctypes.c_int, vp, i64, vp, sz, vp]
+    for name in ("rf_ktilde_workspace_size", "rf_ktilde", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
                  "rf_gram_ter", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
                  "rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",

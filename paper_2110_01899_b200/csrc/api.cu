@@ -15,6 +15,7 @@
 
 #include "../../include/rf.h"
 #include "k_aux.cuh"
+#include "k_center.cuh"
 #include "k_simt.cuh"
 #include "rf_common.cuh"
 #include "tc_gemm.cuh"
@@ -118,7 +119,7 @@ const char* prec_name(rf_prec p) {
 }
 bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
 bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_SIGMOID_HALF; }
-bool valid_out(int o) { return o == RF_OUT_UPPER || o == RF_OUT_FULL; }
+bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_FULL_CENTERED; }
 
 // ---------------------------------------------------------------- device / driver
 struct DevInfo {
@@ -323,7 +324,7 @@ int64_t odd_line_ld(int64_t cols, int64_t es) {
 
 struct GramPlan {
   int64_t ldS, ldp;
-  size_t off_s0, off_s1, off_xhi, off_xlo, off_whi, off_wlo, off_prog, total;
+  size_t off_s0, off_s1, off_xhi, off_xlo, off_whi, off_wlo, off_prog, off_cen, total;
 };
 GramPlan gram_plan(int64_t p, int64_t n, int64_t m_local, rf_prec prec) {
   GramPlan g{};
@@ -342,13 +343,14 @@ GramPlan gram_plan(int64_t p, int64_t n, int64_t m_local, rf_prec prec) {
     g.off_wlo = off; off = align256(off + (size_t)m_local * g.ldp * 4);
   }
   g.off_prog = off; off = align256(off + 1024);      // K4 lockstep progress words (≤ 256 clusters)
+  g.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);   // centering row sums + s (NEXT-2)
   g.total = off;
   return g;
 }
 
 struct PhiPlan {
   int64_t ldp;
-  size_t off_nrm2, off_tau, off_rc, off_nrm2o, off_xhi, off_xlo, total;
+  size_t off_nrm2, off_tau, off_rc, off_nrm2o, off_xhi, off_xlo, off_cen, total;
 };
 PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   PhiPlan g{};
@@ -362,6 +364,7 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
     g.off_xhi = off; off = align256(off + (size_t)n * g.ldp * 4);
     g.off_xlo = off; off = align256(off + (size_t)n * g.ldp * 4);
   }
+  g.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);
   g.total = off;
   return g;
 }
@@ -544,6 +547,35 @@ rf_status launch_k5(const K5Args& a) {
   return ok();
 }
 
+// NEXT-2: K = P·A·P in place for a symmetric n × n matrix stored in its upper triangle (FULL: all entries
+// stored).  cen = (n + 2) doubles of workspace: r[0..n), s.
+template <typename T>
+rf_status center_pass(T* A, int64_t ld, int64_t n, int full, double* cen, cudaStream_t st) {
+  double* r = cen;
+  double* sp = cen + n;
+  RF_CUDA_CHECK(cudaMemsetAsync(r, 0, (size_t)n * 8, st));
+  const unsigned nt = (unsigned)((n + rfk::kCT - 1) / rfk::kCT);
+  {
+    ProfScope ps("KC_center_rowsum", st);
+    rfk::k_center_rowsum<T><<<dim3(nt, nt), 256, 0, st>>>(A, ld, n, r);
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+  }
+  {
+    ProfScope ps("KC_center_scale", st);
+    rfk::k_center_scale<<<1, 1024, 0, st>>>(r, n, sp);
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+  }
+  {
+    ProfScope ps("KC_center_apply", st);
+    rfk::k_center_apply<T><<<dim3(nt, (unsigned)((n + 7) / 8)), 256, 0, st>>>(A, ld, n, r, sp, full);
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+  }
+  return RF_OK;
+}
+
 rf_status validate_output(const char* name, const void* ptr, int64_t ld, int64_t cols, size_t es) {
   if (!ptr) return fail(RF_E_INVALID, "%s is NULL", name);
   if ((reinterpret_cast<uintptr_t>(ptr) % es) != 0) return fail(RF_E_INVALID, "%s is not %zu-byte aligned", name, es);
@@ -674,9 +706,9 @@ rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec 
   return ok();
 }
 
-rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n, int64_t m_local,
-                  int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg, void* ws,
-                  size_t ws_bytes, void* stream) {
+static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n,
+                              int64_t m_local, int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G,
+                              int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
   if (p <= 0 || n <= 0 || m_local <= 0) return fail(RF_E_INVALID, "rf_gram: p, n, m_local must be > 0");
   if (m_total < m_local) return fail(RF_E_INVALID, "rf_gram: m_total (%lld) < m_local (%lld)", (long long)m_total,
@@ -698,7 +730,7 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
   if ((s = check_device(&dev))) return s;
   cudaStream_t st = (cudaStream_t)stream;
   char* w = (char*)ws;
-  const int full = out == RF_OUT_FULL;
+  const int full = (int)out & 1;
 
   if (prec == RF_PREC_FP64 || prec == RF_PREC_FP32) {
     if (prec == RF_PREC_FP64) {
@@ -731,6 +763,20 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_
   // ≈ 2.6e-6 relative (scripts/accum_experiment.py).
   return gram_tc<2, 3, 256, 2>(ga, kchunk_for(prec, 4));
   return ok();
+}
+
+rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n, int64_t m_local,
+                  int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg, void* ws,
+                  size_t ws_bytes, void* stream) {
+  rf_status s = rf_gram_core(X, ldx, W, ldw, p, n, m_local, m_total, act, prec, out, G, ldg, ws, ws_bytes, stream);
+  if (s || !((int)out & RF_OUT_CENTER)) return s;
+  // NEXT-2: K = P·G·P (Eq. (2)).  Centering is linear, so each rank may center its own partial G.
+  const int32_t launches = g_launches;
+  double* cen = (double*)((char*)ws + gram_plan(p, n, m_local, prec).off_cen);
+  s = prec == RF_PREC_FP64 ? center_pass<double>((double*)G, ldg, n, (int)out & 1, cen, (cudaStream_t)stream)
+                           : center_pass<float>((float*)G, ldg, n, (int)out & 1, cen, (cudaStream_t)stream);
+  g_launches += launches;
+  return s ? s : ok();
 }
 
 rf_status rf_debug_gemm_workspace_size(int64_t M, int64_t N, int64_t K, rf_prec prec, size_t* bytes) {
@@ -806,11 +852,140 @@ rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* byte
 }  // extern "C"
 
 // ------------------------------------------------------------------------------------------------
+// NEXT-2: Theorem 1's K̃ (EQ6) on the tensor cores, centred in the same pass.
+namespace {
+struct KtPlan {
+  int64_t ldp;
+  size_t off_xbar, off_vbar, off_rr, off_s, off_u, off_vt, off_rf, off_xhi, off_xlo, total;
+};
+KtPlan kt_plan(int64_t p, int64_t n, rf_prec prec) {
+  KtPlan k{};
+  k.ldp = odd_line_ld(p, 4);
+  size_t off = 0;
+  k.off_xbar = off; off = align256(off + (size_t)p * 8);
+  k.off_vbar = off; off = align256(off + 8 * 8);
+  k.off_rr = off; off = align256(off + (size_t)n * 8);
+  k.off_s = off; off = align256(off + 16);
+  k.off_u = off; off = align256(off + (size_t)n * 8 * 4);
+  k.off_vt = off; off = align256(off + (size_t)round_up(n, 32) * 8 * 4);
+  k.off_rf = off; off = align256(off + (size_t)n * 4);
+  if (prec == RF_PREC_3XTF32) {
+    k.off_xhi = off; off = align256(off + (size_t)n * k.ldp * 4);
+    k.off_xlo = off; off = align256(off + (size_t)n * k.ldp * 4);
+  }
+  k.total = off;
+  return k;
+}
+}  // namespace
+
+extern "C" {
+
+rf_status rf_ktilde_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "p, n must be > 0");
+  *bytes = kt_plan(p, n, prec).total;
+  return ok();
+}
+
+rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv, int32_t kv,
+                    const double* A, double d0, double d1, double d2, rf_prec prec, rf_out out, float* Kt, int64_t ldk,
+                    void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_ktilde: p, n must be > 0");
+  if (n >= (int64_t(1) << 31) || p >= (int64_t(1) << 31)) return fail(RF_E_INVALID, "rf_ktilde: sizes must be < 2^31");
+  if (kv < 0 || kv > rfk::kMaxKv) return fail(RF_E_INVALID, "rf_ktilde: kv must be in [0, %d]", rfk::kMaxKv);
+  if (kv > 0 && (!V || !A || ldv < kv || (reinterpret_cast<uintptr_t>(V) & 3)))
+    return fail(RF_E_INVALID, "rf_ktilde: V (device f32 n × kv, ldv >= kv) and A (host kv × kv) are required");
+  if (prec != RF_PREC_BF16 && prec != RF_PREC_TF32 && prec != RF_PREC_3XTF32)
+    return fail(RF_E_INVALID, "rf_ktilde: tensor-core precisions only (BF16 with bf16 X; TF32 / 3XTF32 with f32 X)");
+  if (out != RF_OUT_UPPER && out != RF_OUT_FULL)
+    return fail(RF_E_INVALID, "rf_ktilde: out must be UPPER or FULL (K̃ is always centred, EQ6)");
+  if (!std::isfinite(d0) || !std::isfinite(d1) || !std::isfinite(d2)) return fail(RF_E_INVALID, "rf_ktilde: d0, d1, d2 must be finite");
+  const size_t es = esize_of(prec);
+  rf_status s;
+  if ((s = validate_matrix("X", X, ldx, p, es))) return s;
+  if ((s = validate_output("Kt", Kt, ldk, n, 4))) return s;
+  const KtPlan pl = kt_plan(p, n, prec);
+  if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(RF_E_WORKSPACE, "rf_ktilde: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total, ws_bytes);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  double* xbar = (double*)(w + pl.off_xbar);
+  double* vbar = (double*)(w + pl.off_vbar);
+  double* rr = (double*)(w + pl.off_rr);
+  double* sp = (double*)(w + pl.off_s);
+  float* u = (float*)(w + pl.off_u);
+  float* vt = (float*)(w + pl.off_vt);
+  float* rf = (float*)(w + pl.off_rf);
+  rfk::KtA Ak{};
+  for (int a = 0; a < kv; ++a)
+    for (int b = 0; b < kv; ++b) Ak.a[a][b] = A[a * kv + b];
+  RF_CUDA_CHECK(cudaMemsetAsync(xbar, 0, (size_t)p * 8, st));
+  RF_CUDA_CHECK(cudaMemsetAsync(vbar, 0, 8 * 8, st));
+  const unsigned chunks = (unsigned)std::min<int64_t>(std::max<int64_t>(n / 512, 1), 256);
+  {
+    ProfScope ps("KT_prep", st);
+    if (prec == RF_PREC_BF16)
+      rfk::k_colsum<__nv_bfloat16><<<dim3((unsigned)((p + 255) / 256), chunks), 256, 0, st>>>(
+          (const __nv_bfloat16*)X, ldx, n, p, xbar);
+    else
+      rfk::k_colsum<float><<<dim3((unsigned)((p + 255) / 256), chunks), 256, 0, st>>>((const float*)X, ldx, n, p, xbar);
+    if (kv > 0) rfk::k_colsum<float><<<dim3(1, chunks), 256, 0, st>>>(V, ldv, n, kv, vbar);
+    const unsigned rg = (unsigned)((n + 7) / 8);
+    const float* Vp = kv > 0 ? V : nullptr;   // never read when kv = 0
+    if (prec == RF_PREC_BF16)
+      rfk::k_ktilde_rows<__nv_bfloat16><<<rg, 256, 0, st>>>((const __nv_bfloat16*)X, ldx, p, n, Vp,
+                                                            ldv, kv, Ak, d0, d1, d2, xbar, vbar, u, vt, round_up(n, 32), rr);
+    else
+      rfk::k_ktilde_rows<float><<<rg, 256, 0, st>>>((const float*)X, ldx, p, n, Vp, ldv, kv, Ak, d0,
+                                                    d1, d2, xbar, vbar, u, vt, round_up(n, 32), rr);
+    rfk::k_center_scale<<<1, 1024, 0, st>>>(rr, n, sp);
+    rfk::k_center_fold<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rr, sp, n, rf);
+    RF_CUDA_CHECK(cudaGetLastError());
+    g_launches += 5 + (kv > 0);
+  }
+  CUtensorMap tA, tAl, tO;
+  const bool tma_out = make_tmap_out(&tO, Kt, n, n, ldk);
+  rfk::EpiKtilde e{Kt, ldk, n, u, vt, round_up(n, 32), rf, (float)d0, (float)d1, (float)d2, kv, (int)out & 1,
+                   tma_out ? 1 : 0};
+  const int tn = (int)((n + 255) / 256);
+  if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
+    const bool bf = prec == RF_PREC_BF16;
+    if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
+    if (!tma_out) tO = tA;
+    if (bf) {
+      using C = rfk::TcCfg<1, 1, 256, 2>;
+      const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
+      if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    } else {
+      using C = rfk::TcCfg<2, 1, 256, 2>;
+      const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
+      if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    }
+  } else {
+    using C = rfk::TcCfg<2, 3, 256>;
+    float* Xh = (float*)(w + pl.off_xhi);
+    float* Xl = (float*)(w + pl.off_xlo);
+    if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
+    if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, 128))) return s;
+    if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
+    if (!tma_out) tO = tA;
+    const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
+    if ((s = launch_tc<C>("KT_ktilde", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
+  }
+  return ok();
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
 // NEXT-1: Ternary Random Features (Eq. (3)-(5), Corollary 1, Algorithm 1).
 namespace {
 struct TerPlan {
   int64_t ldS;   // bytes per Σ^terᵀ row
-  size_t off_s, off_prog, total;
+  size_t off_s, off_prog, off_cen, total;
 };
 TerPlan ter_plan(int64_t n, int64_t m_local) {
   TerPlan t{};
@@ -818,6 +993,7 @@ TerPlan ter_plan(int64_t n, int64_t m_local) {
   size_t off = 0;
   t.off_s = off; off = align256(off + (size_t)n * t.ldS);
   t.off_prog = off; off = align256(off + 1024);
+  t.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);
   t.total = off;
   return t;
 }
@@ -935,8 +1111,10 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
     s4.lock_ks = std::max(1, env_int("RF_LOCKKS", 8));
     RF_CUDA_CHECK(cudaMemsetAsync(s4.prog, 0, 1024, st));
   }
-  rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), out == RF_OUT_FULL ? 1 : 0, tma_out ? 1 : 0};
+  rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0};
   if ((s = launch_tc<C4>("K4_ter_syrk", tA, tA, tA, tA, tO, s4, e4, dev.sms, st))) return s;
+  if ((int)out & RF_OUT_CENTER)
+    if ((s = center_pass<float>(G, ldg, n, (int)out & 1, (double*)(w + pl.off_cen), st))) return s;
   return ok();
 }
 
@@ -1164,7 +1342,7 @@ rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_
   return ok();
 }
 
-rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
                              const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                              void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
@@ -1232,7 +1410,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
   const double e2 = 0.5 * mloc.kd[2][2];
   const double f0 = mloc.kd[0][1] - mloc.kd[1][2];
   const double f1 = mloc.kd[1][2];
-  const int full = out == RF_OUT_FULL;
+  const int full = (int)out & 1;
   if (prec == RF_PREC_FP64) {
     rfk::RowCoefD* rc = (rfk::RowCoefD*)(w + pl.off_rc);
     double* nj = (double*)(w + pl.off_nrm2o);
@@ -1272,6 +1450,22 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
             (float)f1, row_begin, row_end, w, pl, dev.sms, st};
   if (odd_act && env_int("RF_EQ1_GENERAL", 0) == 0) return launch_k5<true>(ka);
   return launch_k5<false>(ka);
+}
+
+rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                             const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  if (((int)out & RF_OUT_CENTER) && !(row_begin == 0 && row_end == n))
+    return fail(RF_E_INVALID, "rf_phi_closed_form: centering (RF_OUT_*_CENTERED) needs the full row range [0, n)");
+  rf_status s = rf_phi_core(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes,
+                            stream);
+  if (s || !((int)out & RF_OUT_CENTER)) return s;
+  const int32_t launches = g_launches;
+  double* cen = (double*)((char*)ws + phi_plan(p, n, prec).off_cen);
+  s = prec == RF_PREC_FP64 ? center_pass<double>((double*)Phi, ldphi, n, (int)out & 1, cen, (cudaStream_t)stream)
+                           : center_pass<float>((float*)Phi, ldphi, n, (int)out & 1, cen, (cudaStream_t)stream);
+  g_launches += launches;
+  return s ? s : ok();
 }
 
 }  // extern "C"

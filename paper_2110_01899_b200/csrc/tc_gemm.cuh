@@ -523,6 +523,94 @@ struct EpiEq1 {
   }
 };
 
+// NEXT-2: Theorem 1's K̃ (EQ6) from the Gram XᵀX, centred in the same pass:
+//   K̃_ij = d1·g_ij + d2·u_iᵀv_j + d0·δ_ij − r'_i − r'_j,   u_i = A v_i,  g = x_iᵀx_j,  r'_i = r_i − s/2,
+// with r_i = (1/n)(d1·x_iᵀx̄ + d2·u_iᵀv̄ + d0) the row means of the uncentred matrix (x̄ = Σ_j x_j, v̄ = Σ_j v_j)
+// and s their mean: P(M)P = M − r1ᵀ − 1rᵀ + s11ᵀ for the symmetric M = d1XᵀX + d2VAVᵀ + d0I.
+// Per-row data: u (n × 8, zero-padded), r' (n); per-column data: Vt (8 × n), r'.  kv ≤ 8 columns of V.
+struct EpiKtilde {
+  float* Kt;
+  int64_t ld, n;
+  const float* u;     // n × 8
+  const float* vt;    // 8 × nvt (rows 16-B aligned)
+  int64_t nvt;
+  const float* r;     // n: r'_i = r_i − s/2
+  float d0, d1, d2;
+  int kv;
+  int full;
+  int use_tma;
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
+    return col0 < n && row_lo < n && col0 + 31 >= row_lo;
+  }
+  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  struct Pre {
+    float u[8];
+    float r;
+  };
+  __device__ __forceinline__ Pre prefetch(int64_t row_lo, int64_t, uint32_t lane) const {
+    Pre pf;
+    const int64_t row = row_lo + lane;
+    const int64_t rr = row < n ? row : n - 1;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(u + rr * 8));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(u + rr * 8) + 1);
+    pf.u[0] = a.x; pf.u[1] = a.y; pf.u[2] = a.z; pf.u[3] = a.w;
+    pf.u[4] = b.x; pf.u[5] = b.y; pf.u[6] = b.z; pf.u[7] = b.w;
+    pf.r = __ldg(r + rr);
+    return pf;
+  }
+  template <class Ctx>
+  __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&acc)[32], int,
+                                             int, long long, const Pre& pf) const {
+    const int64_t row = row_lo + cx.lane;
+    const bool colfull = col0 + 32 <= n;
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = fmaf(d1, __uint_as_float(acc[e]), -pf.r);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float rj[4];
+      if (colfull) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(r + col0) + q);
+        rj[0] = t.x; rj[1] = t.y; rj[2] = t.z; rj[3] = t.w;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rj[b] = (col0 + 4 * q + b < n) ? __ldg(r + col0 + 4 * q + b) : 0.f;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[4 * q + b] -= rj[b];
+    }
+    for (int k = 0; k < kv; ++k) {
+      const float uk = d2 * pf.u[k];
+      const float* vk = vt + (int64_t)k * nvt + col0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float vj[4];
+        if (colfull) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(vk) + q);
+          vj[0] = t.x; vj[1] = t.y; vj[2] = t.z; vj[3] = t.w;
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) vj[b] = (col0 + 4 * q + b < n) ? __ldg(vk + 4 * q + b) : 0.f;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v[4 * q + b] = fmaf(uk, vj[b], v[4 * q + b]);
+      }
+    }
+    if (col0 <= row_lo + 31 && row_lo <= col0 + 31) {            // chunk crosses the diagonal: the d0·I term
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (col0 + e == row) v[e] += d0;
+    }
+    if (use_tma && col0 >= row_lo + 31) {
+      cx.store_block(row_lo, col0, v);
+    } else {
+      if (row >= n) return;
+      store_row_masked(Kt, ld, n, row, col0, row, v);
+    }
+    if (full) store_mirror(Kt, ld, n, row, col0, v);
+  }
+};
+
 // Raw accumulator D = A·Bᵀ (rectangular, fp32, chunk-accumulated) — the mainloop test hook behind
 // rf_debug_gemm_nt.
 struct EpiRaw {
