@@ -45,6 +45,7 @@ import numpy as np
 from scipy import special as _sp  # erf only (a library definition of σ)
 
 ACTS = ("tanh", "erf", "sigmoid_half")
+_TABLE2 = ("relu", "abs", "sign", "step", "cos", "sin", "ident", "quad", "bump")
 
 
 # --------------------------------------------------------------------------------------------
@@ -52,6 +53,9 @@ ACTS = ("tanh", "erf", "sigmoid_half")
 # --------------------------------------------------------------------------------------------
 def sigma(act: str, x):
     x = np.asarray(x, dtype=np.float64)
+    if act in _TABLE2:                      # NEXT-3 activations (oracle/acts.py)
+        from .acts import sigma2
+        return sigma2(act, x)
     if act == "tanh":
         return np.tanh(x)
     if act == "erf":
@@ -157,6 +161,9 @@ def gauss_expect(f: Callable, N: int = 128) -> float:
 def moments(act, tau: float, N: int = 200) -> Dict[str, object]:
     if not (tau > 0.0):
         raise ValueError("tau must be > 0")
+    if isinstance(act, str) and act in _TABLE2:   # weak derivatives through Stein (oracle/acts.py)
+        from .acts import moments_stein
+        return moments_stein(act, tau)
     s0, s1, s2 = derivs(act)
     x, w = hermite_rule(N)
     t = math.sqrt(tau) * x
@@ -312,3 +319,23 @@ def phi_exact_pair(act, u_a: float, v_b: float, u_b: float, N: int = 120) -> flo
     fa = s0(u_a * x)                                   # over ξ_a
     fb = s0(v_b * x[:, None] + u_b * x[None, :])       # [ξ_a, ξ_b]
     return float(np.sum(w[:, None] * w[None, :] * fa[:, None] * fb))
+
+
+def phi_eq2(Xs: np.ndarray, act: str, tau: Optional[float] = None, mom=None, N: int = 200,
+            rows: Optional[np.ndarray] = None) -> np.ndarray:
+    """As phi_eq1 with the six-term EQ2 instead of EQ1 (NEXT-3)."""
+    from .acts import eq2
+    Xs = np.asarray(Xs, dtype=np.float64)
+    if tau is None:
+        tau = tau_hat(Xs)
+    if mom is None:
+        mom = moments(act, tau, N)
+    Xr = Xs if rows is None else Xs[rows]
+    g = Xr @ Xr.T
+    nrm2 = np.sum(Xr * Xr, axis=1)
+    k = len(Xr)
+    I, J = np.triu_indices(k)
+    u_a, v_b, u_b = gram_schmidt(nrm2[I], nrm2[J], g[I, J], I == J)
+    out = np.full((k, k), np.nan)
+    out[I, J] = eq2(mom, u_a, v_b, u_b)
+    return out
