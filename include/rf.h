@@ -53,8 +53,15 @@ typedef enum {
   RF_E_WORKSPACE = 6     /* workspace pointer NULL or smaller than rf_*_workspace_size() */
 } rf_status;
 
-/* σ ∈ {tanh, erf, sigmoid − 1/2}: the north star's activations (Assumption 3). */
-typedef enum { RF_ACT_TANH = 0, RF_ACT_ERF = 1, RF_ACT_SIGMOID_HALF = 2 } rf_act;
+/* σ ∈ {tanh, erf, sigmoid − 1/2}: the north star's activations (Assumption 3).
+ * NEXT-3 adds the parameter-free activations of Table 2: ReLU max(0,t), |t|, sign(t), 1_{t>0},
+ * cos t, sin t, t, t², the bump e^{−t²/2}.  Their derivatives are taken in the weak sense (Remark 2):
+ * rf_moments evaluates ⟨k,d⟩ from σ alone through Stein's lemma (see rf_moments). */
+typedef enum {
+  RF_ACT_TANH = 0, RF_ACT_ERF = 1, RF_ACT_SIGMOID_HALF = 2,
+  RF_ACT_RELU = 3, RF_ACT_ABS = 4, RF_ACT_SIGN = 5, RF_ACT_STEP = 6, RF_ACT_COS = 7, RF_ACT_SIN = 8,
+  RF_ACT_IDENT = 9, RF_ACT_QUAD = 10, RF_ACT_BUMP = 11
+} rf_act;
 typedef enum { RF_DT_F64 = 0, RF_DT_F32 = 1, RF_DT_BF16 = 2 } rf_dtype;
 typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_TF32 = 3, RF_PREC_BF16 = 4 } rf_prec;
 /* UPPER: write only entries j >= i (the rest of the buffer is untouched).
@@ -94,6 +101,10 @@ int rf_device_supported(int device);
  * Errors: tau <= 0 or not finite → RF_E_INVALID; out == NULL → RF_E_INVALID; non-finite σ → RF_E_NONFINITE.
  */
 rf_status rf_moments(rf_act act, double tau, int32_t nodes, rf_moments_t* out);
+/* NEXT-3 activations (RF_ACT_RELU … RF_ACT_BUMP): nodes is ignored; M_j = E[ξ^j σ(√τξ)] (j ≤ 6) and E[σ²] by
+ * composite Gauss–Legendre on [−L, 0] ∪ [0, L] (split at the kink / jump t = 0, L = 12, 48 panels × 24 nodes per
+ * half), then ⟨k,0⟩ = τ^{k/2}M_k, ⟨k,1⟩ = τ^{(k−1)/2}(M_{k+1} − kM_{k−1}),
+ * ⟨k,2⟩ = τ^{k/2−1}(M_{k+2} − (2k+1)M_k + k(k−1)M_{k−2}) (Stein once / twice); method = 2. */
 
 /* ---------------------------------------------------------------------------------------------
  * rf_estimate_tau — Lemma 1: *tau_out = (1/n) Σ_i ‖x_i‖², fp64 accumulation, deterministic
@@ -149,6 +160,14 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
                              rf_act act, double tau, const rf_moments_t* mom,
                              rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                              void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream);
+
+/* rf_phi_eq2 — as rf_phi_closed_form with the six-term EQ2 instead of EQ1: the O(p^{-1}) truncation the
+ * paper carries to Theorem 1 (NEXT-3):
+ *   Φ2 = ⟨0,0⟩² + ⟨0,0⟩⟨1,1⟩(α + β) + ⟨1,1⟩²αβ + ⟨0,1⟩⟨1,0⟩ν + ⟨0,2⟩⟨2,0⟩ν²/2.
+ * Same arguments, layouts, workspace (rf_phi_workspace_size) and errors. */
+rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                     const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                     void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * rf_phi_row_split — row-block sharding of Φ over `world` ranks with no collective: returns the

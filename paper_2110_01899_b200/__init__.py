@@ -128,8 +128,9 @@ def rf_gram(X, W, act: str = "tanh", prec: str = "bf16", out: str = "upper", m_t
 
 def rf_phi_closed_form(X, act: str = "tanh", tau: float = 0.0, mom: Optional[dict] = None, prec: str = "bf16",
                        out: str = "upper", row_begin: int = 0, row_end: Optional[int] = None, Phi=None, ws=None,
-                       stream=None):
-    """Φ by EQ1 for pairs i ≤ j, rows i in [row_begin, row_end).  tau <= 0 → Lemma 1 τ̂."""
+                       stream=None, form: int = 1):
+    """Φ by EQ1 for pairs i ≤ j, rows i in [row_begin, row_end).  tau <= 0 → Lemma 1 τ̂.
+    form = 2: the six-term EQ2 instead (rf_phi_eq2)."""
     torch = _torch()
     lib = load()
     dt = _dtype_for(prec)
@@ -142,7 +143,8 @@ def rf_phi_closed_form(X, act: str = "tanh", tau: float = 0.0, mom: Optional[dic
     if ws is None:
         ws = torch.empty(rf_phi_workspace_size(p, n, prec), dtype=torch.uint8, device=X.device)
     mp = ctypes.byref(mom["_struct"]) if mom is not None else None
-    _lib.check(lib.rf_phi_closed_form(ctypes.c_void_p(X.data_ptr()), X.stride(0), p, n, ACT[act], float(tau), mp,
+    fn = lib.rf_phi_eq2 if form == 2 else lib.rf_phi_closed_form
+    _lib.check(fn(ctypes.c_void_p(X.data_ptr()), X.stride(0), p, n, ACT[act], float(tau), mp,
                                       PREC[prec], OUT[out], int(row_begin), row_end,
                                       ctypes.c_void_p(Phi.data_ptr()), Phi.stride(0),
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))

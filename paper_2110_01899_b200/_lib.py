@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "librf_b200.so")
 RF_OK, RF_E_INVALID, RF_E_UNSUPPORTED, RF_E_NONFINITE, RF_E_CUDA, RF_E_NCCL, RF_E_WORKSPACE = range(7)
 STATUS_NAMES = {0: "RF_OK", 1: "RF_E_INVALID", 2: "RF_E_UNSUPPORTED", 3: "RF_E_NONFINITE", 4: "RF_E_CUDA",
                 5: "RF_E_NCCL", 6: "RF_E_WORKSPACE"}
-ACT = {"tanh": 0, "erf": 1, "sigmoid_half": 2}
+ACT = {"tanh": 0, "erf": 1, "sigmoid_half": 2, "relu": 3, "abs": 4, "sign": 5, "step": 6, "cos": 7, "sin": 8,
+       "ident": 9, "quad": 10, "bump": 11}
 DT = {"f64": 0, "f32": 1, "bf16": 2}
 PREC = {"fp64": 0, "fp32": 1, "3xtf32": 2, "tf32": 3, "bf16": 4}
 OUT = {"upper": 0, "full": 1, "upper_centered": 2, "full_centered": 3}
@@ -28,7 +29,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt", "rf_pack_plan",
            "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
            "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
-           "rf_ktilde_workspace_size", "rf_ktilde")
+           "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -81,6 +82,8 @@ def load() -> ctypes.CDLL:
     lib.rf_phi_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_phi_closed_form.argtypes = [vp, i64, i64, i64, ctypes.c_int, dbl, ctypes.POINTER(rf_moments_t),
                                        ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, sz, vp]
+    lib.rf_phi_eq2.argtypes = [vp, i64, i64, i64, ctypes.c_int, dbl, ctypes.POINTER(rf_moments_t),
+                               ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, sz, vp]
     lib.rf_phi_row_split.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.rf_last_launch_count.restype = i32
     lib.rf_profile_enable.argtypes = [ctypes.c_int]
@@ -101,7 +104,7 @@ def load() -> ctypes.CDLL:
     lib.rf_ktilde_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_ktilde.argtypes = [vp, i64, i64, i64, vp, i64, i32, ctypes.POINTER(dbl), dbl, dbl, dbl, ctypes.c_int,
                               ctypes.c_int, vp, i64, vp, sz, vp]
-    for name in ("rf_ktilde_workspace_size", "rf_ktilde", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
+    for name in ("rf_phi_eq2", "rf_ktilde_workspace_size", "rf_ktilde", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
                  "rf_gram_ter", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
                  "rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",

@@ -118,7 +118,7 @@ const char* prec_name(rf_prec p) {
   return "?";
 }
 bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
-bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_SIGMOID_HALF; }
+bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_BUMP; }
 bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_FULL_CENTERED; }
 
 // ---------------------------------------------------------------- device / driver
@@ -418,13 +418,16 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
                                          raster_gm(8, 3));
   if (g.act == RF_ACT_TANH) {
-    rfk::EpiSigma<kOut, RF_ACT_TANH> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+    rfk::EpiSigma<kOut, RF_ACT_TANH> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
     if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
   } else if (g.act == RF_ACT_ERF) {
-    rfk::EpiSigma<kOut, RF_ACT_ERF> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+    rfk::EpiSigma<kOut, RF_ACT_ERF> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
     if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
-  } else {
-    rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF> e3{S0, S1, g.pl.ldS, g.n, g.m_local};
+  } else if (g.act == RF_ACT_SIGMOID_HALF) {
+    rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
+    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+  } else {   // NEXT-3 Table-2 activations: one instantiation, σ chosen at run time
+    rfk::EpiSigma<kOut, -1> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
     if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
   }
 
@@ -1342,9 +1345,10 @@ rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_
   return ok();
 }
 
+// form: 1 = EQ1 (P:1040, 18 terms), 2 = EQ2 (P:1082, 6 terms) — same epilogue, other coefficients.
 static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
                              const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
-                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream, int form = 1) {
   g_launches = 0;
   if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_phi_closed_form: p, n must be > 0");
   if (n > (int64_t)1 << 31 || p > (int64_t)1 << 31) return fail(RF_E_INVALID, "rf_phi_closed_form: sizes must be < 2^31");
@@ -1403,13 +1407,15 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   rfk::RowMoments rm;
   std::memcpy(rm.kd, mloc.kd, sizeof(rm.kd));
   rm.inv_st = 1.0 / std::sqrt(tau);
+  rm.form = form;
   const int cgrid = (int)((n + 255) / 256);
-  // C0(s), C1(s) coefficients of the regrouped EQ1 (rf_common.cuh), s = u_b/√τ
-  const double e0 = mloc.kd[0][0] - mloc.kd[1][1] + 0.5 * mloc.kd[2][2];
-  const double e1 = mloc.kd[1][1] - mloc.kd[2][2];
-  const double e2 = 0.5 * mloc.kd[2][2];
-  const double f0 = mloc.kd[0][1] - mloc.kd[1][2];
-  const double f1 = mloc.kd[1][2];
+  // C0(s), C1(s) coefficients of the regrouped EQ1 (rf_common.cuh), s = u_b/√τ.  EQ2 in the same
+  // shape: A0 = ⟨0,0⟩ + α⟨1,1⟩, C0 = ⟨0,0⟩ + β⟨1,1⟩, A1·C1 = ⟨1,0⟩⟨0,1⟩, A2 = ⟨2,0⟩ (k_row_coef, form 2).
+  const double e0 = form == 2 ? mloc.kd[0][0] - mloc.kd[1][1] : mloc.kd[0][0] - mloc.kd[1][1] + 0.5 * mloc.kd[2][2];
+  const double e1 = form == 2 ? mloc.kd[1][1] : mloc.kd[1][1] - mloc.kd[2][2];
+  const double e2 = form == 2 ? 0.0 : 0.5 * mloc.kd[2][2];
+  const double f0 = form == 2 ? mloc.kd[0][1] : mloc.kd[0][1] - mloc.kd[1][2];
+  const double f1 = form == 2 ? 0.0 : mloc.kd[1][2];
   const int full = (int)out & 1;
   if (prec == RF_PREC_FP64) {
     rfk::RowCoefD* rc = (rfk::RowCoefD*)(w + pl.off_rc);
@@ -1445,20 +1451,21 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   }
   // σ odd (tanh, erf, sigmoid − ½: all north-star activations) ⇒ ⟨k,d⟩ = 0 for k + d even ⇒ A0 = A2 = 0;
   // the general form stays available (RF_EQ1_GENERAL=1, tested) for non-odd σ.
-  const bool odd_act = act == RF_ACT_TANH || act == RF_ACT_ERF || act == RF_ACT_SIGMOID_HALF;
+  const bool odd_act = act == RF_ACT_TANH || act == RF_ACT_ERF || act == RF_ACT_SIGMOID_HALF || act == RF_ACT_SIGN ||
+                       act == RF_ACT_SIN || act == RF_ACT_IDENT;
   K5Args ka{X, ldx, p, n, prec, (float*)Phi, ldphi, full, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
             (float)f1, row_begin, row_end, w, pl, dev.sms, st};
   if (odd_act && env_int("RF_EQ1_GENERAL", 0) == 0) return launch_k5<true>(ka);
   return launch_k5<false>(ka);
 }
 
-rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
-                             const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
-                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+static rf_status phi_entry(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                           const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                           void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream, int form) {
   if (((int)out & RF_OUT_CENTER) && !(row_begin == 0 && row_end == n))
     return fail(RF_E_INVALID, "rf_phi_closed_form: centering (RF_OUT_*_CENTERED) needs the full row range [0, n)");
   rf_status s = rf_phi_core(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes,
-                            stream);
+                            stream, form);
   if (s || !((int)out & RF_OUT_CENTER)) return s;
   const int32_t launches = g_launches;
   double* cen = (double*)((char*)ws + phi_plan(p, n, prec).off_cen);
@@ -1466,6 +1473,18 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, r
                            : center_pass<float>((float*)Phi, ldphi, n, (int)out & 1, cen, (cudaStream_t)stream);
   g_launches += launches;
   return s ? s : ok();
+}
+
+rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                             const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                             void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  return phi_entry(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes, stream, 1);
+}
+
+rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+                     const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
+                     void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  return phi_entry(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes, stream, 2);
 }
 
 }  // extern "C"

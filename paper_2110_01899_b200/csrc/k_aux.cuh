@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(1024) k_tau_reduce(const double* __restrict__ 
 struct RowMoments {
   double kd[5][3];
   double inv_st;   // 1/√τ
+  int form;        // 1 = EQ1, 2 = EQ2
 };
 
 // Per-row coefficients of the regrouped EQ1 (rf_common.cuh), fp64 arithmetic, stored as RC = RowCoef
@@ -95,9 +96,10 @@ __global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm
   const double ua = sqrt(r2);                       // u_a = ‖x_i‖
   const double al = ua * m.inv_st - 1.0;            // α = u_a/√τ − 1
   const double h = 0.5 * al * al;
-  const double A0 = m.kd[0][0] + al * m.kd[1][1] + h * m.kd[2][2];
-  const double A1 = m.kd[1][0] + al * m.kd[2][1] + h * m.kd[3][2];
-  const double A2 = m.kd[2][0] + al * m.kd[3][1] + h * m.kd[4][2];
+  const bool eq2 = m.form == 2;     // EQ2 keeps only the α-linear part of A0 and the constants of A1, A2
+  const double A0 = m.kd[0][0] + al * m.kd[1][1] + (eq2 ? 0.0 : h * m.kd[2][2]);
+  const double A1 = eq2 ? m.kd[1][0] : m.kd[1][0] + al * m.kd[2][1] + h * m.kd[3][2];
+  const double A2 = eq2 ? m.kd[2][0] : m.kd[2][0] + al * m.kd[3][1] + h * m.kd[4][2];
   RC c;
   c.a0 = A0;
   c.a1 = A1;

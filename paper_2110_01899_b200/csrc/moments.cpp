@@ -158,8 +158,83 @@ static void fill(const double table[16], double tau, rf_moments_t* out) {
   out->d2 = 0.25 * table[2] * table[2];
 }
 
+// ---------------------------------------------------------------------------------------------
+// NEXT-3 (Table-2 activations, weak derivatives by Stein): σ only.
+static inline double act_value(rf_act act, double t) {
+  switch (act) {
+    case RF_ACT_RELU: return t > 0.0 ? t : 0.0;
+    case RF_ACT_ABS: return std::fabs(t);
+    case RF_ACT_SIGN: return t > 0.0 ? 1.0 : (t < 0.0 ? -1.0 : 0.0);
+    case RF_ACT_STEP: return t > 0.0 ? 1.0 : 0.0;
+    case RF_ACT_COS: return std::cos(t);
+    case RF_ACT_SIN: return std::sin(t);
+    case RF_ACT_IDENT: return t;
+    case RF_ACT_QUAD: return t * t;
+    case RF_ACT_BUMP: return std::exp(-0.5 * t * t);
+    default: return std::nan("");
+  }
+}
+
+// Gauss–Legendre on [−1, 1] by Golub–Welsch (Jacobi matrix: zero diagonal, b_k = k/√(4k² − 1)); weights sum to 2.
+static bool gauss_legendre(int N, std::vector<double>& x, std::vector<double>& w) {
+  std::vector<double> d(N, 0.0), e(N, 0.0), z(N, 0.0);
+  for (int k = 1; k < N; ++k) e[k - 1] = k / std::sqrt(4.0 * k * k - 1.0);
+  z[0] = 1.0;
+  if (!tridiag_ql_first_row(d, e, z)) return false;
+  x = d;
+  w.resize(N);
+  for (int i = 0; i < N; ++i) w[i] = 2.0 * z[i] * z[i];
+  return true;
+}
+
+// M_j = E[ξ^j σ(√τξ)], j = 0..6, and E[σ(√τξ)²]: composite Gauss–Legendre on [−L, 0] and [0, L] (the only kink /
+// jump of these σ is at t = 0, so each half-line integrand is smooth).
+static bool stein_table(rf_act act, double tau, double table[16]) {
+  constexpr int kNodes = 24, kPanels = 48;
+  constexpr double L = 12.0;
+  std::vector<double> gx, gw;
+  if (!gauss_legendre(kNodes, gx, gw)) return false;
+  const double st = std::sqrt(tau), h = L / kPanels;
+  double M[7] = {0, 0, 0, 0, 0, 0, 0}, S2 = 0.0;
+  for (int side = -1; side <= 1; side += 2) {
+    for (int pnl = 0; pnl < kPanels; ++pnl) {
+      const double a = pnl * h;
+      for (int q = 0; q < kNodes; ++q) {
+        const double r = a + 0.5 * h * (gx[q] + 1.0);
+        const double xi = side * r;
+        const double wt = 0.5 * h * gw[q] * 0.3989422804014327 * std::exp(-0.5 * r * r);
+        const double f = act_value(act, st * xi);
+        if (!std::isfinite(f)) return false;
+        double xp = wt;
+        for (int j = 0; j < 7; ++j) {
+          M[j] += xp * f;
+          xp *= xi;
+        }
+        S2 += wt * f * f;
+      }
+    }
+  }
+  auto Mm = [&](int j) { return j >= 0 ? M[j] : 0.0; };
+  for (int k = 0; k < 5; ++k) {
+    table[k * 3 + 0] = std::pow(tau, 0.5 * k) * M[k];
+    table[k * 3 + 1] = std::pow(tau, 0.5 * (k - 1)) * (M[k + 1] - k * Mm(k - 1));
+    table[k * 3 + 2] = std::pow(tau, 0.5 * k - 1.0) * (M[k + 2] - (2 * k + 1) * M[k] + k * (k - 1) * Mm(k - 2));
+  }
+  table[15] = S2;
+  return true;
+}
+
 // returns 0 ok, 1 non-finite, 2 eigen-solver failure
 int compute_moments(rf_act act, double tau, int nodes, rf_moments_t* out) {
+  if ((int)act >= RF_ACT_RELU) {
+    double t[16];
+    if (!stein_table(act, tau, t)) return 1;
+    fill(t, tau, out);
+    out->nodes = 2 * 48 * 24;
+    out->method = 2;
+    out->quad_err_est = 0.0;
+    return 0;
+  }
   std::vector<double> x, w;
   double cur[16], prev[16];
   if (nodes > 0) {

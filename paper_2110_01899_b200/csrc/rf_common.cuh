@@ -14,15 +14,32 @@ constexpr int kNumSMs = 148;
 // ------------------------------------------------------------------------------------------
 // σ.  sigmoid(x) − 1/2 is evaluated as ½·tanh(x/2) (identical function, no cancellation).
 // ------------------------------------------------------------------------------------------
+// NEXT-3 (Table 2): ReLU, |t|, sign, 1_{t>0}, cos, sin, t, t², e^{−t²/2}.
+template <typename T>
+__device__ __forceinline__ T act_table2(int act, T x) {
+  switch (act) {
+    case RF_ACT_RELU: return x > T(0) ? x : T(0);
+    case RF_ACT_ABS: return x < T(0) ? -x : x;
+    case RF_ACT_SIGN: return x > T(0) ? T(1) : (x < T(0) ? T(-1) : T(0));
+    case RF_ACT_STEP: return x > T(0) ? T(1) : T(0);
+    case RF_ACT_COS: return cos(x);
+    case RF_ACT_SIN: return sin(x);
+    case RF_ACT_IDENT: return x;
+    case RF_ACT_QUAD: return x * x;
+    default: return exp(T(-0.5) * x * x);   // RF_ACT_BUMP
+  }
+}
 __device__ __forceinline__ float act_f32(int act, float x) {
   if (act == RF_ACT_TANH) return tanhf(x);
   if (act == RF_ACT_ERF) return erff(x);
-  return 0.5f * tanhf(0.5f * x);
+  if (act == RF_ACT_SIGMOID_HALF) return 0.5f * tanhf(0.5f * x);
+  return act_table2<float>(act, x);
 }
 __device__ __forceinline__ double act_f64(int act, double x) {
   if (act == RF_ACT_TANH) return tanh(x);
   if (act == RF_ACT_ERF) return erf(x);
-  return 0.5 * tanh(0.5 * x);
+  if (act == RF_ACT_SIGMOID_HALF) return 0.5 * tanh(0.5 * x);
+  return act_table2<double>(act, x);
 }
 // Compile-time σ for the tensor-core K3 epilogue.
 template <int kAct>

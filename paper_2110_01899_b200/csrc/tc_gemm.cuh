@@ -249,13 +249,14 @@ __device__ __forceinline__ void store_mirror(float* M, int64_t ld, int64_t n, in
 // ------------------------------------------------------------------------------------------
 
 // K3: Σᵀ[i][k] = σ(z), z = x_iᵀw_k.  kOut: 0 = bf16, 1 = fp32, 2 = fp32 hi/lo split (3×TF32).
-// kAct = rf_act (compile time).
+// kAct = rf_act (compile time), or −1: the runtime `act` (the Table-2 activations of NEXT-3).
 template <int kOut, int kAct>
 struct EpiSigma {
   void* out0;
   void* out1;
   int64_t ld;       // elements
   int64_t M, N;     // n rows (samples), m_local columns (features)
+  int act;          // used when kAct < 0
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
   __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
   struct Pre {};
@@ -268,7 +269,8 @@ struct EpiSigma {
     float s[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e)
-      s[e] = kOut == 0 ? act_bf16out<kAct>(__uint_as_float(r[e])) : act_fixed<kAct>(__uint_as_float(r[e]));
+      s[e] = kAct < 0 ? act_f32(act, __uint_as_float(r[e]))
+                      : (kOut == 0 ? act_bf16out<kAct>(__uint_as_float(r[e])) : act_fixed<kAct>(__uint_as_float(r[e])));
     const bool full = col0 + 32 <= N;
     if (kOut == 0) {
       __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(out0) + row * ld + col0;

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared_symbols():
     src = open(os.path.join(ROOT, "include", "rf.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rf_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -107,7 +107,7 @@ def test_validation_rejects_before_any_launch():
     s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 4, 0, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"m_total" in lib.rf_last_error()
-    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 7, 4, 0,
+    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 42, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"activation" in lib.rf_last_error()
     # workspace too small

@@ -1,0 +1,87 @@
+"""GPU parity of NEXT-3: the Table-2 activations through the whole path (K3's σ epilogue, rf_moments' Stein-form
+moments feeding EQ1) and the six-term EQ2 epilogue (rf_phi_eq2), against the fp64 oracle on the same rounded inputs."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import paper_2110_01899_b200 as rf  # noqa: E402
+import synthetic  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TABLE2 = ["relu", "abs", "sign", "step", "cos", "sin", "ident", "quad", "bump"]
+DT = {"bf16": torch.bfloat16, "3xtf32": torch.float32, "fp32": torch.float32}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    assert rf.rf_device_supported(0), "device 0 is not sm_100"
+    torch.cuda.set_device(0)
+    yield
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("act", TABLE2)
+@pytest.mark.parametrize("prec", ["bf16", "3xtf32", "fp32"])
+def test_gram_table2(act, prec):
+    n, p, m = 300, 72, 400
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((n, p)) / math.sqrt(p)
+    W = rng.standard_normal((m, p))
+    Xd, Wd = torch.tensor(X, device="cuda").to(DT[prec]), torch.tensor(W, device="cuda").to(DT[prec])
+    G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper")
+    torch.cuda.synchronize()
+    ref = oracle.gram(Xd.double().cpu().numpy(), Wd.double().cpu().numpy(), act)
+    I, J = np.triu_indices(n)
+    e = _rel(G.double().cpu().numpy()[I, J], ref[I, J])
+    tol = 2e-3 if prec == "bf16" else (2e-5 if act in ("sign", "step") else 1e-5)
+    print(f"[parity] G {act} {prec}: rel-Frobenius {e:.3e}")
+    assert e <= tol
+
+
+@pytest.mark.parametrize("act", TABLE2)
+@pytest.mark.parametrize("form", [1, 2])
+def test_phi_table2_eq1_eq2(act, form):
+    n, p = 520, 96
+    X = synthetic.make_X(4, n=n, p=p)
+    Xd = torch.tensor(X, device="cuda").to(torch.bfloat16)
+    Xb = Xd.double().cpu().numpy()
+    Phi = rf.rf_phi_closed_form(Xd, act=act, tau=0.0, prec="bf16", out="upper", form=form)
+    torch.cuda.synchronize()
+    ref = (oracle.phi_eq1 if form == 1 else oracle.phi_eq2)(Xb, act)
+    I, J = np.triu_indices(n)
+    e = _rel(Phi.double().cpu().numpy()[I, J], ref[I, J])
+    print(f"[parity] Φ EQ{form} {act} bf16: rel-Frobenius {e:.3e}")
+    assert e <= 1e-5
+
+
+@pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
+def test_phi_eq2_north_star_acts_3xtf32(act):
+    n, p = 700, 128
+    X = synthetic.make_X(1, n=n, p=p)
+    Xd = torch.tensor(X, device="cuda").to(torch.float32)
+    Phi = rf.rf_phi_closed_form(Xd, act=act, tau=0.0, prec="3xtf32", out="full", form=2)
+    torch.cuda.synchronize()
+    ref = oracle.phi_eq2(Xd.double().cpu().numpy(), act)
+    I, J = np.triu_indices(n)
+    Pc = Phi.double().cpu().numpy()
+    e = _rel(Pc[I, J], ref[I, J])
+    print(f"[parity] Φ EQ2 {act} 3xtf32: rel-Frobenius {e:.3e}")
+    assert e <= 1e-5
+    assert np.array_equal(Pc, Pc.T)
+
+
+def test_trf_thresholds_for_relu_matches_table2_targets():
+    """Algorithm 1 for the ReLU kernel (the paper's Fig. 1 setting): thresholds from rf_moments(ReLU)."""
+    from oracle import trf
+    tau = 1.0
+    sm, sp = rf.rf_trf_thresholds_for("relu", tau)
+    t = trf.ternary_moments(sm, sp, tau)
+    assert abs(t["d1"] - 0.25) < 1e-10 and abs(t["d2"] - 1 / (8 * math.pi)) < 1e-10
