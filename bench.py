@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phi", action="store_true")
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
+    ap.add_argument("--g5", default="fused", choices=["fused", "nccl"],
+                    help="N>1: G5 as the fused peer-memory epilogue (default) or chunked NCCL reduce-scatter")
     ap.add_argument("--comm-sms", type=int, default=8,
                     help="N>1: SMs left free during K4 for the overlapped reduce-scatter kernels")
     return ap.parse_args()
@@ -215,10 +217,15 @@ def main():
             ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
             G_own = G
         else:
-            # G5: K4 writes packed triangle tiles; chunked NCCL reduce-scatter overlapped on a comm stream
-            rs = collective.GramReduceScatter(n, p, m_local, m, cfg.act, prec, nchunks=16,
-                                              max_sms=torch.cuda.get_device_properties(device).multi_processor_count
-                                              - args.comm_sms)
+            if args.g5 == "fused" and prec in ("bf16", "tf32"):
+                # G5 fused: K4's epilogue stores each owned tile into the owner's staging buffer over NVLink
+                # (CUDA-IPC peer memory), overlapped with the SYRK; owners then sum their R slices.
+                rs = collective.GramFusedP2P(n, p, m_local, m, cfg.act, prec, nchunks=16)
+            else:
+                # G5 baseline: packed tiles + chunked NCCL reduce-scatter overlapped on a comm stream
+                rs = collective.GramReduceScatter(n, p, m_local, m, cfg.act, prec, nchunks=16,
+                                                  max_sms=torch.cuda.get_device_properties(device).multi_processor_count
+                                                  - args.comm_sms)
             G_own = rs.recv
     if do_phi:
         rb, re_ = rf.rf_phi_row_split(n, world, rank)
@@ -428,8 +435,11 @@ def main():
             "data": "synthetic (seeded PCG64 draws of BASELINE.json configs; no dataset)",
             "config": {"workload": f"configs[{args.config}] {cfg.name}" + (" + Φ on the same X" if do_phi and do_gram else ""),
                        "p": p, "n": n, "m": m, "act": cfg.act, "prec": prec,
-                       "parallelism": (f"G: W sharded over m ({world} ranks) + chunked NCCL reduce-scatter of "
-                                       f"packed triangle tiles overlapped with K4; "
+                       "parallelism": (f"G: W sharded over m ({world} ranks); G5 = "
+                                       + ("K4 epilogue storing packed triangle tiles into the owners' buffers over "
+                                          "NVLink peer memory + owner-side sum" if args.g5 == "fused" else
+                                          "chunked NCCL reduce-scatter of packed triangle tiles overlapped with K4")
+                                       + "; "
                                        f"Φ: row blocks, no collective") if world > 1 else "single GPU",
                        "l2": "no flush: inputs/workspace/outputs per step ≫ 126 MB L2"},
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),

@@ -240,6 +240,26 @@ rf_status rf_gram_packed(const void* X, int64_t ldx, const void* W_local, int64_
 rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk_sync, int32_t chunk,
                                uint32_t epoch, void* stream);
 
+/* Fused G5 over peer memory (the product path for R > 1; the NCCL chunks above are the baseline).
+ * rf_gram_packed_p2p runs K3 + K4 with the packed epilogue storing every 256×256 tile of this rank's partial G
+ * directly into its OWNER's staging buffer: staging[o] is the device-visible base pointer (this process's mapping,
+ * e.g. rf_ipc_open, or its own buffer for o = rank) of rank o's staging buffer of world · plan->recv_elems floats,
+ * laid out [source rank][receive slot][65536] — the stores cross NVLink as tiles finish, overlapped with the
+ * SYRK, and no collective kernel runs.  After every rank's call has completed (stream synchronize + a barrier of
+ * the caller's process group), each owner sums its staging buffer in rank order with rf_pack_reduce into recv
+ * (plan->recv_elems floats; same layout and rf_pack_tile_map as the NCCL path; deterministic).
+ * BF16 / TF32 only (3XTF32's K-chunked accumulation would read tiles back over NVLink); world ≤ 16. */
+rf_status rf_gram_packed_p2p(const void* X, int64_t ldx, const void* W_local, int64_t ldw, int64_t p, int64_t n,
+                             int64_t m_local, int64_t m_total, rf_act act, rf_prec prec, const rf_pack_plan_t* plan,
+                             int32_t rank, float* const* staging, int32_t max_sms, void* ws, size_t ws_bytes,
+                             void* stream);
+rf_status rf_pack_reduce(const rf_pack_plan_t* plan, const float* staging_self, float* recv, void* stream);
+/* CUDA IPC plumbing for the staging buffers (64-byte handles exchanged by the caller's process group). */
+rf_status rf_ipc_handle(const void* dptr, uint8_t* handle64);
+rf_status rf_ipc_open(const uint8_t* handle64, void** dptr);
+rf_status rf_ipc_close(void* dptr);
+
+
 /* =============================================================================================
  * NEXT-2 — Theorem 1's asymptotic equivalent K̃ (EQ6):
  *   K̃ = P (d1·XᵀX + d2·V A Vᵀ + d0·I_n) P,   P = I_n − (1/n)11ᵀ,

@@ -17,7 +17,8 @@ __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf
            "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_version", "rf_device_supported",
            "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
            "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter",
-           "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "RFError", "PREC", "ACT"]
+           "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "rf_gram_packed_p2p",
+           "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "RFError", "PREC", "ACT"]
 
 _TORCH_DT = None
 
@@ -328,3 +329,46 @@ def rf_ktilde(X, V, A, d0: float, d1: float, d2: float, prec: str = "bf16", out:
                                 PREC[prec], OUT[out], ctypes.c_void_p(Kt.data_ptr()), Kt.stride(0),
                                 ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
     return Kt
+
+
+# ------------------------------------------------------------------------------------------ fused G5 (peer memory)
+def rf_gram_packed_p2p(X, W, plan: rf_pack_plan_t, rank: int, staging_ptrs, act: str = "tanh", prec: str = "bf16",
+                       m_total: Optional[int] = None, max_sms: int = 0, ws=None, stream=None):
+    """K3 + K4 with every packed tile stored straight into its owner's staging buffer (include/rf.h).
+    staging_ptrs: `world` integer device addresses (this process's mapping of each rank's staging buffer)."""
+    torch = _torch()
+    dt = _dtype_for(prec)
+    _check_tensor("X", X, dt)
+    _check_tensor("W", W, dt)
+    n, p = X.shape
+    m_local = W.shape[0]
+    m_total = m_local if m_total is None else int(m_total)
+    arr = (ctypes.c_void_p * len(staging_ptrs))(*[ctypes.c_void_p(int(a)) for a in staging_ptrs])
+    if ws is None:
+        ws = torch.empty(rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=X.device)
+    _lib.check(load().rf_gram_packed_p2p(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(W.data_ptr()),
+                                         W.stride(0), p, n, m_local, m_total, ACT[act], PREC[prec], ctypes.byref(plan),
+                                         int(rank), arr, int(max_sms), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                         _stream_ptr(stream)))
+
+
+def rf_pack_reduce(plan: rf_pack_plan_t, staging_self, recv, stream=None):
+    _lib.check(load().rf_pack_reduce(ctypes.byref(plan), ctypes.c_void_p(staging_self.data_ptr()),
+                                     ctypes.c_void_p(recv.data_ptr()), _stream_ptr(stream)))
+    return recv
+
+
+def rf_ipc_handle(t) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _lib.check(load().rf_ipc_handle(ctypes.c_void_p(t.data_ptr()), buf))
+    return buf.raw
+
+
+def rf_ipc_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    _lib.check(load().rf_ipc_open(handle, ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def rf_ipc_close(ptr: int) -> None:
+    _lib.check(load().rf_ipc_close(ctypes.c_void_p(int(ptr))))

@@ -29,7 +29,8 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_profile_read", "rf_debug_gemm_workspace_size", "rf_debug_gemm_nt", "rf_pack_plan",
            "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
            "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
-           "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2")
+           "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2", "rf_gram_packed_p2p", "rf_pack_reduce",
+           "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -104,7 +105,13 @@ def load() -> ctypes.CDLL:
     lib.rf_ktilde_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_ktilde.argtypes = [vp, i64, i64, i64, vp, i64, i32, ctypes.POINTER(dbl), dbl, dbl, dbl, ctypes.c_int,
                               ctypes.c_int, vp, i64, vp, sz, vp]
-    for name in ("rf_phi_eq2", "rf_ktilde_workspace_size", "rf_ktilde", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
+    lib.rf_gram_packed_p2p.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, PP, i32,
+                                       ctypes.POINTER(vp), i32, vp, sz, vp]
+    lib.rf_pack_reduce.argtypes = [PP, vp, vp, vp]
+    lib.rf_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+    lib.rf_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    lib.rf_ipc_close.argtypes = [vp]
+    for name in ("rf_gram_packed_p2p", "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_phi_eq2", "rf_ktilde_workspace_size", "rf_ktilde", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size",
                  "rf_gram_ter", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
                  "rf_moments", "rf_tau_workspace_size", "rf_estimate_tau", "rf_gram_workspace_size", "rf_gram",
                  "rf_phi_workspace_size", "rf_phi_closed_form", "rf_phi_row_split", "rf_profile_enable",

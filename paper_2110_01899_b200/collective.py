@@ -119,3 +119,62 @@ class GramReduceScatter:
 
     def owned_tiles(self) -> np.ndarray:
         return owned_tiles(self.plan, self.rank)
+
+
+class GramFusedP2P:
+    """Fused G5 (the product path for R > 1): K4's epilogue stores each tile of this rank's partial G straight into
+    the owner's staging buffer over NVLink (peer memory mapped with CUDA IPC), so the exchange overlaps the SYRK
+    tile by tile and no collective kernel runs; then each owner sums its R staging slices in rank order.
+
+        fz = GramFusedP2P(n, p, m_local, m_total, act, prec, group)
+        recv = fz(X, W_local)          # same layout as GramReduceScatter (owned_tiles)
+    The process group only exchanges the 64-byte IPC handles and provides the barrier between the two phases.
+    """
+
+    def __init__(self, n: int, p: int, m_local: int, m_total: int, act: str, prec: str, group=None,
+                 nchunks: int = 16, max_sms: int = 0, device=None):
+        import torch
+        import torch.distributed as dist
+        from . import rf_ipc_handle, rf_ipc_open
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n, self.p, self.m_local, self.m_total, self.act, self.prec = n, p, m_local, m_total, act, prec
+        self.plan = rf_pack_plan(n, self.world, nchunks, prec)
+        self.max_sms = max_sms
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.staging = torch.empty(self.world * self.plan.recv_elems, dtype=torch.float32, device=dev)
+        self.recv = torch.empty(self.plan.recv_elems, dtype=torch.float32, device=dev)
+        self.ws = torch.empty(rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=dev)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, rf_ipc_handle(self.staging), group=group)
+        self.opened = []
+        self.ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(self.staging.data_ptr())
+            else:
+                a = rf_ipc_open(h)
+                self.opened.append(a)
+                self.ptrs.append(a)
+
+    def __call__(self, X, W):
+        import torch
+        import torch.distributed as dist
+        from . import rf_gram_packed_p2p, rf_pack_reduce
+        dist.barrier(group=self.group)          # every owner has finished reading its staging buffer
+        rf_gram_packed_p2p(X, W, self.plan, self.rank, self.ptrs, act=self.act, prec=self.prec,
+                           m_total=self.m_total, max_sms=self.max_sms, ws=self.ws)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)          # every rank's stores into my staging buffer have landed
+        rf_pack_reduce(self.plan, self.staging, self.recv)
+        return self.recv
+
+    def owned_tiles(self) -> np.ndarray:
+        return owned_tiles(self.plan, self.rank)
+
+    def close(self):
+        from . import rf_ipc_close
+        for a in self.opened:
+            rf_ipc_close(a)
+        self.opened = []

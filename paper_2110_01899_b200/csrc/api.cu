@@ -1182,6 +1182,7 @@ rf_status build_pack_plan(int64_t n, int32_t world, int32_t nchunks, rf_prec pre
     for (int c = 0; c <= C; ++c) {
       dv->tile0[c] = pl->chunk_tile0[c];
       dv->soff[c] = pl->chunk_send_off[c];
+      dv->roff[c] = pl->chunk_recv_off[c];
       dv->rt0[c] = std::min(gfirst[c] * kPackGm, tiles_m);
       if (c < C) dv->slots[c] = pl->chunk_slots[c];
     }
@@ -1316,6 +1317,99 @@ rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
+// Fused G5 over peer memory (include/rf.h): K4's epilogue stores each tile straight into its owner's staging buffer.
+extern "C" {
+
+rf_status rf_ipc_handle(const void* dptr, uint8_t* handle64) {
+  if (!dptr || !handle64) return fail(RF_E_INVALID, "rf_ipc_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  RF_CUDA_CHECK(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, 64);
+  return ok();
+}
+
+rf_status rf_ipc_open(const uint8_t* handle64, void** dptr) {
+  if (!dptr || !handle64) return fail(RF_E_INVALID, "rf_ipc_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  RF_CUDA_CHECK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ok();
+}
+
+rf_status rf_ipc_close(void* dptr) {
+  if (!dptr) return fail(RF_E_INVALID, "rf_ipc_close: NULL argument");
+  RF_CUDA_CHECK(cudaIpcCloseMemHandle(dptr));
+  return ok();
+}
+
+rf_status rf_gram_packed_p2p(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n,
+                             int64_t m_local, int64_t m_total, rf_act act, rf_prec prec, const rf_pack_plan_t* plan,
+                             int32_t rank, float* const* staging, int32_t max_sms, void* ws, size_t ws_bytes,
+                             void* stream) {
+  g_launches = 0;
+  if (p <= 0 || n <= 0 || m_local <= 0 || m_total < m_local)
+    return fail(RF_E_INVALID, "rf_gram_packed_p2p: need p, n, m_local > 0 and m_total >= m_local");
+  if (!valid_act(act)) return fail(RF_E_INVALID, "rf_gram_packed_p2p: unknown activation %d", (int)act);
+  if (!plan || !staging) return fail(RF_E_INVALID, "rf_gram_packed_p2p: NULL plan or staging array");
+  if (prec != RF_PREC_BF16 && prec != RF_PREC_TF32)
+    return fail(RF_E_INVALID, "rf_gram_packed_p2p: BF16 or TF32 only (3XTF32's K-chunked accumulation would "
+                "read back remote tiles)");
+  if (plan->prec != (int32_t)prec || plan->n != n)
+    return fail(RF_E_INVALID, "rf_gram_packed_p2p: plan was made for another n or precision");
+  if (plan->world > rfk::kMaxP2P) return fail(RF_E_INVALID, "rf_gram_packed_p2p: world > %d", rfk::kMaxP2P);
+  if (rank < 0 || rank >= plan->world) return fail(RF_E_INVALID, "rf_gram_packed_p2p: rank out of range");
+  rf_pack_plan_t chk;
+  rfk::PackDev dv;
+  rf_status s = build_pack_plan(n, plan->world, plan->nchunks, prec, &chk, &dv);
+  if (s) return s;
+  if (!same_plan(plan, &chk)) return fail(RF_E_INVALID, "rf_gram_packed_p2p: plan was not made by rf_pack_plan");
+  for (int r = 0; r < plan->world; ++r) {
+    if (!staging[r] || (reinterpret_cast<uintptr_t>(staging[r]) & 15))
+      return fail(RF_E_INVALID, "rf_gram_packed_p2p: staging[%d] must be a 16-B aligned device pointer", r);
+    dv.peer[r] = staging[r];
+  }
+  dv.p2p = 1;
+  dv.self = rank;
+  dv.recv_elems = plan->recv_elems;
+  const size_t es = esize_of(prec);
+  if ((s = validate_matrix("X", X, ldx, p, es))) return s;
+  if ((s = validate_matrix("W", W, ldw, p, es))) return s;
+  const GramPlan pl = gram_plan(p, n, m_local, prec);
+  if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(RF_E_WORKSPACE, "rf_gram_packed_p2p: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total,
+                ws_bytes);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  const int sms = max_sms > 0 ? std::max(2, std::min(dev.sms, (int)max_sms)) : dev.sms;
+  PackArgs pa{nullptr, nullptr, &dv, plan->world, plan->nchunks};
+  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, 0, nullptr, n, (char*)ws, pl, sms,
+                (cudaStream_t)stream, &pa};
+  if (prec == RF_PREC_BF16) return gram_tc<1, 1, 512, 0>(ga, 0);
+  return gram_tc<2, 1, 512, 1>(ga, 0);
+}
+
+rf_status rf_pack_reduce(const rf_pack_plan_t* plan, const float* staging_self, float* recv, void* stream) {
+  if (!plan || !staging_self || !recv) return fail(RF_E_INVALID, "rf_pack_reduce: NULL argument");
+  if ((reinterpret_cast<uintptr_t>(staging_self) & 15) || (reinterpret_cast<uintptr_t>(recv) & 15))
+    return fail(RF_E_INVALID, "rf_pack_reduce: buffers must be 16-B aligned");
+  DevInfo dev;
+  rf_status s;
+  if ((s = check_device(&dev))) return s;
+  const int64_t recv4 = plan->recv_elems / 4;
+  const int grid = (int)std::min<int64_t>((recv4 + 255) / 256, (int64_t)dev.sms * 8);
+  ProfScope ps("G5_pack_reduce", (cudaStream_t)stream);
+  rfk::k_pack_reduce<<<std::max(grid, 1), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(staging_self), recv4, plan->world, reinterpret_cast<float4*>(recv));
+  RF_CUDA_CHECK(cudaGetLastError());
+  g_launches = 1;
+  return ok();
+}
+
+}  // extern "C"
+
 
 extern "C" {
 

@@ -404,11 +404,18 @@ struct EpiSyrk {
 // index; row tile ti) belongs to the chunk whose row-tile range holds ti; its 256×256 sub-tile sub goes to
 // position u = tiles_per_pair·(t − tile0[c]) + sub of the chunk: owner u mod R, slot u div R.  Whole tiles are
 // stored (no triangle mask).  K-chunked accumulation (3×TF32) re-reads the partial from the slot.
+constexpr int kMaxP2P = 16;                  // ranks reachable by the fused (peer-memory) epilogue
 struct PackDev {
   int64_t tile0[RF_PACK_MAX_CHUNKS + 1];
   int64_t slots[RF_PACK_MAX_CHUNKS];
   int64_t soff[RF_PACK_MAX_CHUNKS + 1];
+  int64_t roff[RF_PACK_MAX_CHUNKS + 1];     // element offset of chunk c in a receive buffer
   int32_t rt0[RF_PACK_MAX_CHUNKS + 1];      // first 256-row tile of chunk c
+  // Fused G5 (rf_gram_packed_p2p): when p2p, the tile of owner o goes to peer[o] (o's staging buffer, mapped
+  // into this process; NVLink stores) at [self][recv slot] instead of the local send buffer.
+  int p2p, self;
+  int64_t recv_elems;
+  float* peer[kMaxP2P];
 };
 struct EpiSyrkPacked {
   float* send;
@@ -433,7 +440,9 @@ struct EpiSyrkPacked {
     const int sub = (int)((col0 - tj0) >> 8);
     const int64_t u = (int64_t)(bn >> 8) * (t - pk.tile0[c]) + sub;
     const int64_t owner = u % world, slot = u / world;
-    float* tile = send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
+    float* tile = pk.p2p ? pk.peer[owner] + (int64_t)pk.self * pk.recv_elems + pk.roff[c] +
+                               slot * (int64_t)(RF_PACK_TILE * RF_PACK_TILE)
+                         : send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
     const int64_t lrow = (row_lo & 255) + cx.lane;
     float* dst = tile + lrow * RF_PACK_TILE + ((col0 - tj0) & 255);
     float v[32];
@@ -453,7 +462,7 @@ struct EpiSyrkPacked {
   // After the warp's last store of pair tile t: publish it (system-scope release) to the chunk counter.
   __device__ __forceinline__ void tile_done(long long t, uint32_t lane) const {
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && sync) {
       int c = 0;
       while (c + 1 < nchunks && t >= pk.tile0[c + 1]) ++c;
       __threadfence_system();
