@@ -196,26 +196,69 @@ struct EpiCtx {
   uint64_t pol;
 
   // Whole 32×32 block → smem (128-B swizzle: 16-B chunk c of row r at chunk c ^ (r & 7), conflict-free)
-  // → one TMA store (rows/cols beyond the matrix are clipped by the tensor map).
-  __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
-    static_assert(kBufs >= 1, "store_block needs staging buffers");
-    uint8_t* b = sbuf + cur * 4096;
-    if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
-    __syncwarp();
+  // → TMA store (rows/cols beyond the matrix are clipped by the tensor map).  With two staging buffers the
+  // blocks are batched in pairs: both are staged, then ONE proxy fence and two TMA stores (the fence waits for
+  // the warp's shared stores; one per block cost ≈ 10 % of a store-bound epilogue, scripts/store_probe.cu).
+  int nst;                 // blocks staged in the open batch (kBufs == 2)
+  int32_t pc0, pr0;        // coordinates of the first staged block
+  __device__ __forceinline__ void issue(const uint8_t* b, int32_t c0, int32_t r0) {
+    if (hint)
+      ptx::tma_store_2d_hint(tm, b, c0, r0, pol);
+    else
+      ptx::tma_store_2d(tm, b, c0, r0);
+  }
+  __device__ __forceinline__ void stage(uint8_t* b, const float (&v)[32]) {
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       *reinterpret_cast<float4*>(b + lane * 128 + ((c ^ (lane & 7)) << 4)) =
           make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+  __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
+    static_assert(kBufs >= 1, "store_block needs staging buffers");
+    if (kBufs == 2) {
+      if (nst == 0) {
+        if (lane == 0) ptx::bulk_wait_read<0>();       // the previous batch has been read out of smem
+        __syncwarp();
+        stage(sbuf, v);
+        pc0 = (int32_t)col0;
+        pr0 = (int32_t)row_lo;
+        nst = 1;
+      } else {
+        stage(sbuf + 4096, v);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          issue(sbuf, pc0, pr0);
+          issue(sbuf + 4096, (int32_t)col0, (int32_t)row_lo);
+          ptx::bulk_commit();
+        }
+        nst = 0;
+      }
+      return;
+    }
+    uint8_t* b = sbuf + cur * 4096;
+    if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
+    __syncwarp();
+    stage(b, v);
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
-      if (hint)
-        ptx::tma_store_2d_hint(tm, b, (int32_t)col0, (int32_t)row_lo, pol);
-      else
-        ptx::tma_store_2d(tm, b, (int32_t)col0, (int32_t)row_lo);
+      issue(b, (int32_t)col0, (int32_t)row_lo);
       ptx::bulk_commit();
     }
     cur = (cur + 1 == kBufs) ? 0 : cur + 1;
+  }
+  // Issue a half-filled batch (end of a tile).
+  __device__ __forceinline__ void flush() {
+    if (kBufs == 2 && nst == 1) {
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        issue(sbuf, pc0, pr0);
+        ptx::bulk_commit();
+      }
+      nst = 0;
+    }
   }
 };
 
@@ -832,6 +875,8 @@ __global__ void __launch_bounds__(384, 1)
     cx.tm = &tmOut;
     cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
     cx.cur = 0;
+    cx.nst = 0;
+    cx.pc0 = cx.pr0 = 0;
     cx.lane = lane;
     cx.hint = sched.store_pol;
     cx.pol = ptx::policy_evict_first();
@@ -875,6 +920,7 @@ __global__ void __launch_bounds__(384, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
       }
+      cx.flush();
       epi.tile_done((long long)t, lane);
     }
     if (lane == 0) ptx::bulk_wait_all();
