@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-phi", action="store_true")
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
+    ap.add_argument("--no-phi4", action="store_true", help="skip the configs[4] Φ-only measurement")
     ap.add_argument("--g5", default="fused", choices=["fused", "nccl"],
                     help="N>1: G5 as the fused peer-memory epilogue (default) or chunked NCCL reduce-scatter")
     ap.add_argument("--comm-sms", type=int, default=8,
@@ -418,6 +419,48 @@ def main():
                                               if (k3t + k4t) > 0 else None)}
         del Td, ws_t
 
+    # ---------------- configs[4] (closed-form Φ only, p = 512, n = 131072): the HBM-write-heavy Φ pass the north star
+    # reports in GB/s; rows split over ranks by equal triangle area, no collective.  Reported beside the headline.
+    phi4_line = None
+    if world == 1 and args.config == 3 and not args.no_phi4:
+        if do_phi:
+            del Phi, ws_p
+        if do_gram:
+            del G, ws_g
+        torch.cuda.empty_cache()
+        c4 = synthetic.CONFIGS[4]
+        X4 = torch.from_numpy(synthetic.make_X(c4)).to(torch.bfloat16).to(device)
+        n4, p4 = c4.n, c4.p
+        Phi4 = torch.empty((n4, n4), dtype=torch.float32, device=device)
+        ws4 = torch.empty(rf.rf_phi_workspace_size(p4, n4, "bf16"), dtype=torch.uint8, device=device)
+        tau4 = rf.rf_estimate_tau(X4)
+        mom4 = rf.rf_moments(c4.act, tau4)
+        for _ in range(args.warmup):
+            rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec="bf16", Phi=Phi4, ws=ws4)
+        torch.cuda.synchronize()
+        rf.rf_profile_read()
+        rf.rf_profile_enable(True)
+        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pa.record(stream)
+        for _ in range(args.steps):
+            rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec="bf16", Phi=Phi4, ws=ws4)
+        pb.record(stream)
+        torch.cuda.synchronize()
+        rf.rf_profile_enable(False)
+        prec4 = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
+        k5ms = sum(prec4) / max(1, len(prec4))
+        pms = pa.elapsed_time(pb) / args.steps
+        tri4 = n4 * (n4 + 1) / 2.0
+        by4 = 4.0 * tri4 + X4.numel() * 2
+        phi4_line = {"what": f"configs[4] {c4.name}: Φ by EQ1, bf16 X (products exact in fp32), fp32 upper triangle",
+                     "ms_per_step": pms, "entries_per_s": tri4 / (pms * 1e-3),
+                     "tflops": p4 * n4 * (n4 + 1.0) / (pms * 1e-3) / 1e12,
+                     "K5_ms": k5ms, "K5_hbm_gbs": by4 / (k5ms * 1e-3) / 1e9 if k5ms else None,
+                     "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / pk["hbm_gbs"] if k5ms else None,
+                     "K5_tflops": p4 * n4 * (n4 + 1.0) / (k5ms * 1e-3) / 1e12 if k5ms else None}
+        del Phi4, ws4, X4
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -444,7 +487,7 @@ def main():
                        "l2": "no flush: inputs/workspace/outputs per step ≫ 126 MB L2"},
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches[0], "clocks": clk, "peaks": pk, "trf": trf_line,
+            "gpu_launches": launches[0], "clocks": clk, "peaks": pk, "trf": trf_line, "phi_configs4": phi4_line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
