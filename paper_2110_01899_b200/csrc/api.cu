@@ -386,6 +386,111 @@ struct GramTcArgs {
 
 constexpr int kPackGm = 8;  // raster group of rf_gram_packed's K4 (chunks are runs of groups)
 
+// Hybrid K4 (bf16 / tf32 / fp8 SYRK, 256×512 pair tiles): 4-CTA clusters with B multicast on the first super
+// rows and, concurrently on a second stream, pair clusters on the remaining row tiles.  Clusters of 4 must sit in
+// one GPC, so only 33 fit (132 SMs); the pair kernel takes the 16 SMs left over.  The pair kernel is released
+// only after the multicast kernel has started (a flag its first CTA writes, awaited by a stream-memory wait), so
+// the multicast kernel always gets its clusters.  The work split follows the per-SM rates measured for the two
+// kernels (f = 0.90 at 33 clusters; a ±2 % change costs 2–18 %).  prog: 1 KB of zeroed-per-call progress words.
+typedef CUresult (*PFN_wait32h)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_wait32h wait32_h() {
+  static PFN_wait32h fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_wait32h>(p);
+  });
+  return fn;
+}
+static cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t s[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && !s[dev]) cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking);
+  return (dev >= 0 && dev < 64) ? s[dev] : nullptr;
+}
+
+template <int kFmt, class Epi>
+rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtensorMap& tO, int64_t n, int kb,
+                           const Epi& e, uint32_t* prog, int lockw, int lockks, int sms, cudaStream_t st,
+                           bool* used) {
+  *used = false;
+  const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512);
+  PFN_wait32h wfn = wait32_h();
+  cudaStream_t st2 = side_stream();
+  if (env_int("RF_K4_HYBRID", 1) == 0 || T < 64 || !wfn || !st2) return RF_OK;
+  using Cm = rfk::TcCfg<kFmt, 1, 512, -1, 4>;
+  using Cp = rfk::TcCfg<kFmt, 1, 512>;
+  // how many 4-CTA clusters fit (GPC packing), and the SMs that leaves for pairs
+  int mcl = 0;
+  {
+    auto kern = rfk::tc_gemm_kernel<Cm, Epi>;
+    RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cm::SMEM_BYTES));
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = Cm::SMEM_BYTES;
+    cfg.gridDim = dim3(sms);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&mcl, kern, &cfg) != cudaSuccess) mcl = 0;
+    cudaGetLastError();
+  }
+  const int left = sms - 4 * mcl;
+  if (mcl <= 0 || left < 2) return RF_OK;
+  // work share of the multicast kernel from the per-SM rate ratio r (measured ≈ 1.11: less L2 traffic per flop
+  // buys clock under the power cap for bf16 and bandwidth for fp8); env RF_HYB_FPCT overrides
+  const double rate = env_int("RF_HYB_R100", 111) / 100.0;
+  double f = (4.0 * mcl * rate) / (4.0 * mcl * rate + (left & ~1));
+  if (env_int("RF_HYB_FPCT", 0) > 0) f = std::min(1.0, env_int("RF_HYB_FPCT", 0) / 100.0);
+  double total = 0;
+  for (int I = 0; I < T; ++I) total += T2 - I / 2;
+  double acc = 0;
+  int S1 = 0;
+  while (S1 < T2 && acc < f * total) {
+    for (int I = 2 * S1; I < std::min(T, 2 * S1 + 2); ++I) acc += T2 - I / 2;
+    ++S1;
+  }
+  if (2 * S1 >= T) return RF_OK;
+  rf_status s;
+  RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
+  rfk::Sched sm = rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
+  rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, raster_gm(8, 4));
+  if (lockw > 0) {
+    sm.prog = prog;
+    sp.prog = prog + 128;
+    sm.lock_w = sp.lock_w = lockw;
+    sm.lock_ks = sp.lock_ks = lockks;
+  }
+  sm.started = prog + 255;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // Σ ready (K3) and the progress words / start flag zeroed
+  if ((s = launch_tc<Cm>(name, tS, tS, tS, tS, tO, sm, e, sms, st))) return s;
+  // the pair kernel: on the side stream, after K3 + the memset (ev0) and once the multicast kernel has started
+  RF_CUDA_CHECK(cudaStreamWaitEvent(st2, ev0, 0));
+  CUresult r = wfn((CUstream)st2, (CUdeviceptr)(uintptr_t)(prog + 255), 1u, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(RF_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  s = launch_tc<Cp>(name, tS, tS, tS, tS, tO, sp, e, left & ~1, st2);
+  RF_CUDA_CHECK(cudaEventRecord(ev1, st2));
+  RF_CUDA_CHECK(cudaStreamWaitEvent(st, ev1, 0));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (s) return s;
+  *used = true;
+  return RF_OK;
+}
+
 // kOut: Σ storage (0 bf16, 1 fp32, 2 fp32 hi/lo).  K3 always uses 256-wide pair tiles (σ epilogue
 // overlapped via two TMEM slots); K4 uses kBN4 (512: one slot, a third less L2 traffic per flop than 256).
 template <int kFmt, int kSplit, int kBN4, int kOut>
@@ -454,6 +559,14 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     RF_CUDA_CHECK(cudaMemsetAsync(s4l.prog, 0, 1024, g.st));
   }
   if constexpr (kBN4 == 512 && kSplit == 1) {
+  if (!g.pack && lockw > 0 && env_int("RF_K4_MC", 0) == 0) {
+    rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+    bool used = false;
+    if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
+                                     &used)))
+      return s;
+    if (used) return ok();
+  }
   if (!g.pack && env_int("RF_K4_MC", 0)) {
     // 4-CTA clusters with B multicast: the scheduler walks 512-row super tiles (super-row I2 covers row tiles
     // 2·I2 and 2·I2 + 1; both need column tiles J ≥ I2 of width 512).
@@ -1115,7 +1228,23 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
     RF_CUDA_CHECK(cudaMemsetAsync(s4.prog, 0, 1024, st));
   }
   rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0};
-  if ((s = launch_tc<C4>("K4_ter_syrk", tA, tA, tA, tA, tO, s4, e4, dev.sms, st))) return s;
+  bool hyb = false;
+  if (lockw > 0 && env_int("RF_K4TER_MC", 0) == 0)
+    if ((s = launch_k4_hybrid<3>("K4_ter_syrk", tA, tO, n, kb4, e4, s4.prog, lockw, s4.lock_ks, dev.sms, st, &hyb)))
+      return s;
+  if (hyb) {
+  } else if (env_int("RF_K4TER_MC", 0)) {
+    // 4-CTA clusters, B multicast (DESIGN.md §6 finding 3): the fp8 SYRK runs at full clock and is L2-bound,
+    // so a third less L2 → SM traffic matters more than the SMs the GPC packing of 4-clusters leaves idle.
+    using C4m = rfk::TcCfg<3, 1, 512, -1, 4>;
+    rfk::Sched sm = rfk::Sched::make(1, 256, 0, (int)((n + 511) / 512), (int)((n + 511) / 512), kb4, 0, raster_gm(4, 4));
+    sm.prog = s4.prog;
+    sm.lock_w = s4.lock_w;
+    sm.lock_ks = s4.lock_ks;
+    if ((s = launch_tc<C4m>("K4_ter_syrk", tA, tA, tA, tA, tO, sm, e4, dev.sms, st))) return s;
+  } else if ((s = launch_tc<C4>("K4_ter_syrk", tA, tA, tA, tA, tO, s4, e4, dev.sms, st))) {
+    return s;
+  }
   if ((int)out & RF_OUT_CENTER)
     if ((s = center_pass<float>(G, ldg, n, (int)out & 1, (double*)(w + pl.off_cen), st))) return s;
   return ok();

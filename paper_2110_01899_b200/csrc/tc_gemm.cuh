@@ -97,6 +97,7 @@ struct Sched {
   // L2 policies: operand loads (0 = evict_normal, 1 = evict_last: operands re-read by many tiles, e.g. X in
   // K5) and epilogue TMA stores (0 = normal, 1 = evict_first: a streamed output must not evict them).
   int load_pol, store_pol;
+  uint32_t* started;    // non-null: the first CTA writes 1 here when the kernel starts (hybrid K4 launch order)
 
   struct Group {
     int I0, I1, J0, Jf;
@@ -156,6 +157,7 @@ struct Sched {
     s.lock_ks = 8;
     s.load_pol = 0;
     s.store_pol = 0;
+    s.started = nullptr;
     long long tot = 0;
     for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
     s.num_tiles = (int)tot;
@@ -739,6 +741,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     ptx::fence_mbarrier_init();
   }
+  if (sched.started && blockIdx.x == 0 && threadIdx.x == 0) ptx::st_relaxed_gpu(sched.started, 1u);
   if (warp == 2) ptx::tmem_alloc_cg2(tmem_slot, 512);
   ptx::tc_fence_before();
   ptx::cluster_sync();
