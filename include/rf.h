@@ -68,9 +68,20 @@ typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_T
  * FULL : write all n×n entries; the lower triangle mirrors the upper one (Φ: pivot = row, see below).
  * *_CENTERED (NEXT-2): the result is centered in place, K = P·A·P with P = I − (1/n)11ᵀ (Eq. (2)),
  *   as a post-pass (row sums of the symmetric matrix in fp64, then A_ij − r_i − r_j + s); it is linear, so per-rank
- *   partial G can each be centered.  Φ: only for the full row range. */
-typedef enum { RF_OUT_UPPER = 0, RF_OUT_FULL = 1, RF_OUT_UPPER_CENTERED = 2, RF_OUT_FULL_CENTERED = 3 } rf_out;
+ *   partial G can each be centered.  Φ: only for the full row range.
+ * PACKED_TRI: only the upper triangle's 256 × 256 tiles, contiguous: with T = ceil(n/256), tile (I, J ≥ I) (rows
+ *   256I.., columns 256J..) starts at float offset 65536·(I·T − I(I−1)/2 + J − I) and is row-major with 256 floats
+ *   per row; the buffer holds rf_packed_tri_elems(n) = 65536·T(T+1)/2 floats (≈ n²/2 + 128n) and must be 16-B
+ *   aligned; ld is ignored.  Entries below the diagonal of diagonal tiles and entries past n are unspecified.
+ *   Tensor-core precisions only (BF16, TF32, 3XTF32; rf_gram_ter); no centering.  It halves the bytes a host
+ *   copy of G or Φ moves (the e2e path of bench.py).
+ */
+typedef enum {
+  RF_OUT_UPPER = 0, RF_OUT_FULL = 1, RF_OUT_UPPER_CENTERED = 2, RF_OUT_FULL_CENTERED = 3, RF_OUT_PACKED_TRI = 4
+} rf_out;
 #define RF_OUT_CENTER 2
+/* Number of floats of an RF_OUT_PACKED_TRI buffer for n samples (n > 0; else RF_E_INVALID). */
+rf_status rf_packed_tri_elems(int64_t n, int64_t* elems);
 
 /* Gaussian moments at τ (EQ1 coefficients P:1040; Theorem 1):
  *   kd[k][d] = E[(√τ ξ)^k σ^(d)(√τ ξ)], ξ ~ N(0,1), k = 0..4, d = 0..2

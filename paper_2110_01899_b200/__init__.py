@@ -18,7 +18,8 @@ __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf
            "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
            "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter",
            "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "rf_gram_packed_p2p",
-           "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "RFError", "PREC", "ACT"]
+           "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems", "RFError", "PREC",
+           "ACT"]
 
 _TORCH_DT = None
 
@@ -90,6 +91,28 @@ def rf_estimate_tau(X, ws=None, stream=None) -> float:
     return out.value
 
 
+def rf_packed_tri_elems(n: int) -> int:
+    """Floats of an out="packed_tri" buffer (include/rf.h RF_OUT_PACKED_TRI)."""
+    e = ctypes.c_int64()
+    _lib.check(load().rf_packed_tri_elems(int(n), ctypes.byref(e)))
+    return e.value
+
+
+def _alloc_out(name, buf, n, out, prec, device):
+    """Output buffer for `out`: n × n, or the 1-D packed triangle (RF_OUT_PACKED_TRI, ld ignored → 256)."""
+    torch = _torch()
+    if out == "packed_tri":
+        if buf is None:
+            buf = torch.empty(rf_packed_tri_elems(n), dtype=_out_dtype(prec), device=device)
+        if not buf.is_cuda or buf.dim() != 1 or buf.dtype != _out_dtype(prec) or buf.numel() < rf_packed_tri_elems(n):
+            raise RFError(_lib.RF_E_INVALID, f"{name}: packed_tri needs a 1-D CUDA tensor of rf_packed_tri_elems(n)")
+        return buf, 256
+    if buf is None:
+        buf = torch.zeros((n, n), dtype=_out_dtype(prec), device=device)
+    _check_tensor(name, buf, _out_dtype(prec))
+    return buf, buf.stride(0)
+
+
 def rf_gram_workspace_size(p: int, n: int, m_local: int, prec: str) -> int:
     need = ctypes.c_size_t()
     _lib.check(load().rf_gram_workspace_size(p, n, m_local, PREC[prec], ctypes.byref(need)))
@@ -116,14 +139,12 @@ def rf_gram(X, W, act: str = "tanh", prec: str = "bf16", out: str = "upper", m_t
     if W.shape[1] != p:
         raise RFError(_lib.RF_E_INVALID, "X and W disagree on p")
     m_total = m_local if m_total is None else int(m_total)
-    if G is None:
-        G = torch.zeros((n, n), dtype=_out_dtype(prec), device=X.device)
-    _check_tensor("G", G, _out_dtype(prec))
+    G, ldg = _alloc_out("G", G, n, out, prec, X.device)
     if ws is None:
         ws = torch.empty(rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=X.device)
     _lib.check(lib.rf_gram(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(W.data_ptr()), W.stride(0),
                            p, n, m_local, m_total, ACT[act], PREC[prec], OUT[out], ctypes.c_void_p(G.data_ptr()),
-                           G.stride(0), ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+                           ldg, ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
     return G
 
 
@@ -138,16 +159,14 @@ def rf_phi_closed_form(X, act: str = "tanh", tau: float = 0.0, mom: Optional[dic
     _check_tensor("X", X, dt)
     n, p = X.shape
     row_end = n if row_end is None else int(row_end)
-    if Phi is None:
-        Phi = torch.zeros((n, n), dtype=_out_dtype(prec), device=X.device)
-    _check_tensor("Phi", Phi, _out_dtype(prec))
+    Phi, ldphi = _alloc_out("Phi", Phi, n, out, prec, X.device)
     if ws is None:
         ws = torch.empty(rf_phi_workspace_size(p, n, prec), dtype=torch.uint8, device=X.device)
     mp = ctypes.byref(mom["_struct"]) if mom is not None else None
     fn = lib.rf_phi_eq2 if form == 2 else lib.rf_phi_closed_form
     _lib.check(fn(ctypes.c_void_p(X.data_ptr()), X.stride(0), p, n, ACT[act], float(tau), mp,
                                       PREC[prec], OUT[out], int(row_begin), row_end,
-                                      ctypes.c_void_p(Phi.data_ptr()), Phi.stride(0),
+                                      ctypes.c_void_p(Phi.data_ptr()), ldphi,
                                       ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
     return Phi
 
@@ -287,14 +306,12 @@ def rf_gram_ter(X, T, eps: float, s_minus: float, s_plus: float, out: str = "upp
     n, p = X.shape
     m_local = T.shape[0]
     m_total = m_local if m_total is None else int(m_total)
-    if G is None:
-        G = torch.zeros((n, n), dtype=torch.float32, device=X.device)
-    _check_tensor("G", G, torch.float32)
+    G, ldg = _alloc_out("G", G, n, out, "bf16", X.device)
     if ws is None:
         ws = torch.empty(rf_gram_ter_workspace_size(p, n, m_local), dtype=torch.uint8, device=X.device)
     _lib.check(load().rf_gram_ter(ctypes.c_void_p(X.data_ptr()), X.stride(0), ctypes.c_void_p(T.data_ptr()),
                                   T.stride(0), p, n, m_local, m_total, float(eps), float(s_minus), float(s_plus),
-                                  OUT[out], ctypes.c_void_p(G.data_ptr()), G.stride(0), ctypes.c_void_p(ws.data_ptr()),
+                                  OUT[out], ctypes.c_void_p(G.data_ptr()), ldg, ctypes.c_void_p(ws.data_ptr()),
                                   ws.numel(), _stream_ptr(stream)))
     return G
 

@@ -20,7 +20,7 @@ ACT = {"tanh": 0, "erf": 1, "sigmoid_half": 2, "relu": 3, "abs": 4, "sign": 5, "
        "ident": 9, "quad": 10, "bump": 11}
 DT = {"f64": 0, "f32": 1, "bf16": 2}
 PREC = {"fp64": 0, "fp32": 1, "3xtf32": 2, "tf32": 3, "bf16": 4}
-OUT = {"upper": 0, "full": 1, "upper_centered": 2, "full_centered": 3}
+OUT = {"upper": 0, "full": 1, "upper_centered": 2, "full_centered": 3, "packed_tri": 4}
 
 # exported symbols declared in include/rf.h
 SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "rf_tau_workspace_size",
@@ -30,7 +30,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
            "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
            "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2", "rf_gram_packed_p2p", "rf_pack_reduce",
-           "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close")
+           "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
     lib.rf_gram_workspace_size.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_gram.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64,
                             vp, sz, vp]
+    lib.rf_packed_tri_elems.argtypes = [i64, ctypes.POINTER(i64)]
     lib.rf_phi_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_phi_closed_form.argtypes = [vp, i64, i64, i64, ctypes.c_int, dbl, ctypes.POINTER(rf_moments_t),
                                        ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, sz, vp]

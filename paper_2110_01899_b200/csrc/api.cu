@@ -119,7 +119,20 @@ const char* prec_name(rf_prec p) {
 }
 bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
 bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_BUMP; }
-bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_FULL_CENTERED; }
+bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_PACKED_TRI; }
+int64_t tri_tiles(int64_t n) {
+  const int64_t T = (n + 255) / 256;
+  return T * (T + 1) / 2;
+}
+// RF_OUT_PACKED_TRI: validation of the packed buffer + its TMA view ((tiles·256) × 256 rows of 256 floats)
+rf_status packed_out_setup(const char* fn, const void* ptr, int64_t n, rf_prec prec, int64_t* tri_T) {
+  if (prec == RF_PREC_FP64 || prec == RF_PREC_FP32)
+    return fail(RF_E_INVALID, "%s: RF_OUT_PACKED_TRI needs a tensor-core precision (BF16, TF32, 3XTF32)", fn);
+  if (!ptr) return fail(RF_E_INVALID, "%s: output is NULL", fn);
+  if (reinterpret_cast<uintptr_t>(ptr) & 15) return fail(RF_E_INVALID, "%s: packed output is not 16-byte aligned", fn);
+  *tri_T = (n + 255) / 256;
+  return RF_OK;
+}
 
 // ---------------------------------------------------------------- device / driver
 struct DevInfo {
@@ -382,6 +395,7 @@ struct GramTcArgs {
   rf_act act; int full; float* G; int64_t ldg;
   char* w; GramPlan pl; int sms; cudaStream_t st;
   const PackArgs* pack;     // non-null: K4 writes packed tiles (rf_gram_packed)
+  int64_t tri_T = 0;        // > 0: RF_OUT_PACKED_TRI (G is the packed triangle)
 };
 
 constexpr int kPackGm = 8;  // raster group of rf_gram_packed's K4 (chunks are runs of groups)
@@ -472,16 +486,22 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
     sm.lock_ks = sp.lock_ks = lockks;
   }
   sm.started = prog + 255;
+  // one trace record `name` brackets both kernels on the caller's stream (fork → join); the parts are traced
+  // as `name`_mc / `name`_tail
+  ProfScope whole(name, st);
+  char nm_mc[32], nm_tail[32];
+  std::snprintf(nm_mc, sizeof(nm_mc), "%s_mc", name);
+  std::snprintf(nm_tail, sizeof(nm_tail), "%s_tail", name);
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
   RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // Σ ready (K3) and the progress words / start flag zeroed
-  if ((s = launch_tc<Cm>(name, tS, tS, tS, tS, tO, sm, e, sms, st))) return s;
+  if ((s = launch_tc<Cm>(nm_mc, tS, tS, tS, tS, tO, sm, e, sms, st))) return s;
   // the pair kernel: on the side stream, after K3 + the memset (ev0) and once the multicast kernel has started
   RF_CUDA_CHECK(cudaStreamWaitEvent(st2, ev0, 0));
   CUresult r = wfn((CUstream)st2, (CUdeviceptr)(uintptr_t)(prog + 255), 1u, CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) return fail(RF_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-  s = launch_tc<Cp>(name, tS, tS, tS, tS, tO, sp, e, left & ~1, st2);
+  s = launch_tc<Cp>(nm_tail, tS, tS, tS, tS, tO, sp, e, left & ~1, st2);
   RF_CUDA_CHECK(cudaEventRecord(ev1, st2));
   RF_CUDA_CHECK(cudaStreamWaitEvent(st, ev1, 0));
   cudaEventDestroy(ev0);
@@ -544,7 +564,8 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   } else {
     tAl = tA; tBl = tA;
   }
-  const bool tma_out = make_tmap_out(&tO, g.G, g.n, g.n, g.ldg);
+  const bool tma_out = g.tri_T > 0 ? make_tmap_out(&tO, g.G, tri_tiles(g.n) * 256, 256, 256)
+                                   : make_tmap_out(&tO, g.G, g.n, g.n, g.ldg);
   if (!tma_out) tO = tA;
   const int kb4 = (int)((g.m_local + C4::BK - 1) / C4::BK);
   const rfk::Sched s4 =
@@ -560,7 +581,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   }
   if constexpr (kBN4 == 512 && kSplit == 1) {
   if (!g.pack && lockw > 0 && env_int("RF_K4_MC", 0) == 0) {
-    rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+    rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
     bool used = false;
     if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
                                      &used)))
@@ -576,7 +597,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     sm.prog = s4l.prog;
     sm.lock_w = s4l.lock_w;
     sm.lock_ks = s4l.lock_ks;
-    rfk::EpiSyrk em{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+    rfk::EpiSyrk em{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
     if ((s = launch_tc<C4m>("K4_syrk", tA, tB, tAl, tBl, tO, sm, em, g.sms, g.st))) return s;
     return ok();
   }
@@ -592,7 +613,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     if ((s = launch_tc<C4>("K4_syrk_packed", tA, tB, tAl, tBl, tA, sp, e4, g.sms, g.st))) return s;
     return ok();
   }
-  rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0};
+  rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
   if ((s = launch_tc<C4>("K4_syrk", tA, tB, tAl, tBl, tO, s4l, e4, g.sms, g.st))) return s;
   return ok();
 }
@@ -604,6 +625,7 @@ struct K5Args {
   float e0, e1, e2, f0, f1;
   int64_t row_begin, row_end;
   char* w; PhiPlan pl; int sms; cudaStream_t st;
+  int64_t tri_T;   // > 0: RF_OUT_PACKED_TRI
 };
 
 #ifndef K5_STG
@@ -626,8 +648,9 @@ rf_status launch_k5(const K5Args& a) {
   struct { int sms; } dev{a.sms};
   rf_status s;
   CUtensorMap tA, tAl, tO;
-  const bool tma_out = make_tmap_out(&tO, Phi, n, n, ldphi);
-  rfk::EpiEq1<kOdd> e{Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full, tma_out ? 1 : 0};
+  const bool tma_out = a.tri_T > 0 ? make_tmap_out(&tO, Phi, tri_tiles(n) * 256, 256, 256)
+                                   : make_tmap_out(&tO, Phi, n, n, ldphi);
+  rfk::EpiEq1<kOdd> e{Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full, tma_out ? 1 : 0, a.tri_T};
   const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
   if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
     const bool bf = prec == RF_PREC_BF16;
@@ -716,6 +739,12 @@ extern "C" {
 
 const char* rf_last_error(void) { return g_err.c_str(); }
 const char* rf_version(void) { return "rf_b200 0.1 (sm_100a: tcgen05/TMA/TMEM; SIMT fp32/fp64)"; }
+
+rf_status rf_packed_tri_elems(int64_t n, int64_t* elems) {
+  if (!elems || n <= 0 || n > ((int64_t)1 << 31)) return fail(RF_E_INVALID, "rf_packed_tri_elems: need n in (0, 2^31]");
+  *elems = tri_tiles(n) * 65536;
+  return ok();
+}
 int32_t rf_last_launch_count(void) { return g_launches; }
 
 rf_status rf_profile_enable(int on) {
@@ -783,6 +812,41 @@ rf_status rf_tau_workspace_size(int64_t n, size_t* bytes) {
   return ok();
 }
 
+// τ̂ (Lemma 1) reduced on the device and handed to the host through a mapped pinned mailbox: the kernel stores the
+// two words over the host link itself and the host waits on an event, so the hand-off does not queue behind bulk
+// copies on the copy engines (a 16-byte cudaMemcpyAsync would wait for any multi-GB D2H in flight).
+struct HostMailbox {
+  volatile double* h = nullptr;
+  cudaEvent_t ev = nullptr;
+  int dev = -1;
+};
+static thread_local HostMailbox t_mailbox;
+
+static rf_status tau_reduce_to_host(const double* nrm2, int64_t n, double* out_dev, cudaStream_t st, double h[2]) {
+  int dev = 0;
+  RF_CUDA_CHECK(cudaGetDevice(&dev));
+  HostMailbox& mb = t_mailbox;
+  if (mb.dev != dev) {
+    void* p = nullptr;
+    RF_CUDA_CHECK(cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+    RF_CUDA_CHECK(cudaEventCreateWithFlags(&mb.ev, cudaEventDisableTiming));
+    mb.h = (volatile double*)p;
+    mb.dev = dev;
+  }
+  mb.h[0] = mb.h[1] = -1.0;
+  {
+    ProfScope ps("K1_tau_reduce", st);
+    rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, out_dev, mb.h);
+  }
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  RF_CUDA_CHECK(cudaEventRecord(mb.ev, st));
+  RF_CUDA_CHECK(cudaEventSynchronize(mb.ev));
+  h[0] = mb.h[0];
+  h[1] = mb.h[1];
+  return RF_OK;
+}
+
 rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n, double* tau_out, void* ws,
                           size_t ws_bytes, void* stream) {
   g_launches = 0;
@@ -801,15 +865,8 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
   double* nrm2 = (double*)ws;
   double* out = (double*)((char*)ws + align256((size_t)n * 8));
   if ((s = launch_rownorm(X, pr, ldx, p, n, nrm2, st))) return s;
-  {
-    ProfScope ps("K1_tau_reduce", st);
-    rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, out);
-  }
-  RF_CUDA_CHECK(cudaGetLastError());
-  ++g_launches;
   double h[2];
-  RF_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
-  RF_CUDA_CHECK(cudaStreamSynchronize(st));
+  if ((s = tau_reduce_to_host(nrm2, n, out, st, h))) return s;
   *tau_out = h[0];
   return ok();
 }
@@ -838,7 +895,12 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
   rf_status s;
   if ((s = validate_matrix("X", X, ldx, p, es))) return s;
   if ((s = validate_matrix("W", W, ldw, p, es))) return s;
-  if ((s = validate_output("G", G, ldg, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  int64_t tri_T = 0;
+  if (out == RF_OUT_PACKED_TRI) {
+    if ((s = packed_out_setup("rf_gram", G, n, prec, &tri_T))) return s;
+  } else if ((s = validate_output("G", G, ldg, n, prec == RF_PREC_FP64 ? 8 : 4))) {
+    return s;
+  }
   const GramPlan pl = gram_plan(p, n, m_local, prec);
   if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(RF_E_WORKSPACE, "rf_gram: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total, ws_bytes);
@@ -872,7 +934,7 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
   }
 
   // Tensor-core path: [K2 split] → K3 (pair tiles 256×256, σ epilogue) → K4 (triangle, SYRK epilogue)
-  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, full, (float*)G, ldg, w, pl, dev.sms, st, nullptr};
+  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, full, (float*)G, ldg, w, pl, dev.sms, st, nullptr, tri_T};
   if (prec == RF_PREC_BF16) return gram_tc<1, 1, 512, 0>(ga, kchunk_for(prec, 0));
   if (prec == RF_PREC_TF32) return gram_tc<2, 1, 512, 1>(ga, kchunk_for(prec, 0));
   // 3×TF32: chunks of 4 K-blocks (128 features) bound the truncating tensor-pipe accumulation to
@@ -1200,7 +1262,12 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
   if (m_local > (int64_t(1) << 24))
     return fail(RF_E_INVALID, "rf_gram_ter: m_local > 2^24 (fp32 accumulation of ±1 products is exact below that)");
   if (!valid_out(out)) return fail(RF_E_INVALID, "rf_gram_ter: unknown output mode %d", (int)out);
-  if ((s = validate_output("G", G, ldg, n, 4))) return s;
+  int64_t tri_T = 0;
+  if (out == RF_OUT_PACKED_TRI) {
+    if ((s = packed_out_setup("rf_gram_ter", G, n, RF_PREC_BF16, &tri_T))) return s;
+  } else if ((s = validate_output("G", G, ldg, n, 4))) {
+    return s;
+  }
   const TerPlan pl = ter_plan(n, m_local);
   if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(RF_E_WORKSPACE, "rf_gram_ter: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total, ws_bytes);
@@ -1216,7 +1283,7 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
   using C4 = rfk::TcCfg<3, 1, 512>;
   CUtensorMap tA, tO;
   if ((s = make_tmap_es(&tA, S, 1, n, m_local, pl.ldS, 128))) return s;
-  const bool tma_out = make_tmap_out(&tO, G, n, n, ldg);
+  const bool tma_out = tri_T > 0 ? make_tmap_out(&tO, G, tri_tiles(n) * 256, 256, 256) : make_tmap_out(&tO, G, n, n, ldg);
   if (!tma_out) tO = tA;
   const int kb4 = (int)((m_local + C4::BK - 1) / C4::BK);
   rfk::Sched s4 = rfk::Sched::make(1, 512, 0, (int)((n + 255) / 256), (int)((n + 511) / 512), kb4, 0, raster_gm(8, 4));
@@ -1227,7 +1294,7 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
     s4.lock_ks = std::max(1, env_int("RF_LOCKKS", 8));
     RF_CUDA_CHECK(cudaMemsetAsync(s4.prog, 0, 1024, st));
   }
-  rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0};
+  rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0, tri_T};
   bool hyb = false;
   if (lockw > 0 && env_int("RF_K4TER_MC", 0) == 0)
     if ((s = launch_k4_hybrid<3>("K4_ter_syrk", tA, tO, n, kb4, e4, s4.prog, lockw, s4.lock_ks, dev.sms, st, &hyb)))
@@ -1586,7 +1653,12 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   const size_t es = esize_of(prec);
   rf_status s;
   if ((s = validate_matrix("X", X, ldx, p, es))) return s;
-  if ((s = validate_output("Phi", Phi, ldphi, n, prec == RF_PREC_FP64 ? 8 : 4))) return s;
+  int64_t tri_T = 0;
+  if (out == RF_OUT_PACKED_TRI) {
+    if ((s = packed_out_setup("rf_phi_closed_form", Phi, n, prec, &tri_T))) return s;
+  } else if ((s = validate_output("Phi", Phi, ldphi, n, prec == RF_PREC_FP64 ? 8 : 4))) {
+    return s;
+  }
   const PhiPlan pl = phi_plan(p, n, prec);
   if (!ws || ws_bytes < pl.total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(RF_E_WORKSPACE, "rf_phi_closed_form: workspace needs %zu bytes, 256-B aligned (got %zu)", pl.total,
@@ -1601,15 +1673,8 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   // Φ1: row norms (all n rows: columns j of every row block need ‖x_j‖²)
   if ((s = launch_rownorm(X, prec, ldx, p, n, nrm2, st))) return s;
   if (!(tau > 0.0)) {   // Lemma 1 τ̂
-    {
-      ProfScope ps("K1_tau_reduce", st);
-      rfk::k_tau_reduce<<<1, 1024, 0, st>>>(nrm2, n, tau_dev);
-    }
-    RF_CUDA_CHECK(cudaGetLastError());
-    ++g_launches;
     double h[2];
-    RF_CUDA_CHECK(cudaMemcpyAsync(h, tau_dev, sizeof(h), cudaMemcpyDeviceToHost, st));
-    RF_CUDA_CHECK(cudaStreamSynchronize(st));
+    if ((s = tau_reduce_to_host(nrm2, n, tau_dev, st, h))) return s;
     if (h[1] != 0.0)
       return fail(RF_E_INVALID, "rf_phi_closed_form: %lld sample(s) with zero norm (v_b undefined, P:1017)",
                   (long long)h[1]);
@@ -1677,7 +1742,7 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   const bool odd_act = act == RF_ACT_TANH || act == RF_ACT_ERF || act == RF_ACT_SIGMOID_HALF || act == RF_ACT_SIGN ||
                        act == RF_ACT_SIN || act == RF_ACT_IDENT;
   K5Args ka{X, ldx, p, n, prec, (float*)Phi, ldphi, full, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
-            (float)f1, row_begin, row_end, w, pl, dev.sms, st};
+            (float)f1, row_begin, row_end, w, pl, dev.sms, st, tri_T};
   if (odd_act && env_int("RF_EQ1_GENERAL", 0) == 0) return launch_k5<true>(ka);
   return launch_k5<false>(ka);
 }

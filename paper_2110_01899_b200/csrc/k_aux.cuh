@@ -44,9 +44,10 @@ __global__ void __launch_bounds__(256) k_rownorm(const T* __restrict__ X, int64_
   if (lane == 0) nrm2[row] = s;
 }
 
-// Single block, fixed summation order ⇒ bit-reproducible τ̂.  out[0] = τ̂, out[1] = #zero-norm rows.
+// Single block, fixed summation order ⇒ bit-reproducible τ̂.  out[0] = τ̂, out[1] = #zero-norm rows; the same two
+// words also go to `host` (mapped pinned memory) when non-null, so the caller reads them without a DMA copy.
 __global__ void __launch_bounds__(1024) k_tau_reduce(const double* __restrict__ nrm2, int64_t n,
-                                                     double* __restrict__ out) {
+                                                     double* __restrict__ out, volatile double* host = nullptr) {
   __shared__ double sh[32];
   __shared__ int zc[32];
   double s = 0.0;
@@ -74,6 +75,11 @@ __global__ void __launch_bounds__(1024) k_tau_reduce(const double* __restrict__ 
     if (threadIdx.x == 0) {
       out[0] = s / (double)n;
       out[1] = (double)z;
+      if (host) {
+        host[0] = s / (double)n;
+        host[1] = (double)z;
+        __threadfence_system();
+      }
     }
   }
 }

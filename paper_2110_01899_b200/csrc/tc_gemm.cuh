@@ -288,6 +288,34 @@ __device__ __forceinline__ void store_mirror(float* M, int64_t ld, int64_t n, in
     if (col0 + e > row && col0 + e < n) M[(col0 + e) * ld + row] = v[e];
 }
 
+// RF_OUT_PACKED_TRI (include/rf.h): 256×256 tile (I, J ≥ I) of the T × T tile grid stored contiguously at tile
+// index I·T − I(I−1)/2 + (J − I), row-major inside the tile.  The TMA map of such a buffer is (tiles·256) × 256.
+__device__ __forceinline__ int64_t tri_tile_index(int64_t I, int64_t J, int64_t T) {
+  return I * T - I * (I - 1) / 2 + (J - I);
+}
+template <class Ctx>
+__device__ __forceinline__ void tri_store(Ctx& cx, float* P, int64_t n, int64_t T, int use_tma, int64_t row_lo,
+                                          int64_t col0, float (&v)[32], int chunk = 0, int nchunks = 1) {
+  const int64_t ti = row_lo >> 8, tj = col0 >> 8;
+  const int64_t u = tri_tile_index(ti, tj, T);
+  const int64_t lr = row_lo & 255, lc = col0 & 255;
+  if (nchunks == 1 && use_tma && col0 >= row_lo + 31) {
+    cx.store_block(u * 256 + lr, lc, v);
+    return;
+  }
+  if (row_lo + cx.lane >= n) return;
+  const int64_t nloc = n - (tj << 8) < 256 ? n - (tj << 8) : 256;
+  const int64_t lo = tj == ti ? lr + cx.lane : 0;                 // j ≥ i inside a diagonal tile
+  float* tile = P + u * 65536;
+  if (chunk > 0) {                                                // K-chunked accumulation: add the partial
+    const float* src = tile + (lr + cx.lane) * 256 + lc;
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (lc + e >= lo && lc + e < nloc) v[e] += src[e];
+  }
+  store_row_masked(tile, 256, nloc, lr + cx.lane, lc, lo, v);
+}
+
 // ------------------------------------------------------------------------------------------
 // Epilogue functors: operator()(ctx, row_lo, col0, r[32], chunk, nchunks, t) for the warp's rows
 // [row_lo, row_lo+32) (row = row_lo + lane) and accumulator columns [col0, col0+32).
@@ -416,6 +444,7 @@ struct EpiSyrk {
   float scale;
   int full;
   int use_tma;      // the output tensor map is valid (16-B aligned rows)
+  int64_t tri_T;    // > 0: RF_OUT_PACKED_TRI with T = ceil(n/256)
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
@@ -429,6 +458,10 @@ struct EpiSyrk {
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
+    if (tri_T > 0) {
+      tri_store(cx, G, n, tri_T, use_tma, row_lo, col0, v, chunk, nchunks);
+      return;
+    }
     if (nchunks == 1 && use_tma && col0 >= row_lo + 31) {
       cx.store_block(row_lo, col0, v);
     } else {
@@ -527,6 +560,7 @@ struct EpiEq1 {
   float e0, e1, e2, f0, f1;
   int full;
   int use_tma;
+  int64_t tri_T;          // > 0: RF_OUT_PACKED_TRI
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
@@ -568,6 +602,10 @@ struct EpiEq1 {
       for (int e = 0; e < 32; e += 2)
         eq1_pair<kOdd>(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, a0_2, a1_2, a2h_2, e0_2,
                        e1_2, e2_2, f0_2, f1_2, v[e], v[e + 1]);
+    }
+    if (tri_T > 0) {
+      tri_store(cx, Phi, n, tri_T, use_tma, row_lo, col0, v);
+      return;
     }
     if (use_tma && col0 >= row_lo + 31) {
       cx.store_block(row_lo, col0, v);

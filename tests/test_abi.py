@@ -120,6 +120,48 @@ def test_validation_rejects_before_any_launch():
     assert s == _lib.RF_E_INVALID and b"row range" in lib.rf_last_error()
 
 
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 1300, 65536])
+def test_packed_tri_size_and_host_decoder(n):
+    """RF_OUT_PACKED_TRI: T(T+1)/2 tiles of 65536 floats; the host decoder (layout.py) places tile (I, J) where
+    include/rf.h says, checked on a buffer whose entries encode their own (row, col)."""
+    from paper_2110_01899_b200 import layout
+    T = -(-n // 256)
+    assert rf.rf_packed_tri_elems(n) == T * (T + 1) // 2 * 65536 == layout.packed_tri_elems(n)
+    if n > 1300:
+        return
+    P = np.full(layout.packed_tri_elems(n), -1.0)
+    for I in range(T):
+        for J in range(I, T):
+            base = 65536 * (I * T - I * (I - 1) // 2 + J - I)
+            r, c = np.meshgrid(np.arange(256) + 256 * I, np.arange(256) + 256 * J, indexing="ij")
+            P[base:base + 65536] = (r * 100000 + c).ravel()
+    D = layout.unpack_tri(P, n, out=np.full((n, n), -2.0))
+    I, J = np.triu_indices(n)
+    assert np.array_equal(D[I, J], I * 100000 + J)
+    il = np.tril_indices(n, -1)
+    assert np.all(D[il] == -2.0)
+
+
+def test_packed_tri_validation():
+    lib = rf.load()
+    e = ctypes.c_int64()
+    assert lib.rf_packed_tri_elems(0, ctypes.byref(e)) == _lib.RF_E_INVALID
+    buf = (ctypes.c_char * 4096)()
+    a16 = (ctypes.addressof(buf) + 15) // 16 * 16
+    # fp32 (SIMT) precision cannot write the packed layout
+    s = lib.rf_gram(ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 1, 4,
+                    ctypes.c_void_p(a16), 0, ctypes.c_void_p(a16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"PACKED_TRI" in lib.rf_last_error()
+    # misaligned packed buffer
+    s = lib.rf_phi_closed_form(ctypes.c_void_p(a16), 64, 64, 512, 0, 1.0, None, 4, 4, 0, 512,
+                               ctypes.c_void_p(a16 + 4), 0, ctypes.c_void_p(a16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"16-byte" in lib.rf_last_error()
+    # centering is not defined for the packed layout: 4 | CENTER is not a valid mode
+    s = lib.rf_gram(ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 4, 6,
+                    ctypes.c_void_p(a16), 8, ctypes.c_void_p(a16), 16, None)
+    assert s == _lib.RF_E_INVALID and b"output mode" in lib.rf_last_error()
+
+
 def test_no_cpu_fallback_without_gpu():
     """On a host with no usable sm_100 device a well-formed call fails loudly (never computes on CPU)."""
     import torch
