@@ -1,14 +1,15 @@
-# Round evidence on one B200: bench line, launch list, clocks, ncu --set full of K4 and K5 from bench.py.
+# Round evidence on one B200: tests, smoke, bench line, reference arm, launch list, ncu --set full of K4 (both
+# kernels of the hybrid launch) and K5 from bench.py.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; tail -3 gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json
-B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-trf --no-phi4"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 10 -c 1 -o gpurun_out/k4_bench_full $B > gpurun_out/ncu_k4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 11 -c 1 -o gpurun_out/k5_bench_full $B > gpurun_out/ncu_k5.log 2>&1
-tail -2 gpurun_out/ncu_k4.log gpurun_out/ncu_k5.log
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 13 -c 2 -o gpurun_out/k4_bench_full $B > gpurun_out/ncu_k4.log 2>&1
+tail -2 gpurun_out/ncu_k4.log
 ls -la gpurun_out
