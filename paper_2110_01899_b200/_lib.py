@@ -11,7 +11,7 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librf_b200.so")
+LIB_PATH = os.environ.get("RF_B200_LIB") or os.path.join(_HERE, "librf_b200.so")   # env: A/B experiments only
 
 RF_OK, RF_E_INVALID, RF_E_UNSUPPORTED, RF_E_NONFINITE, RF_E_CUDA, RF_E_NCCL, RF_E_WORKSPACE = range(7)
 STATUS_NAMES = {0: "RF_OK", 1: "RF_E_INVALID", 2: "RF_E_UNSUPPORTED", 3: "RF_E_NONFINITE", 4: "RF_E_CUDA",
