@@ -256,7 +256,7 @@ rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b
   auto kern = rfk::tc_gemm_kernel<Cfg, Epi>;
   RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM_BYTES));
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(384);
+  cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -446,7 +446,7 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
     auto kern = rfk::tc_gemm_kernel<Cm, Epi>;
     RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cm::SMEM_BYTES));
     cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(384);
+    cfg.blockDim = dim3(Cm::THREADS);
     cfg.dynamicSmemBytes = Cm::SMEM_BYTES;
     cfg.gridDim = dim3(sms);
     cudaLaunchAttribute attr[1];
@@ -631,6 +631,16 @@ struct K5Args {
 #ifndef K5_STG
 #define K5_STG 2
 #endif
+// One K5 launch over row tiles [rt0, rt1) of the triangle (tA: X or its hi part; tAl: the lo part in 3×TF32).
+template <class C, class E>
+rf_status k5_go(const CUtensorMap& tA, const CUtensorMap& tAl, const CUtensorMap& tO, const E& e, int64_t p, int rt0,
+                int rt1, int tn, int sms, cudaStream_t st) {
+  rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
+  sc.load_pol = env_int("RF_K5_LOADPOL", 1);
+  sc.store_pol = env_int("RF_K5_STOREPOL", 1);
+  return launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, sms, st);
+}
+
 // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
 template <bool kOdd>
 rf_status launch_k5(const K5Args& a) {
@@ -656,32 +666,27 @@ rf_status launch_k5(const K5Args& a) {
     const bool bf = prec == RF_PREC_BF16;
     if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
     if (!tma_out) tO = tA;
-    if (bf) {
-      using C = rfk::TcCfg<1, 1, 256, K5_STG>;
-      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-      sc.load_pol = env_int("RF_K5_LOADPOL", 1);
-      sc.store_pol = env_int("RF_K5_STOREPOL", 1);
-      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+    // Short K (p ≤ 512): the EQ1 epilogue, latency-bound at two warps per SM sub-partition, sets the pace, and 12
+    // epilogue warps (three per TMEM lane quarter) help (configs[4]: 10.86 → 9.98 ms).  Long K: the MMA sets it
+    // and the 8-warp kernel's fifth operand stage wins (configs[3], p = 1024: 4.3 vs 5.0 ms).  DESIGN.md §7.
+    const bool w12 = env_int("RF_K5_W12", p <= 512 ? 1 : 0) != 0;
+    if (bf && w12) {
+      if ((s = k5_go<rfk::TcCfg<1, 1, 256, 2, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+    } else if (bf) {
+      if ((s = k5_go<rfk::TcCfg<1, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+    } else if (w12) {
+      if ((s = k5_go<rfk::TcCfg<2, 1, 256, 2, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else {
-      using C = rfk::TcCfg<2, 1, 256, K5_STG>;
-      rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-      sc.load_pol = env_int("RF_K5_LOADPOL", 1);
-      sc.store_pol = env_int("RF_K5_STOREPOL", 1);
-      if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
+      if ((s = k5_go<rfk::TcCfg<2, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     }
-  } else {
-    using C = rfk::TcCfg<2, 3, 256>;
+  } else {   // 3×TF32: never K-chunked (EQ1 is nonlinear in g); 8 warps keep three 64-KB operand stages
     float* Xh = (float*)(w + pl.off_xhi);
     float* Xl = (float*)(w + pl.off_xlo);
     if ((s = launch_split((const float*)X, ldx, n, p, Xh, Xl, pl.ldp, dev.sms, st))) return s;
     if ((s = make_tmap(&tA, Xh, false, n, p, pl.ldp, 128))) return s;
     if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
     if (!tma_out) tO = tA;
-    rfk::Sched sc =
-        rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));   // EQ1 is nonlinear in g
-    sc.load_pol = env_int("RF_K5_LOADPOL", 1);
-    sc.store_pol = env_int("RF_K5_STOREPOL", 1);
-    if ((s = launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
+    if ((s = k5_go<rfk::TcCfg<2, 3, 256>>(tA, tAl, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
   }
   return ok();
 }

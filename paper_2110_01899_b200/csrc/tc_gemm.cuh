@@ -41,7 +41,7 @@ namespace rfk {
 // rank-in-pair and TMA-multicasts it to the same rank of both pairs, so a B sub-tile leaves L2 once per cluster
 // instead of once per pair (a third less L2 → SM traffic per flop for BN = 512).  Requires NSUB == 2, kSplit == 1.
 template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
-          int kBN /*256 or 512*/, int kStg = -1, int kCl = 2>
+          int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8>
 struct TcCfg {
   static constexpr int CL = kCl;
   static_assert(kCl == 2 || (kCl == 4 && kBN == 512 && kSplit == 1), "4-CTA clusters: BN = 512, one operand split");
@@ -56,7 +56,11 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + NSUB * B_BYTES);
   static constexpr int ACC_COLS = kBN;
   static constexpr int ACC_SLOTS = 512 / kBN;
-  static constexpr int EPI_WARPS = 8;
+  // 8 epilogue warps (two per TMEM lane quarter, each owning half of the accumulator columns), or 12 (three per
+  // quarter, 32-column chunks dealt round-robin; unpipelined TMEM loads to fit 128 registers per thread)
+  static constexpr int EPI_WARPS = kEpiW;
+  static_assert(kEpiW == 8 || kEpiW == 12, "8 or 12 epilogue warps");
+  static constexpr int THREADS = 128 + 32 * kEpiW;
   static constexpr int STG_BUFS = kStg >= 0 ? kStg : ((kSplit == 3 || kBN == 512) ? 1 : 2);   // per epi warp
   static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
   static constexpr int STAGES = (225 * 1024 - STG_BYTES) / STAGE_BYTES;
@@ -736,7 +740,7 @@ struct EpiRaw {
 // The kernel.  Launch: grid = 2 × (#clusters), cluster dims (2,1,1), 384 threads, Cfg::SMEM_BYTES.
 // ------------------------------------------------------------------------------------------
 template <class Cfg, class Epi>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA_lo, const __grid_constant__ CUtensorMap tmB_lo,
                    const __grid_constant__ CUtensorMap tmOut, const Sched sched, const Epi epi) {
@@ -911,7 +915,7 @@ __global__ void __launch_bounds__(384, 1)
   } else if (warp >= 4) {
     // ===== Epilogue: TMEM → registers → fused op → global (8 warps) =====
     const uint32_t q = warp & 3;               // TMEM lane quarter this warp may access
-    const uint32_t h = (warp - 4) >> 2;        // column half of the accumulator
+    const uint32_t h = (warp - 4) >> 2;        // column share of the accumulator (0 .. EPI_WARPS/4 − 1)
     EpiCtx<Cfg::STG_BUFS> cx;
     cx.tm = &tmOut;
     cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
@@ -936,6 +940,26 @@ __global__ void __launch_bounds__(384, 1)
         const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
         const uint32_t tbase = tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF;
+        if constexpr (Cfg::EPI_WARPS == 12) {
+          // three warps per lane quarter: 32-column chunks cc ≡ h (mod 3) of the accumulator row
+          const int64_t col_t = (int64_t)tj * Cfg::BN;
+          const uint32_t tb = tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS;
+          const typename Epi::Pre pf = epi.prefetch(row_lo, col_t, lane);
+          ptx::mbar_wait(&tfull[slot], acc_phase);
+          ptx::tc_fence_after();
+          uint32_t ra[32];
+#pragma unroll 1
+          for (int cc = (int)h; cc < Cfg::ACC_COLS / 32; cc += Cfg::EPI_WARPS / 4) {
+            ptx::tmem_ld_32x32b_x32(tb + cc * 32, ra);
+            ptx::tmem_ld_wait();
+            const int64_t col0 = col_t + cc * 32;
+            if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, ra, c, nchunks, (long long)t, pf);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
+          continue;
+        }
         const typename Epi::Pre pf = epi.prefetch(row_lo, colb, lane);   // per-row inputs: before the wait
         ptx::mbar_wait(&tfull[slot], acc_phase);
         ptx::tc_fence_after();
