@@ -311,6 +311,25 @@ def phi_eq1(Xs: np.ndarray, act: str, tau: Optional[float] = None, mom=None, N: 
     return out
 
 
+def phi_pivot_asymmetry(Xs: np.ndarray, act: str, tau: Optional[float] = None, mom=None, N: int = 200) -> float:
+    """Diagnostic of reading R6: max_{i<j} |Φ(x_i, x_j) − Φ(x_j, x_i)|, each side by EQ1 with its first argument
+    as the Gram–Schmidt pivot.  EQ1 is not symmetric; the swap changes u_a, v_b, u_b only when
+    ‖x_i‖ ≠ ‖x_j‖, so the asymmetry vanishes for equal norms."""
+    Xs = np.asarray(Xs, dtype=np.float64)
+    if tau is None:
+        tau = tau_hat(Xs)
+    if mom is None:
+        mom = moments(act, tau, N)
+    g = Xs @ Xs.T
+    nrm2 = np.sum(Xs * Xs, axis=1)
+    I, J = np.triu_indices(len(Xs), 1)
+    if len(I) == 0:
+        return 0.0
+    fwd = eq1(mom, *gram_schmidt(nrm2[I], nrm2[J], g[I, J], I == J))
+    bwd = eq1(mom, *gram_schmidt(nrm2[J], nrm2[I], g[I, J], I == J))
+    return float(np.max(np.abs(fwd - bwd)))
+
+
 def phi_exact_pair(act, u_a: float, v_b: float, u_b: float, N: int = 120) -> float:
     """κ(x_i,x_j) = E[σ(u_a ξ_a) σ(v_b ξ_a + u_b ξ_b)] by the N×N tensor Gauss–Hermite rule
     (the quantity EQ1 approximates, Eq. (1) P:360-364 after Gram–Schmidt)."""
