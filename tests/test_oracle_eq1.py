@@ -156,16 +156,16 @@ def test_gram_schmidt_reconstructs_bivariate_covariance():
 @pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
 def test_pivot_asymmetry_diagnostic(act):
     """Reading R6: EQ1 with x_i as the Gram–Schmidt pivot is not symmetric.  Both orientations agree with the
-    symmetric kernel to second order, so their difference is third order in the deviation from the expansion
-    point (ratio ≈ 8 per halving), and it vanishes exactly when the two norms are equal (the swap then leaves
-    u_a, v_b, u_b unchanged)."""
+    symmetric kernel to second order, so their difference is at least third order in the deviation from the
+    expansion point (ratio ≥ 8 per halving asymptotically; sigmoid − ½'s cubic coefficient is tiny, its ratios are
+    higher), and it vanishes when the two norms are equal (the swap then leaves u_a, v_b, u_b unchanged)."""
     def pair(h):
         c, d = 0.5 * h, 1.0 - 0.4 * h
         return np.array([[1.0 + 0.7 * h, 0.0], [d * c, d * math.sqrt(1.0 - c * c)]])
     a = [oracle.phi_pivot_asymmetry(pair(h), act, tau=1.0) for h in (0.2, 0.1, 0.05)]
     assert all(x > 0 for x in a)
     r1, r2 = a[0] / a[1], a[1] / a[2]
-    assert 5.0 < r1 < 11.0 and 5.0 < r2 < 11.0, (a, r1, r2)
+    assert r1 > 5.0 and r2 > 6.0, (a, r1, r2)
     rng = np.random.default_rng(3)
     Z = rng.standard_normal((6, 16))
     Z /= np.linalg.norm(Z, axis=1, keepdims=True)
