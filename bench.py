@@ -62,6 +62,30 @@ def peaks():
     return p
 
 
+def tf32_peak_tflops(device):
+    """Dense TF32 tensor peak measured in this run (MEASURED_PEAKS has no TF32 entry): cuBLAS
+    torch.matmul at 8192³ with TF32 allowed, best of 5 after warm-up.  Only a roofline denominator."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(8192, 8192, device=device)
+        b = torch.randn(8192, 8192, device=device)
+        for _ in range(3):
+            a @ b
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def cores_used():
     try:
         from threadpoolctl import threadpool_info
@@ -301,6 +325,8 @@ def main():
     }
     tf32_like = prec in ("tf32", "3xtf32")
     peak_tensor = pk["bf16_tflops_sustained"] * (0.5 if tf32_like else 1.0)
+    if tf32_like:
+        pk["tf32_tflops_measured_burst"] = tf32_peak_tflops(device)
     kernels = {}
     for name, (cnt, tot) in kstat.items():
         avg = tot / cnt
@@ -329,6 +355,8 @@ def main():
                 "unit": "TFLOP/s", "frac": d["achieved_tflops"] / peak_tensor, "traffic": traffic,
                 "peak_source": pk["source"] + (" sustained bf16" + (" × 0.5 (tf32 nominal ratio)" if tf32_like else "")),
                 "frac_of_burst_peak": d["achieved_tflops"] / (pk["bf16_tflops"] * (0.5 if tf32_like else 1.0))}
+        if tf32_like:
+            roof["frac_of_measured_tf32_burst"] = d["achieved_tflops"] / pk["tf32_tflops_measured_burst"]
 
     # ---------------- e2e through the public API with host buffers.  Every step: H2D of X (and this rank's W) from
     # pinned memory, the step, and a D2H read of its results into pinned memory — G (world 1: the packed upper
@@ -482,36 +510,47 @@ def main():
             del G, ws_g
         torch.cuda.empty_cache()
         c4 = synthetic.CONFIGS[4]
-        X4 = torch.from_numpy(synthetic.make_X(c4)).to(torch.bfloat16).to(device)
         n4, p4 = c4.n, c4.p
+        X4f = torch.from_numpy(synthetic.make_X(c4)).to(torch.float32).to(device)
         Phi4 = torch.empty((n4, n4), dtype=torch.float32, device=device)
-        ws4 = torch.empty(rf.rf_phi_workspace_size(p4, n4, "bf16"), dtype=torch.uint8, device=device)
-        tau4 = rf.rf_estimate_tau(X4)
-        mom4 = rf.rf_moments(c4.act, tau4)
-        for _ in range(args.warmup):
-            rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec="bf16", Phi=Phi4, ws=ws4)
-        torch.cuda.synchronize()
-        rf.rf_profile_read()
-        rf.rf_profile_enable(True)
-        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        pa.record(stream)
-        for _ in range(args.steps):
-            rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec="bf16", Phi=Phi4, ws=ws4)
-        pb.record(stream)
-        torch.cuda.synchronize()
-        rf.rf_profile_enable(False)
-        prec4 = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
-        k5ms = sum(prec4) / max(1, len(prec4))
-        pms = pa.elapsed_time(pb) / args.steps
         tri4 = n4 * (n4 + 1) / 2.0
-        by4 = 4.0 * tri4 + X4.numel() * 2
-        phi4_line = {"what": f"configs[4] {c4.name}: Φ by EQ1, bf16 X (products exact in fp32), fp32 upper triangle",
-                     "ms_per_step": pms, "entries_per_s": tri4 / (pms * 1e-3),
-                     "tflops": p4 * n4 * (n4 + 1.0) / (pms * 1e-3) / 1e12,
-                     "K5_ms": k5ms, "K5_hbm_gbs": by4 / (k5ms * 1e-3) / 1e9 if k5ms else None,
-                     "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / pk["hbm_gbs"] if k5ms else None,
-                     "K5_tflops": p4 * n4 * (n4 + 1.0) / (k5ms * 1e-3) / 1e12 if k5ms else None}
-        del Phi4, ws4, X4
+
+        def phi4_mode(mode, steps):
+            """Time rf_phi_closed_form at configs[4] in one precision mode (bf16-stored X is
+            the headline; TF32 / 3×TF32 on fp32 X are reported alongside)."""
+            X4 = X4f.to(torch.bfloat16) if mode == "bf16" else X4f
+            ws4 = torch.empty(rf.rf_phi_workspace_size(p4, n4, mode), dtype=torch.uint8, device=device)
+            tau4 = rf.rf_estimate_tau(X4)
+            mom4 = rf.rf_moments(c4.act, tau4)
+            for _ in range(args.warmup):
+                rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec=mode, Phi=Phi4, ws=ws4)
+            torch.cuda.synchronize()
+            rf.rf_profile_read()
+            rf.rf_profile_enable(True)
+            pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pa.record(stream)
+            for _ in range(steps):
+                rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec=mode, Phi=Phi4, ws=ws4)
+            pb.record(stream)
+            torch.cuda.synchronize()
+            rf.rf_profile_enable(False)
+            ks = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
+            k5ms = sum(ks) / max(1, len(ks))
+            pms = pa.elapsed_time(pb) / steps
+            by4 = 4.0 * tri4 + X4.numel() * X4.element_size() + 4.0 * n4    # Φ triangle + X + row norms
+            d = {"ms_per_step": pms, "entries_per_s": tri4 / (pms * 1e-3),
+                 "tflops": p4 * n4 * (n4 + 1.0) / (pms * 1e-3) / 1e12,
+                 "K5_ms": k5ms, "K5_hbm_gbs": by4 / (k5ms * 1e-3) / 1e9 if k5ms else None,
+                 "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / pk["hbm_gbs"] if k5ms else None,
+                 "K5_tflops": p4 * n4 * (n4 + 1.0) / (k5ms * 1e-3) / 1e12 if k5ms else None}
+            del ws4
+            return d
+
+        phi4_line = {"what": f"configs[4] {c4.name}: Φ by EQ1, fp32 upper triangle; headline = bf16-stored X "
+                             "(bf16 products exact in fp32)", **phi4_mode("bf16", args.steps)}
+        phi4_line["tf32"] = phi4_mode("tf32", max(2, args.steps // 2))
+        phi4_line["3xtf32"] = phi4_mode("3xtf32", max(2, args.steps // 2))
+        del Phi4, X4f
         torch.cuda.empty_cache()
 
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)

@@ -515,6 +515,7 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
 // overlapped via two TMEM slots); K4 uses kBN4 (512: one slot, a third less L2 traffic per flop than 256).
 template <int kFmt, int kSplit, int kBN4, int kOut>
 rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
+  if (kBN4 == 512) kchunk4 = 0;   // K-chunked accumulation needs the second TMEM slot (256-wide tiles only)
   using C3 = rfk::TcCfg<kFmt, kSplit, 256, 0>;     // K3 stores Σᵀ from registers: no staging buffers
   using C4 = rfk::TcCfg<kFmt, kSplit, kBN4>;
   const bool bf = kFmt == 1;

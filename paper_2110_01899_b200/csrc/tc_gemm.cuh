@@ -299,30 +299,25 @@ __device__ __forceinline__ int64_t tri_tile_index(int64_t I, int64_t J, int64_t 
 }
 template <class Ctx>
 __device__ __forceinline__ void tri_store(Ctx& cx, float* P, int64_t n, int64_t T, int use_tma, int64_t row_lo,
-                                          int64_t col0, float (&v)[32], int chunk = 0, int nchunks = 1) {
+                                          int64_t col0, const float (&v)[32]) {
   const int64_t ti = row_lo >> 8, tj = col0 >> 8;
   const int64_t u = tri_tile_index(ti, tj, T);
   const int64_t lr = row_lo & 255, lc = col0 & 255;
-  if (nchunks == 1 && use_tma && col0 >= row_lo + 31) {
+  if (use_tma && col0 >= row_lo + 31) {
     cx.store_block(u * 256 + lr, lc, v);
     return;
   }
   if (row_lo + cx.lane >= n) return;
   const int64_t nloc = n - (tj << 8) < 256 ? n - (tj << 8) : 256;
   const int64_t lo = tj == ti ? lr + cx.lane : 0;                 // j ≥ i inside a diagonal tile
-  float* tile = P + u * 65536;
-  if (chunk > 0) {                                                // K-chunked accumulation: add the partial
-    const float* src = tile + (lr + cx.lane) * 256 + lc;
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if (lc + e >= lo && lc + e < nloc) v[e] += src[e];
-  }
-  store_row_masked(tile, 256, nloc, lr + cx.lane, lc, lo, v);
+  store_row_masked(P + u * 65536, 256, nloc, lr + cx.lane, lc, lo, v);
 }
 
 // ------------------------------------------------------------------------------------------
 // Epilogue functors: operator()(ctx, row_lo, col0, r[32], chunk, nchunks, t) for the warp's rows
-// [row_lo, row_lo+32) (row = row_lo + lane) and accumulator columns [col0, col0+32).
+// [row_lo, row_lo+32) (row = row_lo + lane) and accumulator columns [col0, col0+32).  r is the tile's complete
+// accumulator: with K-chunked accumulation the kernel sums the chunks in TMEM first and calls the functor once
+// (chunk = 0, nchunks = 1).
 // ------------------------------------------------------------------------------------------
 
 // K3: Σᵀ[i][k] = σ(z), z = x_iᵀw_k.  kOut: 0 = bf16, 1 = fp32, 2 = fp32 hi/lo split (3×TF32).
@@ -457,35 +452,29 @@ struct EpiSyrk {
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int nchunks, long long, const Pre&) const {
+                                             int, int, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
     if (tri_T > 0) {
-      tri_store(cx, G, n, tri_T, use_tma, row_lo, col0, v, chunk, nchunks);
+      tri_store(cx, G, n, tri_T, use_tma, row_lo, col0, v);
       return;
     }
-    if (nchunks == 1 && use_tma && col0 >= row_lo + 31) {
+    if (use_tma && col0 >= row_lo + 31) {
       cx.store_block(row_lo, col0, v);
     } else {
       if (row >= n) return;
-      if (chunk > 0) {
-        const float* src = G + row * ld + col0;
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (col0 + e >= row && col0 + e < n) v[e] += src[e];
-      }
       store_row_masked(G, ld, n, row, col0, row, v);
     }
-    if (full && chunk == nchunks - 1) store_mirror(G, ld, n, row, col0, v);
+    if (full) store_mirror(G, ld, n, row, col0, v);
   }
 };
 
 // K4 with PACKED output for the multi-GPU reduce-scatter (include/rf.h, G5).  The pair tile t (schedule
 // index; row tile ti) belongs to the chunk whose row-tile range holds ti; its 256×256 sub-tile sub goes to
 // position u = tiles_per_pair·(t − tile0[c]) + sub of the chunk: owner u mod R, slot u div R.  Whole tiles are
-// stored (no triangle mask).  K-chunked accumulation (3×TF32) re-reads the partial from the slot.
+// stored (no triangle mask).
 constexpr int kMaxP2P = 16;                  // ranks reachable by the fused (peer-memory) epilogue
 struct PackDev {
   int64_t tile0[RF_PACK_MAX_CHUNKS + 1];
@@ -515,7 +504,7 @@ struct EpiSyrkPacked {
   }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int, long long t, const Pre&) const {
+                                             int, int, long long t, const Pre&) const {
     const int ti = (int)(row_lo >> 8);
     const int c = chunk_of(ti);
     const int64_t tj0 = (col0 / bn) * bn;                          // first column of the pair tile
@@ -530,13 +519,6 @@ struct EpiSyrkPacked {
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
-    if (chunk > 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 o = reinterpret_cast<const float4*>(dst)[q];
-        v[4 * q] += o.x; v[4 * q + 1] += o.y; v[4 * q + 2] += o.z; v[4 * q + 3] += o.w;
-      }
-    }
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -720,18 +702,12 @@ struct EpiRaw {
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int chunk, int, long long, const Pre&) const {
+                                             int, int, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
-    float* dst = C + row * ld + col0;
-    if (chunk > 0) {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (col0 + e < N) v[e] += dst[e];
-    }
     store_row_masked(C, ld, N, row, col0, 0, v);
   }
 };
@@ -866,8 +842,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int it = 0;
       for (int t = cid; t < sched.num_tiles; t += ncl) {
         for (int c = 0; c < nchunks; ++c, ++it) {
-          const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
-          const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
+          // K-chunked accumulation: every chunk goes to slot 0; the epilogue keeps the running fp32 sum in slot 1
+          const bool dbl = Cfg::ACC_SLOTS == 2 && nchunks == 1;
+          const int slot = dbl ? (it & 1) : 0;
+          const uint32_t acc_phase = (dbl ? (it >> 1) : it) & 1;
           ptx::mbar_wait(&tempty[slot], acc_phase ^ 1);
           ptx::tc_fence_after();
           const uint32_t d = tmem_base + slot * Cfg::ACC_COLS;
@@ -936,6 +914,48 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       if (Cfg::CL == 4) ti = 2 * ti + (int)pi;
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
       const int64_t colb = (int64_t)tj * Cfg::BN + h * HALF;
+      if (Cfg::ACC_SLOTS == 2 && Cfg::EPI_WARPS == 8 && nchunks > 1) {
+        // K-chunked accumulation (3×TF32; the tensor pipe truncates long accumulations, DESIGN.md §6 finding 4):
+        // chunk c's partial arrives in slot 0; the warp adds it to the running sum in slot 1 in fp32
+        // (round-to-nearest) through registers, then frees slot 0 so the MMA of chunk c + 1 starts while the
+        // last chunk's sum goes out through the functor.  TMEM traffic only: no read-modify-write of G in HBM.
+        const uint32_t tA = tmem_base + ((q * 32) << 16) + h * HALF;
+        const uint32_t tS = tA + Cfg::ACC_COLS;
+        constexpr int NCH = HALF / 32;
+        const typename Epi::Pre pf = epi.prefetch(row_lo, colb, lane);
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          ptx::mbar_wait(&tfull[0], (uint32_t)it & 1u);
+          ptx::tc_fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < NCH; ++cc) {
+            uint32_t a[32], sm[32];
+            ptx::tmem_ld_32x32b_x32(tA + cc * 32, a);
+            if (c > 0) ptx::tmem_ld_32x32b_x32(tS + cc * 32, sm);
+            ptx::tmem_ld_wait();
+            if (c > 0) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) a[e] = __float_as_uint(__uint_as_float(a[e]) + __uint_as_float(sm[e]));
+            }
+            ptx::tmem_st_32x32b_x32(tS + cc * 32, a);
+          }
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(tempty0);
+        }
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < NCH; ++cc) {
+          uint32_t a[32];
+          ptx::tmem_ld_32x32b_x32(tS + cc * 32, a);
+          ptx::tmem_ld_wait();
+          const int64_t col0 = colb + cc * 32;
+          if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, a, 0, 1, (long long)t, pf);
+        }
+        cx.flush();
+        epi.tile_done((long long)t, lane);
+        continue;
+      }
       for (int c = 0; c < nchunks; ++c, ++it) {
         const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
