@@ -1139,12 +1139,14 @@ rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const floa
     const bool bf = prec == RF_PREC_BF16;
     if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
     if (!tma_out) tO = tA;
+    // 12 epilogue warps: K̃'s epilogue (a rank-8 product per entry) is latency-bound at two warps per SM
+    // sub-partition even at p = 1024 (n = 65536: 6.87 → 4.72 ms; n = 131072, p = 512: 26.7 → 18.3 ms)
     if (bf) {
-      using C = rfk::TcCfg<1, 1, 256, 2>;
+      using C = rfk::TcCfg<1, 1, 256, 2, 2, 12>;
       const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     } else {
-      using C = rfk::TcCfg<2, 1, 256, 2>;
+      using C = rfk::TcCfg<2, 1, 256, 2, 2, 12>;
       const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     }
