@@ -668,15 +668,16 @@ rf_status launch_k5(const K5Args& a) {
     if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
     if (!tma_out) tO = tA;
     // Short K (p ≤ 512): the EQ1 epilogue, latency-bound at two warps per SM sub-partition, sets the pace, and 12
-    // epilogue warps (three per TMEM lane quarter) help (configs[4]: 10.86 → 9.98 ms).  Long K: the MMA sets it
-    // and the 8-warp kernel's fifth operand stage wins (configs[3], p = 1024: 4.3 vs 5.0 ms).  DESIGN.md §7.
+    // epilogue warps (three per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages)
+    // help (configs[4]: 11.3 → 9.94 ms).  Long K: the MMA sets it and the 8-warp kernel stays ≈ 1 % ahead
+    // (configs[3] shape, p = 1024: 3.63 vs 3.67 ms).  DESIGN.md §7.
     const bool w12 = env_int("RF_K5_W12", p <= 512 ? 1 : 0) != 0;
     if (bf && w12) {
-      if ((s = k5_go<rfk::TcCfg<1, 1, 256, 2, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (bf) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (w12) {
-      if ((s = k5_go<rfk::TcCfg<2, 1, 256, 2, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      if ((s = k5_go<rfk::TcCfg<2, 1, 256, 1, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else {
       if ((s = k5_go<rfk::TcCfg<2, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     }
