@@ -667,17 +667,17 @@ rf_status launch_k5(const K5Args& a) {
     const bool bf = prec == RF_PREC_BF16;
     if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
     if (!tma_out) tO = tA;
-    // Short K (p ≤ 512): the EQ1 epilogue, latency-bound at two warps per SM sub-partition, sets the pace, and 12
-    // epilogue warps (three per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages)
-    // help (configs[4]: 11.3 → 9.94 ms).  Long K: the MMA sets it and the 8-warp kernel stays ≈ 1 % ahead
-    // (configs[3] shape, p = 1024: 3.63 vs 3.67 ms).  DESIGN.md §7.
-    const bool w12 = env_int("RF_K5_W12", p <= 512 ? 1 : 0) != 0;
+    // Short K (p ≤ 512): the EQ1 epilogue, latency-bound at two warps per SM sub-partition, sets the pace, and 16
+    // epilogue warps (four per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages;
+    // 96 registers) help: configs[4] 11.3 → 9.54 ms (12 warps: 9.94).  Long K: the MMA sets it and the 8-warp
+    // kernel stays ahead (configs[3] shape, p = 1024: 3.63 vs 3.78 ms).  DESIGN.md §7.
+    const bool w12 = env_int("RF_K5_WIDE", p <= 512 ? 1 : 0) != 0;
     if (bf && w12) {
-      if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (bf) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (w12) {
-      if ((s = k5_go<rfk::TcCfg<2, 1, 256, 1, 2, 12>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      if ((s = k5_go<rfk::TcCfg<2, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else {
       if ((s = k5_go<rfk::TcCfg<2, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     }
@@ -1140,14 +1140,15 @@ rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const floa
     const bool bf = prec == RF_PREC_BF16;
     if ((s = make_tmap(&tA, X, bf, n, p, ldx, 128))) return s;
     if (!tma_out) tO = tA;
-    // 12 epilogue warps: K̃'s epilogue (a rank-8 product per entry) is latency-bound at two warps per SM
-    // sub-partition even at p = 1024 (n = 65536: 6.87 → 4.72 ms; n = 131072, p = 512: 26.7 → 18.3 ms)
+    // 16 epilogue warps: K̃'s epilogue (a rank-8 product per entry) is latency-bound at two warps per SM
+    // sub-partition even at p = 1024 (n = 65536: 8 / 12 / 16 warps 6.87 / 4.72 / 4.22 ms; n = 131072, p = 512:
+    // 26.7 / 18.2 / 15.5 ms)
     if (bf) {
-      using C = rfk::TcCfg<1, 1, 256, 2, 2, 12>;
+      using C = rfk::TcCfg<1, 1, 256, 1, 2, 16>;
       const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     } else {
-      using C = rfk::TcCfg<2, 1, 256, 2, 2, 12>;
+      using C = rfk::TcCfg<2, 1, 256, 1, 2, 16>;
       const rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     }

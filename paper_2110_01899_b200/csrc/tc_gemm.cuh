@@ -56,10 +56,10 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + NSUB * B_BYTES);
   static constexpr int ACC_COLS = kBN;
   static constexpr int ACC_SLOTS = 512 / kBN;
-  // 8 epilogue warps (two per TMEM lane quarter, each owning half of the accumulator columns), or 12 (three per
-  // quarter, 32-column chunks dealt round-robin; unpipelined TMEM loads to fit 128 registers per thread)
+  // 8 epilogue warps (two per TMEM lane quarter, each owning half of the accumulator columns), or 12 / 16 (three /
+  // four per quarter, 32-column chunks dealt round-robin; unpipelined TMEM loads to fit 128 / 96 registers)
   static constexpr int EPI_WARPS = kEpiW;
-  static_assert(kEpiW == 8 || kEpiW == 12, "8 or 12 epilogue warps");
+  static_assert(kEpiW == 8 || kEpiW == 12 || kEpiW == 16, "8, 12 or 16 epilogue warps");
   static constexpr int THREADS = 128 + 32 * kEpiW;
   static constexpr int STG_BUFS = kStg >= 0 ? kStg : ((kSplit == 3 || kBN == 512) ? 1 : 2);   // per epi warp
   static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
@@ -960,8 +960,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         const int slot = Cfg::ACC_SLOTS == 2 ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_SLOTS == 2 ? (it >> 1) : it) & 1;
         const uint32_t tbase = tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS + h * HALF;
-        if constexpr (Cfg::EPI_WARPS == 12) {
-          // three warps per lane quarter: 32-column chunks cc ≡ h (mod 3) of the accumulator row
+        if constexpr (Cfg::EPI_WARPS != 8) {
+          // three (four) warps per lane quarter: 32-column chunks cc ≡ h (mod 3 (4)) of the accumulator row
           const int64_t col_t = (int64_t)tj * Cfg::BN;
           const uint32_t tb = tmem_base + ((q * 32) << 16) + slot * Cfg::ACC_COLS;
           const typename Epi::Pre pf = epi.prefetch(row_lo, col_t, lane);
