@@ -152,6 +152,19 @@ __device__ __forceinline__ void eq1_pair(float g0, float g1, float nj0, float nj
   up2(o, out0, out1);
 }
 
+// Odd σ, off the diagonal, with the row constants folded: Φ = ν·A1·(f0 + f1·s) = g·(P + Q·s), P = c·A1·f0,
+// Q = c·A1·f1 (ν = g·c); one packed multiply fewer per pair than eq1_pair<true>.
+__device__ __forceinline__ void eq1_pair_odd(float g0, float g1, float nj0, float nj1, uint64_t c2, uint64_t p2,
+                                             uint64_t q2, float& out0, float& out1) {
+  const uint64_t g = pk2(g0, g1);
+  const uint64_t nu = mul2(g, c2);
+  const uint64_t r = sub2(pk2(nj0, nj1), mul2(nu, nu));
+  float r0, r1;
+  up2(r, r0, r1);
+  const uint64_t s = pk2(sqrt_fast(fmaxf(r0, 0.f)), sqrt_fast(fmaxf(r1, 0.f)));
+  up2(mul2(g, fma2(s, q2, p2)), out0, out1);
+}
+
 template <typename T>
 __device__ __forceinline__ T eq1_entry(T g, T a0, T a1, T a2h, T c, T njt, bool diag, T nu_diag, T e0, T e1, T e2,
                                        T f0, T f1) {

@@ -581,6 +581,12 @@ struct EpiEq1 {
       for (int e = 0; e < 32; ++e)
         v[e] = eq1_entry<float>(__uint_as_float(r[e]), c.a0, c.a1, c.a2h, c.c, nj[e], col0 + e == row, c.nu_diag, e0,
                                 e1, e2, f0, f1);
+    } else if (kOdd) {
+      const float P = c.c * c.a1 * f0, Q = c.c * c.a1 * f1;
+      const uint64_t c2 = pk2(c.c, c.c), p2 = pk2(P, P), q2 = pk2(Q, Q);
+#pragma unroll
+      for (int e = 0; e < 32; e += 2)
+        eq1_pair_odd(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, p2, q2, v[e], v[e + 1]);
     } else {
       const uint64_t c2 = pk2(c.c, c.c), a0_2 = pk2(c.a0, c.a0), a1_2 = pk2(c.a1, c.a1), a2h_2 = pk2(c.a2h, c.a2h);
       const uint64_t e0_2 = pk2(e0, e0), e1_2 = pk2(e1, e1), e2_2 = pk2(e2, e2), f0_2 = pk2(f0, f0), f1_2 = pk2(f1, f1);
