@@ -556,8 +556,19 @@ def main():
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # a probe at |S| = 1024, then |S| sized for ≈ 10–30 s of CPU work (time ~ |S|^1.5 between the linear
+        # σ(WX) part and the quadratic G_SS part), capped by host memory (≈ 3 fp64 |S| × m arrays)
         size = 1024
         t, f = oracle_sample(cfg, size)
+        try:
+            import psutil
+            mem_cap = int(psutil.virtual_memory().available * 0.5 / (3 * 8 * max(m, 1)))
+        except Exception:
+            mem_cap = 4096
+        target = min(8192, mem_cap, int(size * (15.0 / max(t, 1e-3)) ** (1 / 1.5)))
+        if target > size:
+            size = target // 256 * 256
+            t, f = oracle_sample(cfg, size, seed=1)
         cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
                "sample": f"|S|={size} random rows of configs[{args.config}]: G_SS (σ(W x_i) over all m={m}) + "
                          f"Φ_SS by the 18-term EQ1, fp64 NumPy, {t:.1f} s"}

@@ -1,5 +1,6 @@
-# Round evidence on one B200: tests, smoke, bench line, reference arm, launch list, ncu --set full of K4 (both
-# kernels of the hybrid launch) and K5 from bench.py.
+# Round evidence on one B200 (call 1 of 2): tests, smoke, bench line, reference arm, then the launch list of the
+# bench command under ncu (gpu__time_duration + DRAM bytes per launch) after the same command exited 0 without ncu.
+# Call 2 (scripts/gpu_k5ncu4.sh / a K4 capture) takes the one `ncu --set full` capture.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
@@ -10,6 +11,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-trf --no-phi4"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 13 -c 2 -o gpurun_out/k4_bench_full $B > gpurun_out/ncu_k4.log 2>&1
-tail -2 gpurun_out/ncu_k4.log
 ls -la gpurun_out
