@@ -270,3 +270,25 @@ def test_config3_full_size_bf16():
 @pytest.mark.parametrize("prec", ["bf16", "3xtf32"])
 def test_config4_full_size_phi(prec):
     _sampled_phi(4, prec, count=1024, stride=1024)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+@pytest.mark.parametrize("out", ["upper", "full", "packed_tri"])
+def test_phi_wide_epilogue_bit_exact(prec, out, monkeypatch):
+    """K5's 16-warp epilogue (p ≤ 512: four warps per TMEM lane quarter, chunks dealt round-robin) computes every
+    entry with the same arithmetic as the 8-warp kernel: the two agree bit for bit, in every output layout."""
+    X = synthetic.make_X(4, n=1100, p=200)
+    Xd = dev(X, prec)
+    res = []
+    for wide in ("1", "0"):
+        monkeypatch.setenv("RF_K5_WIDE", wide)
+        P = rf.rf_phi_closed_form(Xd, act="tanh", prec=prec, out=out)
+        torch.cuda.synchronize()
+        res.append(P.cpu().numpy())
+    if out == "packed_tri":
+        from paper_2110_01899_b200 import layout
+        res = [layout.unpack_tri(r, X.shape[0]) for r in res]
+        I, J = upper_idx(X.shape[0])
+        assert np.array_equal(res[0][I, J], res[1][I, J])
+    else:
+        assert np.array_equal(res[0], res[1])
