@@ -5,6 +5,8 @@
 // Nodes/weights by Golub–Welsch: the probabilists' Hermite Jacobi matrix (zero diagonal, off-diagonal
 // √k) is diagonalised by implicit-shift QL; nodes = eigenvalues, weights = squared first components of
 // the normalised eigenvectors (they sum to 1 for the N(0,1) density).
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -65,7 +67,7 @@ static bool tridiag_ql_first_row(std::vector<double>& d, std::vector<double>& e,
   return true;
 }
 
-bool gauss_hermite(int N, std::vector<double>& x, std::vector<double>& w) {
+static bool gauss_hermite_compute(int N, std::vector<double>& x, std::vector<double>& w) {
   std::vector<double> d(N, 0.0), e(N, 0.0), z(N, 0.0);
   for (int k = 0; k < N - 1; ++k) e[k] = std::sqrt((double)(k + 1));
   z[0] = 1.0;
@@ -88,6 +90,31 @@ bool gauss_hermite(int N, std::vector<double>& x, std::vector<double>& w) {
   }
   if (N & 1) x[N / 2] = 0.0;
   return true;
+}
+
+// The rules depend on N only: computed once per N (Golub–Welsch at N = 512 costs ≈ 10 ms) and cached.
+static bool cached_rule(std::map<int, std::pair<std::vector<double>, std::vector<double>>>& cache, std::mutex& mu,
+                        bool (*compute)(int, std::vector<double>&, std::vector<double>&), int N,
+                        std::vector<double>& x, std::vector<double>& w) {
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(N);
+    if (it != cache.end()) {
+      x = it->second.first;
+      w = it->second.second;
+      return true;
+    }
+  }
+  if (!compute(N, x, w)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(N, std::make_pair(x, w));
+  return true;
+}
+
+bool gauss_hermite(int N, std::vector<double>& x, std::vector<double>& w) {
+  static std::map<int, std::pair<std::vector<double>, std::vector<double>>> cache;
+  static std::mutex mu;
+  return cached_rule(cache, mu, gauss_hermite_compute, N, x, w);
 }
 
 // σ, σ', σ'' of the north-star activations (analytic; sigmoid − ½ = ½ tanh(t/2)).
@@ -176,7 +203,7 @@ static inline double act_value(rf_act act, double t) {
 }
 
 // Gauss–Legendre on [−1, 1] by Golub–Welsch (Jacobi matrix: zero diagonal, b_k = k/√(4k² − 1)); weights sum to 2.
-static bool gauss_legendre(int N, std::vector<double>& x, std::vector<double>& w) {
+static bool gauss_legendre_compute(int N, std::vector<double>& x, std::vector<double>& w) {
   std::vector<double> d(N, 0.0), e(N, 0.0), z(N, 0.0);
   for (int k = 1; k < N; ++k) e[k - 1] = k / std::sqrt(4.0 * k * k - 1.0);
   z[0] = 1.0;
@@ -185,6 +212,12 @@ static bool gauss_legendre(int N, std::vector<double>& x, std::vector<double>& w
   w.resize(N);
   for (int i = 0; i < N; ++i) w[i] = 2.0 * z[i] * z[i];
   return true;
+}
+
+static bool gauss_legendre(int N, std::vector<double>& x, std::vector<double>& w) {
+  static std::map<int, std::pair<std::vector<double>, std::vector<double>>> cache;
+  static std::mutex mu;
+  return cached_rule(cache, mu, gauss_legendre_compute, N, x, w);
 }
 
 // M_j = E[ξ^j σ(√τξ)], j = 0..6, and E[σ(√τξ)²]: composite Gauss–Legendre on [−L, 0] and [0, L] (the only kink /
