@@ -287,7 +287,7 @@ rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b
 template <typename T, class Epi>
 rf_status launch_simt(const char* name, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N,
                       int64_t K, int tri, int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st) {
-  const int tn = (int)((N + 63) / 64);
+  const int tn = (int)((N + rfk::kSimtTile - 1) / rfk::kSimtTile);
   if (row_tile1 <= row_tile0 || tn == 0) return RF_OK;
   ProfScope ps(name, st);
   dim3 grid(tn, row_tile1 - row_tile0);
@@ -922,19 +922,19 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
       double* S = (double*)(w + pl.off_s0);
       rfk::SimtSigma<double> e1{S, pl.ldS, n, m_local, (int)act};
       if ((s = launch_simt<double>("K6_simt_gemm_sigma", (const double*)X, ldx, (const double*)W, ldw, n, m_local, p, 0, 0,
-                                   (int)((n + 63) / 64), e1, st)))
+                                   (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e1, st)))
         return s;
       rfk::SimtSyrk<double> e2{(double*)G, ldg, n, 1.0 / (double)m_total, full};
-      if ((s = launch_simt<double>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+      if ((s = launch_simt<double>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e2, st)))
         return s;
     } else {
       float* S = (float*)(w + pl.off_s0);
       rfk::SimtSigma<float> e1{S, pl.ldS, n, m_local, (int)act};
       if ((s = launch_simt<float>("K6_simt_gemm_sigma", (const float*)X, ldx, (const float*)W, ldw, n, m_local, p, 0, 0,
-                                  (int)((n + 63) / 64), e1, st)))
+                                  (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e1, st)))
         return s;
       rfk::SimtSyrk<float> e2{(float*)G, ldg, n, (float)(1.0 / (double)m_total), full};
-      if ((s = launch_simt<float>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + 63) / 64), e2, st)))
+      if ((s = launch_simt<float>("K6_simt_syrk", S, pl.ldS, S, pl.ldS, n, n, m_local, 1, 0, (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e2, st)))
         return s;
     }
     return ok();
@@ -1725,8 +1725,8 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
     RF_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     rfk::SimtEq1<double, rfk::RowCoefD> e{(double*)Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full};
-    return (s = launch_simt<double>("K6_simt_xtx_eq1", (const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
-                                    (int)((row_end + 63) / 64), e, st))
+    return (s = launch_simt<double>("K6_simt_xtx_eq1", (const double*)X, ldx, (const double*)X, ldx, n, n, p, 1, (int)(row_begin / rfk::kSimtTile),
+                                    (int)((row_end + rfk::kSimtTile - 1) / rfk::kSimtTile), e, st))
                ? s
                : ok();
   }
@@ -1742,8 +1742,8 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   if (prec == RF_PREC_FP32) {
     rfk::SimtEq1<float, rfk::RowCoef> e{(float*)Phi, ldphi, n, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
                                         (float)f1, full};
-    return (s = launch_simt<float>("K6_simt_xtx_eq1", (const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / 64),
-                                   (int)((row_end + 63) / 64), e, st))
+    return (s = launch_simt<float>("K6_simt_xtx_eq1", (const float*)X, ldx, (const float*)X, ldx, n, n, p, 1, (int)(row_begin / rfk::kSimtTile),
+                                   (int)((row_end + rfk::kSimtTile - 1) / rfk::kSimtTile), e, st))
                ? s
                : ok();
   }

@@ -1,8 +1,10 @@
 // K6: SIMT (CUDA-core) versions of K3/K4/K5 for the fp32-accurate FP32 mode (FFMA) and the FP64
-// mode (DFMA).  C[i][j] = Σ_k A[i][k]·B[j][k] over 64×64 tiles, 256 threads, 4×4 register micro-tile,
-// operands staged transposed in shared memory; the same fused epilogues as the tensor-core path.
+// mode (DFMA).  C[i][j] = Σ_k A[i][k]·B[j][k] over 128×128 tiles, 256 threads, 8×8 register micro-tile,
+// operands staged k-major in shared memory; the same fused epilogues as the tensor-core path.
 #pragma once
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "rf_common.cuh"
 
@@ -50,55 +52,103 @@ struct SimtEq1 {
   }
 };
 
-// grid: (tiles_n, row tiles in [row_tile0, row_tile0 + gridDim.y)); tri ⇒ skip tiles strictly below
-// the diagonal (64×64 tiles: J < I).
+// grid: (tiles_n, row tiles in [row_tile0, row_tile0 + gridDim.y)); tri ⇒ skip tiles strictly below the diagonal
+// (J < I).  128×128 tiles, 256 threads, 8×8 register micro-tile per thread (rows ty·4 + {0..3} and 64 + ty·4 +
+// {0..3}, columns likewise with tx), K-slices of 16 staged k-major in shared memory (two 16-B loads per operand per
+// k give 64 FMAs), next slice prefetched into registers with 16-B global loads while the current one is consumed.
+// Rows are 16-B aligned (ld·sizeof(T) a multiple of 16 B, validated at the ABI); the K tail is zero-filled.
+constexpr int kSimtTile = 128;
 template <typename T, class Epi>
 __global__ void __launch_bounds__(256) simt_gemm_nt(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
                                                     int64_t ldb, int64_t M, int64_t N, int64_t K, int tri,
                                                     int row_tile0, Epi epi) {
-  constexpr int BM = 64, BN = 64, BK = 16;
+  constexpr int BM = kSimtTile, BN = kSimtTile, BK = 16, PAD = 4;
+  constexpr int VEC = 16 / (int)sizeof(T);                 // elements per 16-B vector
+  constexpr int NV = BM * BK / VEC / 256;                  // vectors per thread per operand per slice
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   const int bi = blockIdx.y + row_tile0, bj = blockIdx.x;
   if (tri && bj < bi) return;
-  __shared__ T As[BK][BM + 1];
-  __shared__ T Bs[BK][BN + 1];
+  __shared__ __align__(16) T As[BK][BM + PAD];
+  __shared__ __align__(16) T Bs[BK][BN + PAD];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int64_t i0 = (int64_t)bi * BM, j0 = (int64_t)bj * BN;
-  T acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
 
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+  T ra[NV][VEC], rb[NV][VEC];
+  auto gload = [&](int64_t k0) __attribute__((always_inline)) {
 #pragma unroll
-    for (int q = 0; q < (BM * BK) / 256; ++q) {
-      const int e = tid + 256 * q;
-      const int r = e / BK, kk = e % BK;
-      const int64_t gi = i0 + r, gj = j0 + r, gk = k0 + kk;
-      As[kk][r] = (gi < M && gk < K) ? A[gi * lda + gk] : T(0);
-      Bs[kk][r] = (gj < N && gk < K) ? B[gj * ldb + gk] : T(0);
+    for (int q = 0; q < NV; ++q) {
+      const int idx = tid + 256 * q;
+      const int r = idx / (BK / VEC), c = (idx % (BK / VEC)) * VEC;
+      const int64_t k = k0 + c;
+      const int64_t gi = i0 + r, gj = j0 + r;
+      if (gi < M && k + VEC <= K) {
+        const V v = *reinterpret_cast<const V*>(A + gi * lda + k);
+        const T* pv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) ra[q][e] = pv[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) ra[q][e] = (gi < M && k + e < K) ? A[gi * lda + k + e] : T(0);
+      }
+      if (gj < N && k + VEC <= K) {
+        const V v = *reinterpret_cast<const V*>(B + gj * ldb + k);
+        const T* pv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) rb[q][e] = pv[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) rb[q][e] = (gj < N && k + e < K) ? B[gj * ldb + k + e] : T(0);
+      }
     }
+  };
+  auto sstore = [&]() __attribute__((always_inline)) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int idx = tid + 256 * q;
+      const int r = idx / (BK / VEC), c = (idx % (BK / VEC)) * VEC;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        As[c + e][r] = ra[q][e];
+        Bs[c + e][r] = rb[q][e];
+      }
+    }
+  };
+
+  T acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = T(0);
+
+  gload(0);
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();                       // the previous slice has been consumed
+    sstore();
     __syncthreads();
+    if (k0 + BK < K) gload(k0 + BK);      // in flight while this slice is consumed
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      T a[4], b[4];
+      T a[8], b[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = As[kk][ty + 16 * u];
-        b[u] = Bs[kk][tx + 16 * u];
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          a[4 * h + e] = As[kk][64 * h + 4 * ty + e];
+          b[4 * h + e] = Bs[kk][64 * h + 4 * tx + e];
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
-    __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) epi(i0 + ty + 16 * u, j0 + tx + 16 * v, acc[u][v]);
+    for (int v = 0; v < 8; ++v)
+      epi(i0 + 64 * (u >> 2) + 4 * ty + (u & 3), j0 + 64 * (v >> 2) + 4 * tx + (v & 3), acc[u][v]);
 }
 
 }  // namespace rfk
