@@ -59,7 +59,7 @@ struct SimtEq1 {
 // Rows are 16-B aligned (ld·sizeof(T) a multiple of 16 B, validated at the ABI); the K tail is zero-filled.
 constexpr int kSimtTile = 128;
 template <typename T, class Epi>
-__global__ void __launch_bounds__(256) simt_gemm_nt(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) simt_gemm_nt(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
                                                     int64_t ldb, int64_t M, int64_t N, int64_t K, int tri,
                                                     int row_tile0, Epi epi) {
   constexpr int BM = kSimtTile, BN = kSimtTile, BK = 16, PAD = 4;
@@ -115,11 +115,18 @@ __global__ void __launch_bounds__(256) simt_gemm_nt(const T* __restrict__ A, int
     }
   };
 
+  // fp32: the accumulators are packed pairs (FFMA2, two FMAs per instruction, each rounded as the scalar op)
+  constexpr bool kPk = sizeof(T) == 4;
   T acc[8][8];
+  uint64_t acc2[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = T(0);
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc2[a][b] = 0ull;
 
   gload(0);
   for (int64_t k0 = 0; k0 < K; k0 += BK) {
@@ -138,11 +145,34 @@ __global__ void __launch_bounds__(256) simt_gemm_nt(const T* __restrict__ A, int
           b[4 * h + e] = Bs[kk][64 * h + 4 * tx + e];
         }
       }
+      if constexpr (kPk) {
+        uint64_t b2[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+        for (int w = 0; w < 4; ++w) b2[w] = pk2((float)b[2 * w], (float)b[2 * w + 1]);
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t a2 = pk2((float)a[u], (float)a[u]);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc2[u][w] = fma2(a2, b2[w], acc2[u][w]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int v = 0; v < 8; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      }
     }
+  }
+  if constexpr (kPk) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        float lo, hi;
+        up2(acc2[u][w], lo, hi);
+        acc[u][2 * w] = (T)lo;
+        acc[u][2 * w + 1] = (T)hi;
+      }
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
