@@ -478,7 +478,9 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
   rf_status s;
   RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
   rfk::Sched sm = rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
-  rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, raster_gm(8, 4));
+  // tail raster: with 8 pair clusters in flight, groups of 4 row tiles × 2 column tiles re-read the fewest Σᵀ panels
+  // (4·32 + 2·64 MB per 8 tiles vs 8·32 + 64 for groups of 8); measured ≈ 0.8 % on the whole K4 (scripts/gpu_tailgm.sh)
+  rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, env_int("RF_TAIL_GM", 4));
   if (lockw > 0) {
     sm.prog = prog;
     sp.prog = prog + 128;
