@@ -162,6 +162,7 @@ class GramFusedP2P:
         import torch
         import torch.distributed as dist
         from . import rf_gram_packed_p2p, rf_pack_reduce
+        torch.cuda.current_stream().synchronize()   # my previous rf_pack_reduce has finished reading staging
         dist.barrier(group=self.group)          # every owner has finished reading its staging buffer
         rf_gram_packed_p2p(X, W, self.plan, self.rank, self.ptrs, act=self.act, prec=self.prec,
                            m_total=self.m_total, max_sms=self.max_sms, ws=self.ws)
