@@ -220,17 +220,30 @@ def _sampled_gram(cfg_idx, prec, count, stride):
     assert r <= TOL[prec]
 
 
-def _sampled_phi(cfg_idx, prec, count, stride):
+def _sampled_phi(cfg_idx, prec, count, stride, packed=False):
     cfg = synthetic.CONFIGS[cfg_idx]
     X = synthetic.make_X(cfg)
     Xd = dev(X, prec)
     tau_ref = oracle.tau_hat(back(Xd))
-    Phi = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="upper")
-    torch.cuda.synchronize()
     S = synthetic.sample_indices(cfg.n, count=count, tile_stride=stride)
     St = torch.tensor(S, device="cuda")
-    sub = back(Phi.index_select(0, St).index_select(1, St))
-    del Phi
+    if packed:
+        # RF_OUT_PACKED_TRI (the e2e read-back layout): gather the sampled upper-triangle entries on the device by
+        # the include/rf.h offsets, tile (I, J) at 65536·(I·T − I(I−1)/2 + J − I), row-major inside
+        P = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="packed_tri")
+        torch.cuda.synchronize()
+        T = -(-cfg.n // 256)
+        ii, jj = np.meshgrid(S, S, indexing="ij")
+        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+        It, Jt = lo // 256, hi // 256
+        off = 65536 * (It * T - It * (It - 1) // 2 + Jt - It) + (lo % 256) * 256 + (hi % 256)
+        sub = back(P[torch.tensor(off.ravel(), device="cuda")]).reshape(len(S), len(S))
+        del P
+    else:
+        Phi = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="upper")
+        torch.cuda.synchronize()
+        sub = back(Phi.index_select(0, St).index_select(1, St))
+        del Phi
     ref = oracle.phi_eq1(back(Xd.index_select(0, St)), cfg.act, tau_ref)
     I, J = upper_idx(len(S))
     tol = {"fp32": 1e-5, "3xtf32": 1e-5, "tf32": 2e-3, "bf16": 1e-5}[prec]
@@ -265,6 +278,12 @@ def test_config2_full_size_bf16():
 
 def test_config3_full_size_bf16():
     _sampled_gram(3, "bf16", count=256, stride=2048)
+    _sampled_phi(3, "bf16", count=768, stride=2048)    # the bench step's Φ on the same X
+
+
+def test_config4_full_size_phi_packed_tri():
+    """configs[4] Φ in the packed upper-triangle layout (16-warp K5, tile-remapped TMA stores), sampled."""
+    _sampled_phi(4, "bf16", count=1024, stride=1024, packed=True)
 
 
 @pytest.mark.parametrize("prec", ["bf16", "3xtf32"])
