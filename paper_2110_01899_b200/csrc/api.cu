@@ -673,12 +673,12 @@ rf_status launch_k5(const K5Args& a) {
     // epilogue warps (four per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages;
     // 96 registers) help: configs[4] 11.3 → 9.54 ms (12 warps: 9.94).  Long K: the MMA sets it and the 8-warp
     // kernel stays ahead (configs[3] shape, p = 1024: 3.63 vs 3.78 ms).  DESIGN.md §7.
-    const bool w12 = env_int("RF_K5_WIDE", p <= 512 ? 1 : 0) != 0;
-    if (bf && w12) {
+    const bool wide = env_int("RF_K5_WIDE", p <= 512 ? 1 : 0) != 0;
+    if (bf && wide) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (bf) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
-    } else if (w12) {
+    } else if (wide) {
       if ((s = k5_go<rfk::TcCfg<2, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else {
       if ((s = k5_go<rfk::TcCfg<2, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
