@@ -137,7 +137,8 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
  *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode).
  * Pipeline: [3XTF32: K2 split X, W] → K3 fused Σᵀ = σ(X·Wᵀ) (tcgen05 GEMM, σ in the epilogue)
  *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 256×512 CTA-pair tiles with j ≥ i (3XTF32:
- *           256×256 tiles, K cut into fp32-summed chunks of 256 to bound tensor-pipe accumulation error).
+ *           256×256 tiles, K cut into chunks of 128 features whose partial sums are added in fp32, in TMEM, to
+ *           bound the tensor pipe's truncating accumulation).
  * Alignment: X, W 16-B aligned with ldx·esize, ldw·esize multiples of 16 B (TMA); G aligned to its element
  *            size, any ldg ≥ n (16-B vector stores are used where rows allow); ws 256-B aligned.
  */
