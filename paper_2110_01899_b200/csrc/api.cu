@@ -429,36 +429,73 @@ static cudaStream_t side_stream() {
   return (dev >= 0 && dev < 64) ? s[dev] : nullptr;
 }
 
+// How many 4-CTA clusters of kernel <Cm, Epi> can be co-resident (clusters must sit inside one GPC).
+template <class Cm, class Epi>
+rf_status max_clusters4(int sms, int* mcl) {
+  *mcl = 0;
+  auto kern = rfk::tc_gemm_kernel<Cm, Epi>;
+  RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cm::SMEM_BYTES));
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(Cm::THREADS);
+  cfg.dynamicSmemBytes = Cm::SMEM_BYTES;
+  cfg.gridDim = dim3(sms);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(mcl, kern, &cfg) != cudaSuccess) *mcl = 0;
+  cudaGetLastError();
+  return RF_OK;
+}
+
+// Launch the multicast kernel <Cm> (schedule sm, 4·mcl SMs) on st and, concurrently on the side stream, the pair
+// kernel <Cp> (schedule sp, tail_sms SMs) once the multicast kernel has started (sm.started = flag, zeroed by
+// the caller on st before this call).  One trace record `name` brackets both (fork → join); the parts are traced
+// as `name`_mc / `name`_tail.  tBm / tBp: the B-operand "lo" maps of the two kernels (the multicast kernel of
+// 256-wide tiles reads B through a 64-row box).
+template <class Cm, class Cp, class Epi>
+rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tBm,
+                             const CUtensorMap& tBp, const CUtensorMap& tO, const rfk::Sched& sm, const rfk::Sched& sp,
+                             const Epi& e, uint32_t* flag, int mc_sms, int tail_sms, cudaStream_t st) {
+  PFN_wait32h wfn = wait32_h();
+  cudaStream_t st2 = side_stream();
+  rf_status s;
+  ProfScope whole(name, st);
+  char nm_mc[32], nm_tail[32];
+  std::snprintf(nm_mc, sizeof(nm_mc), "%s_mc", name);
+  std::snprintf(nm_tail, sizeof(nm_tail), "%s_tail", name);
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // inputs ready and the progress words / start flag zeroed
+  if ((s = launch_tc<Cm>(nm_mc, tA, tB, tA, tBm, tO, sm, e, mc_sms, st))) return s;
+  // the pair kernel: on the side stream, after ev0 and once the multicast kernel has started
+  RF_CUDA_CHECK(cudaStreamWaitEvent(st2, ev0, 0));
+  CUresult r = wfn((CUstream)st2, (CUdeviceptr)(uintptr_t)flag, 1u, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(RF_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  s = launch_tc<Cp>(nm_tail, tA, tB, tA, tBp, tO, sp, e, tail_sms, st2);
+  RF_CUDA_CHECK(cudaEventRecord(ev1, st2));
+  RF_CUDA_CHECK(cudaStreamWaitEvent(st, ev1, 0));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  return s;
+}
+
 template <int kFmt, class Epi>
 rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtensorMap& tO, int64_t n, int kb,
                            const Epi& e, uint32_t* prog, int lockw, int lockks, int sms, cudaStream_t st,
                            bool* used) {
   *used = false;
   const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512);
-  PFN_wait32h wfn = wait32_h();
-  cudaStream_t st2 = side_stream();
-  if (env_int("RF_K4_HYBRID", 1) == 0 || T < 64 || !wfn || !st2) return RF_OK;
+  if (env_int("RF_K4_HYBRID", 1) == 0 || T < 64 || !wait32_h() || !side_stream()) return RF_OK;
   using Cm = rfk::TcCfg<kFmt, 1, 512, -1, 4>;
   using Cp = rfk::TcCfg<kFmt, 1, 512>;
-  // how many 4-CTA clusters fit (GPC packing), and the SMs that leaves for pairs
   int mcl = 0;
-  {
-    auto kern = rfk::tc_gemm_kernel<Cm, Epi>;
-    RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cm::SMEM_BYTES));
-    cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(Cm::THREADS);
-    cfg.dynamicSmemBytes = Cm::SMEM_BYTES;
-    cfg.gridDim = dim3(sms);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 4;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&mcl, kern, &cfg) != cudaSuccess) mcl = 0;
-    cudaGetLastError();
-  }
+  rf_status s;
+  if ((s = max_clusters4<Cm, Epi>(sms, &mcl))) return s;
   const int left = sms - 4 * mcl;
   if (mcl <= 0 || left < 2) return RF_OK;
   // work share of the multicast kernel from the per-SM rate ratio r (measured ≈ 1.11: less L2 traffic per flop
@@ -475,7 +512,6 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
     ++S1;
   }
   if (2 * S1 >= T) return RF_OK;
-  rf_status s;
   RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
   rfk::Sched sm = rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
   // tail raster: with 8 pair clusters in flight, groups of 4 row tiles × 2 column tiles re-read the fewest Σᵀ panels
@@ -488,27 +524,38 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
     sm.lock_ks = sp.lock_ks = lockks;
   }
   sm.started = prog + 255;
-  // one trace record `name` brackets both kernels on the caller's stream (fork → join); the parts are traced
-  // as `name`_mc / `name`_tail
-  ProfScope whole(name, st);
-  char nm_mc[32], nm_tail[32];
-  std::snprintf(nm_mc, sizeof(nm_mc), "%s_mc", name);
-  std::snprintf(nm_tail, sizeof(nm_tail), "%s_tail", name);
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
-  RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // Σ ready (K3) and the progress words / start flag zeroed
-  if ((s = launch_tc<Cm>(nm_mc, tS, tS, tS, tS, tO, sm, e, sms, st))) return s;
-  // the pair kernel: on the side stream, after K3 + the memset (ev0) and once the multicast kernel has started
-  RF_CUDA_CHECK(cudaStreamWaitEvent(st2, ev0, 0));
-  CUresult r = wfn((CUstream)st2, (CUdeviceptr)(uintptr_t)(prog + 255), 1u, CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) return fail(RF_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-  s = launch_tc<Cp>(nm_tail, tS, tS, tS, tS, tO, sp, e, left & ~1, st2);
-  RF_CUDA_CHECK(cudaEventRecord(ev1, st2));
-  RF_CUDA_CHECK(cudaStreamWaitEvent(st, ev1, 0));
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
-  if (s) return s;
+  if ((s = launch_hybrid_pair<Cm, Cp>(name, tS, tS, tS, tS, tO, sm, sp, e, prog + 255, sms, left & ~1, st))) return s;
+  *used = true;
+  return RF_OK;
+}
+
+// Hybrid K3 (bf16 / tf32 GEMM + σ, 256×256 pair tiles, rectangular): 4-CTA clusters that share each B tile (two
+// 64-row halves, one loaded by each pair and multicast to both) on the first super rows, pair clusters on the
+// rest on the SMs the GPC packing leaves.  K3 is L2 → SM bandwidth bound with 256-wide tiles (64 B per SM-clock at
+// full rate against the ≈ 6.3 KB/clk chip limit); the multicast cuts that to 48 B (configs[3]: 9.57 → 7.97 ms on
+// 132 SMs alone).
+template <class Cm, class Cp, class Epi>
+rf_status launch_k3_hybrid(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tBh, int64_t n,
+                           int64_t m, int kb, const Epi& e, uint32_t* prog, int sms, cudaStream_t st, bool* used) {
+  *used = false;
+  const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512), tn = (int)((m + 255) / 256);
+  if (env_int("RF_K3_HYBRID", 1) == 0 || T < 32 || !wait32_h() || !side_stream()) return RF_OK;
+  int mcl = 0;
+  rf_status s;
+  if ((s = max_clusters4<Cm, Epi>(sms, &mcl))) return s;
+  const int left = sms - 4 * mcl;
+  if (mcl <= 0 || left < 2) return RF_OK;
+  const double rate = env_int("RF_HYB3_R100", 120) / 100.0;   // per-SM rate, multicast vs pair kernel
+  const double f = (4.0 * mcl * rate) / (4.0 * mcl * rate + (left & ~1));
+  const int S1 = std::min(T2, (int)std::lround(f * T / 2.0));   // rows are uniform: split by row count
+  if (S1 <= 0 || 2 * S1 >= T) return RF_OK;
+  RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
+  rfk::Sched sm = rfk::Sched::make(0, 256, 0, S1, tn, kb, 0, raster_gm(4, 3));
+  rfk::Sched sp = rfk::Sched::make(0, 256, 2 * S1, T, tn, kb, 0, raster_gm(8, 3));
+  sm.started = prog + 255;
+  if ((s = launch_hybrid_pair<Cm, Cp>("K3_gemm_sigma", tA, tB, tBh, tA, tA, sm, sp, e, prog + 255, sms, left & ~1,
+                                      st)))
+    return s;
   *used = true;
   return RF_OK;
 }
@@ -545,19 +592,34 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
   const rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
                                          raster_gm(8, 3));
+  // K3 = the pair kernel, or (bf16 / tf32, large n) the multicast + pair hybrid (launch_k3_hybrid)
+  auto run_k3 = [&](const auto& e3) -> rf_status {
+    using E3 = std::decay_t<decltype(e3)>;
+    if constexpr (kSplit == 1) {
+      if (env_int("RF_K3_MC", 1)) {
+        using C3m = rfk::TcCfg<kFmt, kSplit, 256, 0, 4>;
+        CUtensorMap tBh;   // W with a 64-row box: the multicast kernel's half B tiles
+        rf_status r;
+        if ((r = make_tmap(&tBh, WB, bf, g.m_local, g.p, ldwb, 64))) return r;
+        bool used = false;
+        if ((r = launch_k3_hybrid<C3m, C3, E3>(tA, tB, tBh, g.n, g.m_local, kb3, e3, (uint32_t*)(g.w + g.pl.off_prog),
+                                               g.sms, g.st, &used)))
+          return r;
+        if (used) return RF_OK;
+      }
+    }
+    return launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st);
+  };
   if (g.act == RF_ACT_TANH) {
-    rfk::EpiSigma<kOut, RF_ACT_TANH> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
-    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_TANH>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
   } else if (g.act == RF_ACT_ERF) {
-    rfk::EpiSigma<kOut, RF_ACT_ERF> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
-    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_ERF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
   } else if (g.act == RF_ACT_SIGMOID_HALF) {
-    rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
-    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
   } else {   // NEXT-3 Table-2 activations: one instantiation, σ chosen at run time
-    rfk::EpiSigma<kOut, -1> e3{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act};
-    if ((s = launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st))) return s;
+    s = run_k3(rfk::EpiSigma<kOut, -1>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
   }
+  if (s) return s;
 
   if ((s = make_tmap(&tA, S0, bf, g.n, g.m_local, g.pl.ldS, 128))) return s;
   tB = tA;

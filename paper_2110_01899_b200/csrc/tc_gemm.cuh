@@ -44,7 +44,7 @@ template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)
           int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8>
 struct TcCfg {
   static constexpr int CL = kCl;
-  static_assert(kCl == 2 || (kCl == 4 && kBN == 512 && kSplit == 1), "4-CTA clusters: BN = 512, one operand split");
+  static_assert(kCl == 2 || (kCl == 4 && kSplit == 1), "4-CTA clusters: one operand split");
   static constexpr int BM = 256, BN = kBN;      // pair tile
   static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
   static constexpr int ESZ = kFmt == 1 ? 2 : (kFmt == 3 ? 1 : 4);
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (NOPS == 2) {
+    if (NOPS == 2 || Cfg::CL == 4) {
       ptx::prefetch_tmap(&tmA_lo);
       ptx::prefetch_tmap(&tmB_lo);
     }
@@ -817,9 +817,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
             uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
             ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
-            if (Cfg::CL == 4) {
+            if (Cfg::CL == 4 && NSUB == 2) {
               ptx::tma_load_2d_cg2_mc(b + pi * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)pi, mc_mask,
                                       pol);
+            } else if (Cfg::CL == 4) {
+              // 256-wide tiles: the pair's B tile is one sub-tile; CTA (pi, r) loads the 64-row half pi of its rank's
+              // 128 rows (tmB_lo: the same operand with a 64-row box) and multicasts it to rank r of both pairs
+              ptx::tma_load_2d_cg2_mc(b + pi * (Cfg::B_BYTES / 2), &tmB_lo, full_rel0 + stage * 8, k, rb + 64 * (int)pi,
+                                      mc_mask, pol);
             } else {
 #pragma unroll
               for (int s = 0; s < NSUB; ++s)

@@ -311,3 +311,29 @@ def test_phi_wide_epilogue_bit_exact(prec, out, monkeypatch):
         assert np.array_equal(res[0][I, J], res[1][I, J])
     else:
         assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("act,prec", [("erf", "bf16"), ("relu", "bf16"), ("erf", "tf32")])
+def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
+    """K3's multicast + pair hybrid (n ≥ 32 row tiles: 4-CTA clusters sharing each B tile as two multicast 64-row
+    halves, pair clusters on the leftover SMs) accumulates in the same order as the pair kernel: G agrees bit for
+    bit, and with the oracle.  (TF32 truncates its inputs, so a one-sided σ such as ReLU carries a −2e-3 bias
+    there: TF32 is checked with erf.)"""
+    n, p, m = 8448 + 77, 128, 1024 + 40          # 34 row tiles, ragged rows and features
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((n, p)) / math.sqrt(p)
+    W = rng.standard_normal((m, p))
+    Xd, Wd = dev(X, prec), dev(W, prec)
+    res = []
+    for mc in ("1", "0"):
+        monkeypatch.setenv("RF_K3_MC", mc)
+        G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper")
+        torch.cuda.synchronize()
+        res.append(G)
+    assert torch.equal(res[0], res[1])
+    S = synthetic.sample_indices(n, count=256, tile_stride=512)
+    St = torch.tensor(S, device="cuda")
+    sub = back(res[0].index_select(0, St).index_select(1, St))
+    ref = oracle.gram(back(Xd.index_select(0, St)), back(Wd), act)
+    I, J = upper_idx(len(S))
+    assert report(f"G K3-multicast {act} {prec} n={n}", sub[I, J], ref[I, J], S[I], S[J]) <= TOL[prec]
