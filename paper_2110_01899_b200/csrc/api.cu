@@ -535,8 +535,9 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
 // full rate against the ≈ 6.3 KB/clk chip limit); the multicast cuts that to 48 B (configs[3]: 9.57 → 7.97 ms on
 // 132 SMs alone).
 template <class Cm, class Cp, class Epi>
-rf_status launch_k3_hybrid(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tBh, int64_t n,
-                           int64_t m, int kb, const Epi& e, uint32_t* prog, int sms, cudaStream_t st, bool* used) {
+rf_status launch_k3_hybrid(const char* name, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tBh,
+                           int64_t n, int64_t m, int kb, const Epi& e, uint32_t* prog, int sms, cudaStream_t st,
+                           bool* used) {
   *used = false;
   const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512), tn = (int)((m + 255) / 256);
   if (env_int("RF_K3_HYBRID", 1) == 0 || T < 32 || !wait32_h() || !side_stream()) return RF_OK;
@@ -553,8 +554,7 @@ rf_status launch_k3_hybrid(const CUtensorMap& tA, const CUtensorMap& tB, const C
   rfk::Sched sm = rfk::Sched::make(0, 256, 0, S1, tn, kb, 0, raster_gm(4, 3));
   rfk::Sched sp = rfk::Sched::make(0, 256, 2 * S1, T, tn, kb, 0, raster_gm(8, 3));
   sm.started = prog + 255;
-  if ((s = launch_hybrid_pair<Cm, Cp>("K3_gemm_sigma", tA, tB, tBh, tA, tA, sm, sp, e, prog + 255, sms, left & ~1,
-                                      st)))
+  if ((s = launch_hybrid_pair<Cm, Cp>(name, tA, tB, tBh, tA, tA, sm, sp, e, prog + 255, sms, left & ~1, st)))
     return s;
   *used = true;
   return RF_OK;
@@ -602,8 +602,8 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
         rf_status r;
         if ((r = make_tmap(&tBh, WB, bf, g.m_local, g.p, ldwb, 64))) return r;
         bool used = false;
-        if ((r = launch_k3_hybrid<C3m, C3, E3>(tA, tB, tBh, g.n, g.m_local, kb3, e3, (uint32_t*)(g.w + g.pl.off_prog),
-                                               g.sms, g.st, &used)))
+        if ((r = launch_k3_hybrid<C3m, C3, E3>("K3_gemm_sigma", tA, tB, tBh, g.n, g.m_local, kb3, e3,
+                                               (uint32_t*)(g.w + g.pl.off_prog), g.sms, g.st, &used)))
           return r;
         if (used) return RF_OK;
       }
@@ -1267,7 +1267,7 @@ rf_status ter_validate(const char* fn, const void* X, int64_t ldx, const void* T
 // K3^ter into `feat` (bytes, ld multiple of 16): σ^ter(c·XTᵀ) as fp8 codes.
 rf_status launch_k3_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n, int64_t m_local,
                         double eps, double s_minus, double s_plus, uint8_t* feat, int64_t ldf, int sms,
-                        cudaStream_t st) {
+                        cudaStream_t st, uint32_t* prog = nullptr) {
   using C3 = rfk::TcCfg<1, 1, 256, 0>;
   CUtensorMap tA, tB;
   rf_status s;
@@ -1276,6 +1276,15 @@ rf_status launch_k3_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, 
   const double inv_c = std::sqrt(1.0 - eps);   // t± = s± / c, c = (1 − ε)^{-1/2}
   rfk::EpiSigmaTer e{feat, ldf, n, m_local, (float)(s_minus * inv_c), (float)(s_plus * inv_c)};
   const int kb = (int)((p + C3::BK - 1) / C3::BK);
+  if (prog && env_int("RF_K3_MC", 1)) {   // multicast + pair hybrid (workspace progress words available)
+    using C3m = rfk::TcCfg<1, 1, 256, 0, 4>;
+    CUtensorMap tBh;
+    if ((s = make_tmap(&tBh, T, true, m_local, p, ldt, 64))) return s;
+    bool used = false;
+    if ((s = launch_k3_hybrid<C3m, C3>("K3_ter_features", tA, tB, tBh, n, m_local, kb, e, prog, sms, st, &used)))
+      return s;
+    if (used) return RF_OK;
+  }
   const rfk::Sched sc =
       rfk::Sched::make(0, 256, 0, (int)((n + 255) / 256), (int)((m_local + 255) / 256), kb, 0, raster_gm(8, 3));
   return launch_tc<C3>("K3_ter_features", tA, tB, tA, tB, tA, sc, e, sms, st);
@@ -1351,7 +1360,9 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
   char* w = (char*)ws;
   uint8_t* S = (uint8_t*)(w + pl.off_s);
   // K3^ter: Σ^terᵀ = σ^ter(c·X Tᵀ) as fp8 codes
-  if ((s = launch_k3_ter(X, ldx, T, ldt, p, n, m_local, eps, s_minus, s_plus, S, pl.ldS, dev.sms, st))) return s;
+  if ((s = launch_k3_ter(X, ldx, T, ldt, p, n, m_local, eps, s_minus, s_plus, S, pl.ldS, dev.sms, st,
+                         (uint32_t*)(w + pl.off_prog))))
+    return s;
   // K4^ter: G^ter = Σ^terᵀΣ^ter / m on the fp8 tensor path (kind::f8f6f4): ±1·±1 products and their sums
   // (|sum| ≤ m_local ≤ 2^24) are exact in the fp32 accumulator, so m·G^ter is an exact integer count.
   using C4 = rfk::TcCfg<3, 1, 512>;
