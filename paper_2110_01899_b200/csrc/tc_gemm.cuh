@@ -13,13 +13,15 @@
 // 256·BN·64 MACs — half (BN=256) or a third (BN=512) of the 1-CTA 128×256 tile's L2 traffic per flop.
 // K-block = one 128-byte swizzle row (64 bf16 / 32 fp32).
 //
-// Warp roles (384 threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA, one thread), w2 TMEM
-// allocator, w3 idle, w4..w11 epilogue (warp w: TMEM lane quarter w%4, column half (w-4)/4).
+// Warp roles (128 + 32·kEpiW threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA, one thread), w2 TMEM
+// allocator, w3 idle, w4.. epilogue (warp w: TMEM lane quarter w%4; with 8 epilogue warps column half (w-4)/4,
+// with 12 / 16 the 32-column chunks ≡ (w-4)/4 mod 3 / 4).
 // Pipelines: smem ring (full barrier in the leader, empty barriers in both CTAs) TMA→MMA; TMEM
 // accumulator slots (2 × 256 columns for BN = 256, 1 × 512 for BN = 512) MMA→epilogue.
 //
 // K-chunked accumulation (kchunk k-blocks): the K range of a tile is cut into chunks whose partial sums
-// start from zero in TMEM and are added in fp32 (round-to-nearest) in the epilogue.  The tensor pipe's
+// start from zero in TMEM slot 0 and are added in fp32 (round-to-nearest) into a running sum in TMEM slot 1
+// by the epilogue warps; the functor sees the final sum once.  The tensor pipe's
 // accumulation into TMEM loses up to ~2^-23 relative per MMA (measured: 3×TF32 SYRK error grows
 // linearly with K), so long-K fp32-accurate results need short chunks.
 // 3×TF32 (kSplit = 3): each stage holds A_hi, A_lo, B_hi, B_lo; per K-step three MMAs lo·hi, hi·lo,
@@ -37,7 +39,9 @@ namespace rfk {
 // kStg: 4-KB TMA-store staging buffers per epilogue warp (-1 = default: 1 if stages are large, else 2;
 // 0 for epilogues that store directly from registers, e.g. K3).
 // kCl: CTAs per cluster.  2 = one CTA pair per cluster.  4 = two pairs computing vertically adjacent tiles
-// (row tiles 2I, 2I+1, same column tile): each CTA loads its own A half and ONE of the NSUB B sub-tiles for its
+// (row tiles 2I, 2I+1, same column tile).  BN = 256: each CTA loads one 64-row half of its rank's B rows (through
+// the 64-row-box map passed as tmB_lo) and multicasts it to the same rank of both pairs.  BN = 512: each CTA
+// loads its own A half and ONE of the NSUB B sub-tiles for its
 // rank-in-pair and TMA-multicasts it to the same rank of both pairs, so a B sub-tile leaves L2 once per cluster
 // instead of once per pair (a third less L2 → SM traffic per flop for BN = 512).  Requires NSUB == 2, kSplit == 1.
 template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
