@@ -43,7 +43,8 @@ namespace rfk {
 // the 64-row-box map passed as tmB_lo) and multicasts it to the same rank of both pairs.  BN = 512: each CTA
 // loads its own A half and ONE of the NSUB B sub-tiles for its
 // rank-in-pair and TMA-multicasts it to the same rank of both pairs, so a B sub-tile leaves L2 once per cluster
-// instead of once per pair (a third less L2 → SM traffic per flop for BN = 512).  Requires NSUB == 2, kSplit == 1.
+// instead of once per pair (a third less L2 → SM traffic per flop for BN = 512, a quarter for BN = 256).
+// Requires kSplit == 1.
 template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
           int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8>
 struct TcCfg {
