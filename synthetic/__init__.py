@@ -200,3 +200,22 @@ def make_T(cfg: Config | int, eps: float, rows: Optional[np.ndarray] = None, *, 
         sel = blocks == b
         out[sel] = full[rows[sel] - b * BLOCK]
     return out
+
+
+def make_ridge_gmm(n_train: int, n_test: int, p: int, seed: int = 0):
+    """Two-class GMM of the paper's ridge experiments (Eq. (GMM)): x = μ_a/√p + z,
+    z ~ N(0, C_a/p), μ_a = 4·e_a (a = 1, 2), C_a = (1 + 4(a − 1)/√p)·I_p; balanced classes in random order; the
+    regression target is the class sign y = −1 (a = 1) / +1 (a = 2).  Returns X (n_train + n_test, p) with the
+    training samples first, and y (n_train + n_test, 1).  Stands in for the paper's MNIST / Cov-Type / Census data.
+    Data only: no arithmetic of the method."""
+    rng = np.random.Generator(np.random.PCG64(SEED_BASE + 7001 + seed))
+    n = n_train + n_test
+    lab = np.concatenate([np.zeros(n // 2, dtype=np.int64), np.ones(n - n // 2, dtype=np.int64)])
+    rng.shuffle(lab)
+    X = rng.standard_normal((n, p))
+    scale = np.where(lab == 0, 1.0, math.sqrt(1.0 + 4.0 / math.sqrt(p)))
+    X *= scale[:, None] / math.sqrt(p)
+    X[np.arange(n), lab] += 4.0 / math.sqrt(p)
+    y = np.where(lab == 0, -1.0, 1.0)[:, None]
+    return X, y
+
