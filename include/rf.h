@@ -337,6 +337,26 @@ rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ld
                            rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
                            void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * NEXT-4: random-features kernel ridge regression on G (the paper's downstream use of G: Section 5 P:757-761,
+ * App. A; the estimator is the textbook one, R20).  For each γ in gammas:
+ *     α_γ = (G_train + γ·I)^{-1} Y        (fp64 blocked Cholesky of G_train + γI, then two triangular solves)
+ *     Ŷ_γ = G_cross · α_γ                 (G_cross[t][i] = the Gram of test sample t and training sample i)
+ * G_train and G_cross are read from ONE Gram over the stacked samples [X_train; X_test] (n_all = n_train + n_test
+ * rows), as rf_gram / rf_gram_ter write it: only entries j ≥ i are read (UPPER or FULL layout, ld = ldg ≥ n_all).
+ *   G       device f32, n_all × n_all (ldg), 4-B aligned
+ *   gammas  HOST, n_gamma values, each finite and > 0
+ *   Y       device f64, n_train × nrhs row-major (ldy ≥ nrhs): the training targets
+ *   alpha   device f64, n_gamma blocks of n_train × nrhs (row-major, ld nrhs), block g for gammas[g]
+ *   Yhat    device f64, n_gamma blocks of n_test × nrhs (ld nrhs); may be NULL when n_test = 0
+ *   ws      ≥ rf_ridge_workspace_size(n_train) bytes, 256-B aligned (the fp64 factor)
+ * Synchronous at the end (one event wait, through mapped host memory) to report the factorisation:
+ * G_train + γI not positive definite (a non-positive pivot) → RF_E_NONFINITE. */
+rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes);
+rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
+                   int32_t n_gamma, const double* Y, int64_t ldy, int32_t nrhs, double* alpha, double* Yhat,
+                   void* ws, size_t ws_bytes, void* stream);
+
 /* Number of kernel launches the last successful rf_gram / rf_phi_closed_form call on this thread
  * enqueued (for bench accounting). */
 int32_t rf_last_launch_count(void);

@@ -18,8 +18,8 @@ __all__ = ["rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed_form", "rf
            "rf_last_launch_count", "rf_pack_plan", "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk",
            "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter",
            "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "rf_gram_packed_p2p",
-           "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems", "RFError", "PREC",
-           "ACT"]
+           "rf_pack_reduce", "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems", "rf_ridge",
+           "rf_ridge_workspace_size", "RFError", "PREC", "ACT"]
 
 _TORCH_DT = None
 
@@ -51,7 +51,7 @@ def _check_tensor(name, t, dtype):
         raise RFError(_lib.RF_E_INVALID, f"{name} must be a CUDA tensor")
     if t.dtype != dtype:
         raise RFError(_lib.RF_E_INVALID, f"{name} has dtype {t.dtype}, precision mode needs {dtype}")
-    if t.dim() != 2 or t.stride(1) != 1:
+    if t.dim() != 2 or (t.stride(1) != 1 and t.shape[1] > 1):
         raise RFError(_lib.RF_E_INVALID, f"{name} must be 2-D with unit column stride")
 
 
@@ -389,3 +389,35 @@ def rf_ipc_open(handle: bytes) -> int:
 
 def rf_ipc_close(ptr: int) -> None:
     _lib.check(load().rf_ipc_close(ctypes.c_void_p(int(ptr))))
+
+
+def rf_ridge_workspace_size(n_train: int) -> int:
+    need = ctypes.c_size_t()
+    _lib.check(load().rf_ridge_workspace_size(int(n_train), ctypes.byref(need)))
+    return need.value
+
+
+def rf_ridge(G, n_train: int, gammas, Y, n_test: Optional[int] = None, ws=None, stream=None):
+    """NEXT-4 kernel ridge regression on the stacked Gram G of [X_train; X_test] (include/rf.h rf_ridge).
+    G: (n_all, n_all) float32 CUDA tensor (upper triangle read); Y: (n_train, r) float64 CUDA tensor.
+    Returns (alpha, Yhat): (len(gammas), n_train, r) and (len(gammas), n_test, r) float64 tensors."""
+    torch = _torch()
+    _check_tensor("G", G, torch.float32)
+    if Y.dim() == 1:
+        Y = Y[:, None]
+    _check_tensor("Y", Y, torch.float64)
+    n_all = G.shape[0]
+    n_test = n_all - int(n_train) if n_test is None else int(n_test)
+    gam = [float(g) for g in gammas]
+    r = Y.shape[1]
+    alpha = torch.empty((len(gam), int(n_train), r), dtype=torch.float64, device=G.device)
+    Yhat = torch.empty((len(gam), max(n_test, 0), r), dtype=torch.float64, device=G.device)
+    if ws is None:
+        ws = torch.empty(rf_ridge_workspace_size(n_train), dtype=torch.uint8, device=G.device)
+    garr = (ctypes.c_double * len(gam))(*gam)
+    _lib.check(load().rf_ridge(ctypes.c_void_p(G.data_ptr()), G.stride(0), int(n_train), n_test, garr, len(gam),
+                               ctypes.c_void_p(Y.data_ptr()), Y.stride(0), r, ctypes.c_void_p(alpha.data_ptr()),
+                               ctypes.c_void_p(Yhat.data_ptr()) if n_test > 0 else None,
+                               ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_ptr(stream)))
+    return alpha, Yhat
+

@@ -30,7 +30,8 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_pack_tile_map", "rf_gram_packed", "rf_stream_wait_chunk", "rf_trf_thresholds",
            "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
            "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2", "rf_gram_packed_p2p", "rf_pack_reduce",
-           "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems")
+           "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems", "rf_ridge_workspace_size",
+           "rf_ridge")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -81,6 +82,8 @@ def load() -> ctypes.CDLL:
     lib.rf_gram.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64,
                             vp, sz, vp]
     lib.rf_packed_tri_elems.argtypes = [i64, ctypes.POINTER(i64)]
+    lib.rf_ridge_workspace_size.argtypes = [i64, ctypes.POINTER(sz)]
+    lib.rf_ridge.argtypes = [vp, i64, i64, i64, ctypes.POINTER(dbl), i32, vp, i64, i32, vp, vp, vp, sz, vp]
     lib.rf_phi_workspace_size.argtypes = [i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_phi_closed_form.argtypes = [vp, i64, i64, i64, ctypes.c_int, dbl, ctypes.POINTER(rf_moments_t),
                                        ctypes.c_int, ctypes.c_int, i64, i64, vp, i64, vp, sz, vp]

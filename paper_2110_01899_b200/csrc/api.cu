@@ -17,6 +17,7 @@
 #include "k_aux.cuh"
 #include "k_center.cuh"
 #include "k_simt.cuh"
+#include "k_ridge.cuh"
 #include "rf_common.cuh"
 #include "tc_gemm.cuh"
 
@@ -893,7 +894,7 @@ struct HostMailbox {
 };
 static thread_local HostMailbox t_mailbox;
 
-static rf_status tau_reduce_to_host(const double* nrm2, int64_t n, double* out_dev, cudaStream_t st, double h[2]) {
+static rf_status host_mailbox(HostMailbox** out) {
   int dev = 0;
   RF_CUDA_CHECK(cudaGetDevice(&dev));
   HostMailbox& mb = t_mailbox;
@@ -904,6 +905,15 @@ static rf_status tau_reduce_to_host(const double* nrm2, int64_t n, double* out_d
     mb.h = (volatile double*)p;
     mb.dev = dev;
   }
+  *out = &mb;
+  return RF_OK;
+}
+
+static rf_status tau_reduce_to_host(const double* nrm2, int64_t n, double* out_dev, cudaStream_t st, double h[2]) {
+  HostMailbox* pmb = nullptr;
+  rf_status s0;
+  if ((s0 = host_mailbox(&pmb))) return s0;
+  HostMailbox& mb = *pmb;
   mb.h[0] = mb.h[1] = -1.0;
   {
     ProfScope ps("K1_tau_reduce", st);
@@ -1861,3 +1871,143 @@ rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act ac
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------------------------
+// NEXT-4: random-features kernel ridge regression on G, include/rf.h rf_ridge.
+namespace {
+int64_t ridge_lda(int64_t n) { return (n + 7) / 8 * 8; }
+}  // namespace
+
+extern "C" {
+
+rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes) {
+  if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
+  if (n_train <= 0 || n_train > ((int64_t)1 << 31)) return fail(RF_E_INVALID, "rf_ridge: n_train must be in (0, 2^31]");
+  *bytes = align256((size_t)n_train * ridge_lda(n_train) * 8) + 256;
+  return ok();
+}
+
+rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
+                   int32_t n_gamma, const double* Y, int64_t ldy, int32_t nrhs, double* alpha, double* Yhat,
+                   void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!G || !Y || !alpha || !gammas) return fail(RF_E_INVALID, "rf_ridge: G, Y, alpha and gammas are required");
+  if (n_train <= 0 || n_test < 0 || nrhs <= 0 || n_gamma <= 0)
+    return fail(RF_E_INVALID, "rf_ridge: need n_train > 0, n_test >= 0, nrhs > 0, n_gamma > 0");
+  if (n_test > 0 && !Yhat) return fail(RF_E_INVALID, "rf_ridge: Yhat is required when n_test > 0");
+  if (ldg < n_train + n_test) return fail(RF_E_INVALID, "rf_ridge: ldg (%lld) < n_train + n_test", (long long)ldg);
+  if (ldy < nrhs) return fail(RF_E_INVALID, "rf_ridge: ldy < nrhs");
+  if ((reinterpret_cast<uintptr_t>(G) & 3) || (reinterpret_cast<uintptr_t>(Y) & 7) ||
+      (reinterpret_cast<uintptr_t>(alpha) & 7) || (Yhat && (reinterpret_cast<uintptr_t>(Yhat) & 7)))
+    return fail(RF_E_INVALID, "rf_ridge: misaligned pointer (G 4 B, Y / alpha / Yhat 8 B)");
+  for (int g = 0; g < n_gamma; ++g)
+    if (!(gammas[g] > 0.0) || !std::isfinite(gammas[g]))
+      return fail(RF_E_INVALID, "rf_ridge: gamma[%d] = %g must be finite and > 0", g, gammas[g]);
+  size_t need = 0;
+  rf_status s;
+  if ((s = rf_ridge_workspace_size(n_train, &need))) return s;
+  if (!ws || ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(RF_E_WORKSPACE, "rf_ridge: workspace needs %zu bytes, 256-B aligned (got %zu)", need, ws_bytes);
+  DevInfo dev;
+  if ((s = check_device(&dev))) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = n_train, lda = ridge_lda(n);
+  double* A = (double*)ws;
+  int* info = (int*)((char*)ws + align256((size_t)n * lda * 8));
+  RF_CUDA_CHECK(cudaMemsetAsync(info, 0, sizeof(int), st));
+  RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, rfk::kPanelSmem));
+  const int nblk = (int)((n + rfk::kRB - 1) / rfk::kRB);
+  auto check = [&]() -> rf_status {
+    RF_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    return RF_OK;
+  };
+  for (int g = 0; g < n_gamma; ++g) {
+    double* al = alpha + (int64_t)g * n * nrhs;
+    {
+      ProfScope ps("KR_build", st);
+      const unsigned nt = (unsigned)((n + 31) / 32);
+      rfk::k_ridge_build<<<dim3(nt, nt), 256, 0, st>>>(G, ldg, n, gammas[g], A, lda);
+    }
+    if ((s = check())) return s;
+    for (int k = 0; k < nblk; ++k) {
+      {
+        ProfScope ps("KR_chol_diag", st);
+        rfk::k_chol_diag<<<1, 256, 0, st>>>(A, lda, n, k, info);
+      }
+      if ((s = check())) return s;
+      const int64_t r0 = (int64_t)k * rfk::kRB, r1 = r0 + rfk::kRB, m = n - r1;
+      if (m <= 0) continue;
+      {
+        ProfScope ps("KR_chol_panel", st);
+        rfk::k_chol_panel<<<(unsigned)((m + rfk::kRB - 1) / rfk::kRB), rfk::kRB, rfk::kPanelSmem, st>>>(A, lda, n, k);
+      }
+      if ((s = check())) return s;
+      const double* Pn = A + r1 * lda + r0;                  // panel rows r1.., columns r0 .. r0 + 64
+      if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, m, rfk::kRB, 1, 0,
+                                   (int)((m + rfk::kSimtTile - 1) / rfk::kSimtTile),
+                                   rfk::SimtCholUpd{A, lda, r1, m}, st)))
+        return s;
+    }
+    // α = L^{-T} L^{-1} Y, in place in alpha (row-major n × nrhs)
+    RF_CUDA_CHECK(cudaMemcpy2DAsync(al, (size_t)nrhs * 8, Y, (size_t)ldy * 8, (size_t)nrhs * 8, (size_t)n,
+                                    cudaMemcpyDeviceToDevice, st));
+    const unsigned rw = (unsigned)((nrhs + 3) / 4);
+    for (int k = 0; k < nblk; ++k) {
+      {
+        ProfScope ps("KR_trsv", st);
+        rfk::k_trsv_fwd<<<rw, 128, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+      }
+      if ((s = check())) return s;
+      const int64_t below = n - (int64_t)(k + 1) * rfk::kRB;
+      if (below > 0) {
+        {
+          ProfScope ps("KR_gemv", st);
+          const unsigned gb = (unsigned)std::min<int64_t>((below + 7) / 8, (int64_t)dev.sms * 8);
+          rfk::k_gemv_fwd<<<gb, 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+        }
+        if ((s = check())) return s;
+      }
+    }
+    for (int k = nblk - 1; k >= 0; --k) {
+      {
+        ProfScope ps("KR_trsv", st);
+        rfk::k_trsv_bwd<<<rw, 128, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+      }
+      if ((s = check())) return s;
+      const int64_t r0 = (int64_t)k * rfk::kRB;
+      if (r0 > 0) {
+        {
+          ProfScope ps("KR_gemv", st);
+          const unsigned gb = (unsigned)std::min<int64_t>((r0 + 255) / 256, (int64_t)dev.sms * 4);
+          rfk::k_axpy_bwd<<<gb, 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+        }
+        if ((s = check())) return s;
+      }
+    }
+    if (n_test > 0) {
+      {
+        ProfScope ps("KR_predict", st);
+        const unsigned gb = (unsigned)std::min<int64_t>((n_test + 127) / 128, (int64_t)dev.sms * 8);
+        rfk::k_ridge_predict<<<gb, 128, 0, st>>>(G, ldg, n_train, n_test, al, nrhs, nrhs,
+                                                 Yhat + (int64_t)g * n_test * nrhs, nrhs);
+      }
+      if ((s = check())) return s;
+    }
+  }
+  // factorisation status (one host sync, through the mapped mailbox)
+  HostMailbox* mb = nullptr;
+  if ((s = host_mailbox(&mb))) return s;
+  volatile int* hi = reinterpret_cast<volatile int*>(mb->h);
+  hi[0] = -1;
+  rfk::k_publish_u32<<<1, 1, 0, st>>>(info, hi);
+  if ((s = check())) return s;
+  RF_CUDA_CHECK(cudaEventRecord(mb->ev, st));
+  RF_CUDA_CHECK(cudaEventSynchronize(mb->ev));
+  if (hi[0] != 0)
+    return fail(RF_E_NONFINITE, "rf_ridge: G_train + gamma*I is not positive definite (pivot %d)", (int)hi[0]);
+  return ok();
+}
+
+}  // extern "C"
+

@@ -1,0 +1,188 @@
+// NEXT-4: random-features kernel ridge regression on the Gram G, the paper's downstream use of G
+// (P:757-761).  For each ridge parameter γ:  A = G_train + γ·I (fp64, lower triangle), A = L·Lᵀ by a
+// blocked right-looking Cholesky (64-wide panels), α = L^{-T} L^{-1} Y, Ŷ_test = G_cross·α.  G_train and G_cross
+// are read from the upper triangle of ONE Gram over the stacked samples [X_train; X_test] (include/rf.h rf_ridge).
+//   k_ridge_build ...... A's lower triangle from G's upper triangle (32×32 smem transpose tiles), + γ on the diagonal
+//   k_chol_diag ........ Cholesky of the 64×64 diagonal block in shared memory (one CTA)
+//   k_chol_panel ....... L_ik = A_ik·L_kk^{-T} for the row blocks below (one CTA per block, one thread per row)
+//   trailing update .... A_ij −= L_ik·L_jkᵀ on the lower triangle: the K6 SIMT GEMM (k_simt.cuh) with SimtCholUpd
+//   k_trsv_fwd / k_gemv_fwd, k_trsv_bwd / k_axpy_bwd ... the two triangular solves, block by block
+//   k_ridge_predict .... Ŷ[t] = Σ_i G[i][n_train + t]·α[i]
+#pragma once
+#include <stdint.h>
+
+namespace rfk {
+
+constexpr int kRB = 64;
+
+__global__ void __launch_bounds__(256) k_ridge_build(const float* __restrict__ G, int64_t ldg, int64_t n,
+                                                     double gamma, double* __restrict__ A, int64_t lda) {
+  __shared__ float t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;          // A block (bi, bj), bj ≤ bi (lower)
+  if (bj > bi) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 × 8
+  // read G rows j ∈ block bj, columns i ∈ block bi (coalesced along i): G[j][i] with j ≤ i is the upper triangle
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = bj * 32 + r, i = bi * 32 + tx;
+    t[r][tx] = (j < n && i < n) ? G[j * ldg + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+    if (i < n && j < n) {
+      double v = j <= i ? (double)t[tx][r] : 0.0;
+      if (i == j) v += gamma;
+      A[i * lda + j] = v;
+    }
+  }
+}
+
+// In-place Cholesky of the diagonal block k (rows/cols [64k, 64k + nb)).  info: first non-positive pivot (1-based).
+__global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64_t lda, int64_t n, int k,
+                                                   int* __restrict__ info) {
+  __shared__ double a[kRB][kRB + 1];
+  const int64_t r0 = (int64_t)k * kRB;
+  const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    a[r][c] = c <= r ? A[(r0 + r) * lda + r0 + c] : 0.0;
+  }
+  __syncthreads();
+  for (int c = 0; c < nb; ++c) {
+    if (tid == 0) {
+      const double d = a[c][c];
+      if (!(d > 0.0) && *info == 0) *info = (int)(r0 + c + 1);
+      a[c][c] = sqrt(d);
+    }
+    __syncthreads();
+    const double inv = 1.0 / a[c][c];
+    for (int r = c + 1 + tid; r < nb; r += 256) a[r][c] *= inv;
+    __syncthreads();
+    const int w = nb - c - 1;
+    for (int e = tid; e < w * w; e += 256) {
+      const int r = c + 1 + e / w, s = c + 1 + e % w;
+      if (s <= r) a[r][s] -= a[r][c] * a[s][c];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    if (c <= r) A[(r0 + r) * lda + r0 + c] = a[r][c];
+  }
+}
+
+// Row block b (rows 64(k + 1 + b) ..) of panel k: X·L_kkᵀ = A_ik, one thread per row, forward over the columns.
+constexpr int kPanelSmem = 2 * kRB * (kRB + 1) * 8;     // dynamic shared memory of k_chol_panel (66.5 KB)
+__global__ void __launch_bounds__(kRB) k_chol_panel(double* __restrict__ A, int64_t lda, int64_t n, int k) {
+  extern __shared__ double panel_smem[];
+  double(*L)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(panel_smem);
+  double(*X)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(panel_smem + kRB * (kRB + 1));
+  const int64_t r0 = (int64_t)k * kRB, rb = r0 + kRB * (1 + (int64_t)blockIdx.x);
+  const int r = threadIdx.x;
+  for (int c = 0; c < kRB; ++c) L[c][r] = (r <= c) ? A[(r0 + c) * lda + r0 + r] : 0.0;   // L[c][r], r ≤ c
+  const bool live = rb + r < n;
+  for (int c = 0; c < kRB; ++c) X[r][c] = live ? A[(rb + r) * lda + r0 + c] : 0.0;
+  __syncthreads();
+  for (int c = 0; c < kRB; ++c) {
+    double s = X[r][c];
+    for (int t = 0; t < c; ++t) s -= X[r][t] * L[c][t];
+    X[r][c] = s / L[c][c];
+  }
+  if (live)
+    for (int c = 0; c < kRB; ++c) A[(rb + r) * lda + r0 + c] = X[r][c];
+}
+
+// Trailing update A_ij −= (L·Lᵀ)_ij, i ≥ j, from the GEMM over the panel rows (the GEMM computes the upper tiles
+// (i ≤ j) of the symmetric product; the lower element A[r1 + j][r1 + i] receives it).
+struct SimtCholUpd {
+  double* A;
+  int64_t lda, r1, m;
+  __device__ __forceinline__ void operator()(int64_t i, int64_t j, double v) const {
+    if (i < m && j < m && j >= i) A[(r1 + j) * lda + r1 + i] -= v;
+  }
+};
+
+// Forward solve of block k for every right-hand side: z_k = L_kk^{-1} y_k (one warp per right-hand side).
+__global__ void k_trsv_fwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
+                           int64_t ldy, int nrhs) {
+  const int lane = threadIdx.x & 31, rhs = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (rhs >= nrhs) return;
+  const int64_t r0 = (int64_t)k * kRB;
+  const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
+  for (int r = 0; r < nb; ++r) {
+    double s = 0.0;
+    for (int t = lane; t < r; t += 32) s += A[(r0 + r) * lda + r0 + t] * Y[(r0 + t) * ldy + rhs];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0) Y[(r0 + r) * ldy + rhs] = (Y[(r0 + r) * ldy + rhs] - s) / A[(r0 + r) * lda + r0 + r];
+    __syncwarp();
+  }
+}
+
+// y_i −= L[i][64k .. 64k+64)·z_k for the rows below block k (one warp per row).
+__global__ void k_gemv_fwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
+                           int64_t ldy, int nrhs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)k * kRB;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = r0 + kRB + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    const double l0 = A[i * lda + r0 + lane], l1 = A[i * lda + r0 + 32 + lane];
+    for (int h = 0; h < nrhs; ++h) {
+      double s = l0 * Y[(r0 + lane) * ldy + h] + l1 * Y[(r0 + 32 + lane) * ldy + h];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+      if (lane == 0) Y[i * ldy + h] -= s;
+    }
+  }
+}
+
+// Backward solve of block k: α_k = L_kk^{-T} z_k (one warp per right-hand side, rows from the last up).
+__global__ void k_trsv_bwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
+                           int64_t ldy, int nrhs) {
+  const int lane = threadIdx.x & 31, rhs = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (rhs >= nrhs) return;
+  const int64_t r0 = (int64_t)k * kRB;
+  const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
+  for (int r = nb - 1; r >= 0; --r) {
+    double s = 0.0;
+    for (int t = r + 1 + lane; t < nb; t += 32) s += A[(r0 + t) * lda + r0 + r] * Y[(r0 + t) * ldy + rhs];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0) Y[(r0 + r) * ldy + rhs] = (Y[(r0 + r) * ldy + rhs] - s) / A[(r0 + r) * lda + r0 + r];
+    __syncwarp();
+  }
+}
+
+// z_j −= Σ_{t < nb} L[64k + t][j]·α[64k + t] for the rows j above block k (one thread per j, coalesced along j).
+__global__ void k_axpy_bwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
+                           int64_t ldy, int nrhs) {
+  const int64_t r0 = (int64_t)k * kRB;
+  const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < r0; j += (int64_t)gridDim.x * blockDim.x) {
+    for (int h = 0; h < nrhs; ++h) {
+      double s = 0.0;
+      for (int t = 0; t < nb; ++t) s += A[(r0 + t) * lda + j] * Y[(r0 + t) * ldy + h];
+      Y[j * ldy + h] -= s;
+    }
+  }
+}
+
+// Ŷ[t][h] = Σ_{i < n_train} G[i][n_train + t]·α[i][h] (G's upper triangle: rows of training samples, columns of test
+// samples), one thread per test sample, coalesced along t.
+__global__ void k_ridge_predict(const float* __restrict__ G, int64_t ldg, int64_t n_train, int64_t n_test,
+                                const double* __restrict__ alpha, int64_t lda_, int nrhs, double* __restrict__ Yhat,
+                                int64_t ldyh) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_test; t += (int64_t)gridDim.x * blockDim.x) {
+    for (int h = 0; h < nrhs; ++h) {
+      double s = 0.0;
+      for (int64_t i = 0; i < n_train; ++i) s += (double)G[i * ldg + n_train + t] * alpha[i * lda_ + h];
+      Yhat[t * ldyh + h] = s;
+    }
+  }
+}
+
+// Copies one 32-bit word to mapped pinned host memory (status read-back that does not queue behind DMA copies).
+__global__ void k_publish_u32(const int* __restrict__ src, volatile int* dst) {
+  dst[0] = src[0];
+  __threadfence_system();
+}
+
+}  // namespace rfk

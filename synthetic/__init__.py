@@ -216,6 +216,6 @@ def make_ridge_gmm(n_train: int, n_test: int, p: int, seed: int = 0):
     scale = np.where(lab == 0, 1.0, math.sqrt(1.0 + 4.0 / math.sqrt(p)))
     X *= scale[:, None] / math.sqrt(p)
     X[np.arange(n), lab] += 4.0 / math.sqrt(p)
-    y = np.where(lab == 0, -1.0, 1.0)[:, None]
+    y = np.ascontiguousarray(np.where(lab == 0, -1.0, 1.0)[:, None])
     return X, y
 

@@ -263,3 +263,27 @@ def test_trf_thresholds_sign_function_and_errors():
     for bad in [(0.7, 0.0, 1.0), (0.25, 1 / (16 * math.pi), 2.0), (0.1, 0.0, 0.0), (-0.1, 0.0, 1.0)]:
         with pytest.raises(rf.RFError):
             rf.rf_trf_thresholds(*bad, 1)
+
+
+def test_ridge_validation():
+    lib = rf.load()
+    need = ctypes.c_size_t()
+    assert lib.rf_ridge_workspace_size(1000, ctypes.byref(need)) == 0 and need.value >= 1000 * 1000 * 8
+    assert lib.rf_ridge_workspace_size(0, ctypes.byref(need)) == _lib.RF_E_INVALID
+    buf = (ctypes.c_char * 4096)()
+    a = (ctypes.addressof(buf) + 255) // 256 * 256
+    g_ok = (ctypes.c_double * 2)(0.5, 1.0)
+    g_bad = (ctypes.c_double * 2)(0.5, 0.0)
+    vp = ctypes.c_void_p
+    # γ must be > 0
+    s = lib.rf_ridge(vp(a), 16, 8, 8, g_bad, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    assert s == _lib.RF_E_INVALID and b"gamma" in lib.rf_last_error()
+    # ldg must cover the stacked samples
+    s = lib.rf_ridge(vp(a), 15, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    assert s == _lib.RF_E_INVALID and b"ldg" in lib.rf_last_error()
+    # test predictions need Yhat
+    s = lib.rf_ridge(vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), None, vp(a), 16, None)
+    assert s == _lib.RF_E_INVALID and b"Yhat" in lib.rf_last_error()
+    # workspace too small
+    s = lib.rf_ridge(vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    assert s == _lib.RF_E_WORKSPACE
