@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-phi", action="store_true")
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
     ap.add_argument("--no-phi4", action="store_true", help="skip the configs[4] Φ-only measurement")
+    ap.add_argument("--no-ridge", action="store_true", help="skip the NEXT-4 ridge-regression measurement")
     ap.add_argument("--g5", default="fused", choices=["fused", "nccl"],
                     help="N>1: G5 as the fused peer-memory epilogue (default) or chunked NCCL reduce-scatter")
     ap.add_argument("--comm-sms", type=int, default=8,
@@ -553,6 +554,67 @@ def main():
         del Phi4, X4f
         torch.cuda.empty_cache()
 
+    # ---------------- NEXT-4: random-features ridge regression (the paper's downstream task): the
+    # whole solver including the random features (P:761 footnote), ReLU features with Gaussian W vs TRFs (ε = 0.9)
+    # matched to ReLU (Algorithm 1), on the GMM of P:1177 (p = 512, 1024 training + 512 test samples, m = 5·10^4),
+    # over a γ grid; plus the fp64 Cholesky rate at n = 16384.
+    ridge_line = None
+    if world == 1 and args.config == 3 and not args.no_ridge:
+        n_tr, n_te, pr, mr, eps_r = 1024, 512, 512, 50000, 0.9
+        Xr, yr = synthetic.make_ridge_gmm(n_tr, n_te, pr)
+        Xrd = torch.from_numpy(Xr).to(torch.bfloat16).to(device)
+        Wrd = torch.from_numpy(synthetic.make_W(1, m=mr, p=pr)).to(torch.bfloat16).to(device)
+        Trd = torch.from_numpy(synthetic.make_T(1, eps_r, m=mr, p=pr)).to(torch.bfloat16).to(device)
+        Yrd = torch.from_numpy(yr[:n_tr]).to(device)
+        gam = [1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3, 1e4]
+        tau_r = rf.rf_estimate_tau(Xrd)
+
+        def rf_path():
+            G_ = rf.rf_gram(Xrd, Wrd, act="relu", prec="bf16", out="upper")
+            return rf.rf_ridge(G_, n_tr, gam, Yrd)[1]
+
+        def ter_path():
+            sm_, sp_ = rf.rf_trf_thresholds_for("relu", tau_r)
+            G_ = rf.rf_gram_ter(Xrd, Trd, eps_r, sm_, sp_, out="upper")
+            return rf.rf_ridge(G_, n_tr, gam, Yrd)[1]
+
+        def timed(fn, reps=3):
+            fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                out_ = fn()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a_.elapsed_time(b_))
+            return sorted(ts)[len(ts) // 2], out_
+
+        t_rf, yh_rf = timed(rf_path)
+        t_ter, yh_ter = timed(ter_path)
+        y_te = torch.from_numpy(yr[n_tr:]).to(device)
+        mse_rf = [float(((yh_rf[g] - y_te) ** 2).mean()) for g in range(len(gam))]      # test MSE (reported metric)
+        mse_ter = [float(((yh_ter[g] - y_te) ** 2).mean()) for g in range(len(gam))]
+        del Wrd, Trd
+        # fp64 Cholesky rate: one γ on a 16384-sample Gram (n³/3 flops of the factorisation)
+        nc = 16384
+        Xc = torch.from_numpy(synthetic.make_ridge_gmm(nc, 0, pr)[0]).to(torch.bfloat16).to(device)
+        Wc = torch.from_numpy(synthetic.make_W(1, m=4096, p=pr)).to(torch.bfloat16).to(device)
+        Gc = rf.rf_gram(Xc, Wc, act="relu", prec="bf16", out="upper")
+        Yc = torch.ones((nc, 1), dtype=torch.float64, device=device)
+        wsc = torch.empty(rf.rf_ridge_workspace_size(nc), dtype=torch.uint8, device=device)
+        t_ch, _ = timed(lambda: rf.rf_ridge(Gc, nc, [1.0], Yc, n_test=0, ws=wsc), reps=2)
+        ridge_line = {"what": "NEXT-4 ridge regression, whole solver incl. random features (P:761): ReLU features, "
+                              f"Gaussian W vs TRF ε={eps_r} matched to ReLU; GMM of P:1177, p={pr}, n_train={n_tr}, "
+                              f"n_test={n_te}, m={mr}; {len(gam)} γ values per solve",
+                      "gammas": gam, "test_mse_relu_rf": mse_rf, "test_mse_trf": mse_ter,
+                      "ms_relu_rf": t_rf, "ms_trf": t_ter,
+                      "cholesky_n": nc, "cholesky_ms": t_ch,
+                      "cholesky_fp64_tflops": nc ** 3 / 3.0 / (t_ch * 1e-3) / 1e12}
+        del Gc, Xc, Wc, wsc
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -591,6 +653,7 @@ def main():
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches[0], "clocks": clk, "peaks": pk, "trf": trf_line, "phi_configs4": phi4_line,
+            "ridge": ridge_line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

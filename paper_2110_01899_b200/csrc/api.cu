@@ -1883,7 +1883,8 @@ extern "C" {
 rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes) {
   if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
   if (n_train <= 0 || n_train > ((int64_t)1 << 31)) return fail(RF_E_INVALID, "rf_ridge: n_train must be in (0, 2^31]");
-  *bytes = align256((size_t)n_train * ridge_lda(n_train) * 8) + 256;
+  const size_t nblk = (size_t)((n_train + rfk::kRB - 1) / rfk::kRB);
+  *bytes = align256((size_t)n_train * ridge_lda(n_train) * 8) + 256 + nblk * rfk::kRB * rfk::kRB * 8;
   return ok();
 }
 
@@ -1914,8 +1915,10 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
   const int64_t n = n_train, lda = ridge_lda(n);
   double* A = (double*)ws;
   int* info = (int*)((char*)ws + align256((size_t)n * lda * 8));
+  double* Linv = (double*)((char*)ws + align256((size_t)n * lda * 8) + 256);   // 64×64 inverse per diagonal block
   RF_CUDA_CHECK(cudaMemsetAsync(info, 0, sizeof(int), st));
   RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, rfk::kPanelSmem));
+  RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, rfk::kDiagSmem));
   const int nblk = (int)((n + rfk::kRB - 1) / rfk::kRB);
   auto check = [&]() -> rf_status {
     RF_CUDA_CHECK(cudaGetLastError());
@@ -1933,7 +1936,7 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
     for (int k = 0; k < nblk; ++k) {
       {
         ProfScope ps("KR_chol_diag", st);
-        rfk::k_chol_diag<<<1, 256, 0, st>>>(A, lda, n, k, info);
+        rfk::k_chol_diag<<<1, 256, rfk::kDiagSmem, st>>>(A, lda, n, k, info, Linv + (int64_t)k * rfk::kRB * rfk::kRB);
       }
       if ((s = check())) return s;
       const int64_t r0 = (int64_t)k * rfk::kRB, r1 = r0 + rfk::kRB, m = n - r1;
@@ -1944,7 +1947,7 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
       }
       if ((s = check())) return s;
       const double* Pn = A + r1 * lda + r0;                  // panel rows r1.., columns r0 .. r0 + 64
-      if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, m, rfk::kRB, 1, 0,
+      if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, m, rfk::kRB, 2, 0,
                                    (int)((m + rfk::kSimtTile - 1) / rfk::kSimtTile),
                                    rfk::SimtCholUpd{A, lda, r1, m}, st)))
         return s;
@@ -1952,11 +1955,11 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
     // α = L^{-T} L^{-1} Y, in place in alpha (row-major n × nrhs)
     RF_CUDA_CHECK(cudaMemcpy2DAsync(al, (size_t)nrhs * 8, Y, (size_t)ldy * 8, (size_t)nrhs * 8, (size_t)n,
                                     cudaMemcpyDeviceToDevice, st));
-    const unsigned rw = (unsigned)((nrhs + 3) / 4);
+    const unsigned rw = (unsigned)((nrhs + 3) / 4);   // 4 right-hand sides per CTA of the block solves
     for (int k = 0; k < nblk; ++k) {
       {
         ProfScope ps("KR_trsv", st);
-        rfk::k_trsv_fwd<<<rw, 128, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+        rfk::k_trsv_fwd<<<rw, 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs, nrhs);
       }
       if ((s = check())) return s;
       const int64_t below = n - (int64_t)(k + 1) * rfk::kRB;
@@ -1972,7 +1975,7 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
     for (int k = nblk - 1; k >= 0; --k) {
       {
         ProfScope ps("KR_trsv", st);
-        rfk::k_trsv_bwd<<<rw, 128, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+        rfk::k_trsv_bwd<<<rw, 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs, nrhs);
       }
       if ((s = check())) return s;
       const int64_t r0 = (int64_t)k * rfk::kRB;

@@ -3,10 +3,11 @@
 // blocked right-looking Cholesky (64-wide panels), α = L^{-T} L^{-1} Y, Ŷ_test = G_cross·α.  G_train and G_cross
 // are read from the upper triangle of ONE Gram over the stacked samples [X_train; X_test] (include/rf.h rf_ridge).
 //   k_ridge_build ...... A's lower triangle from G's upper triangle (32×32 smem transpose tiles), + γ on the diagonal
-//   k_chol_diag ........ Cholesky of the 64×64 diagonal block in shared memory (one CTA)
+//   k_chol_diag ........ Cholesky of the 64×64 diagonal block in shared memory (one CTA), and its inverse
 //   k_chol_panel ....... L_ik = A_ik·L_kk^{-T} for the row blocks below (one CTA per block, one thread per row)
 //   trailing update .... A_ij −= L_ik·L_jkᵀ on the lower triangle: the K6 SIMT GEMM (k_simt.cuh) with SimtCholUpd
-//   k_trsv_fwd / k_gemv_fwd, k_trsv_bwd / k_axpy_bwd ... the two triangular solves, block by block
+//   k_trsv_fwd / k_gemv_fwd, k_trsv_bwd / k_axpy_bwd ... the two triangular solves, block by block (the diagonal
+//                        blocks through their inverses)
 //   k_ridge_predict .... Ŷ[t] = Σ_i G[i][n_train + t]·α[i]
 #pragma once
 #include <stdint.h>
@@ -37,39 +38,55 @@ __global__ void __launch_bounds__(256) k_ridge_build(const float* __restrict__ G
   }
 }
 
-// In-place Cholesky of the diagonal block k (rows/cols [64k, 64k + nb)).  info: first non-positive pivot (1-based).
+// In-place Cholesky of the diagonal block k (rows/cols [64k, 64k + nb)) in shared memory, then its inverse
+// L_kk^{-1} (column j by forward substitution on e_j, one thread per column) into Linv (64 × 64, row-major), which
+// turns the block solves of k_trsv_fwd / k_trsv_bwd into parallel triangular products.
+// info: first non-positive pivot (1-based).  Dynamic shared memory: kDiagSmem.
+constexpr int kDiagSmem = 2 * kRB * (kRB + 1) * 8;
 __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64_t lda, int64_t n, int k,
-                                                   int* __restrict__ info) {
-  __shared__ double a[kRB][kRB + 1];
+                                                   int* __restrict__ info, double* __restrict__ Linv) {
+  extern __shared__ double diag_smem[];
+  double(*a)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(diag_smem);
+  double(*x)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(diag_smem + kRB * (kRB + 1));
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
-  const int tid = threadIdx.x;
-  for (int e = tid; e < nb * nb; e += 256) {
-    const int r = e / nb, c = e % nb;
-    a[r][c] = c <= r ? A[(r0 + r) * lda + r0 + c] : 0.0;
-  }
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;   // 16 × 16 thread grid for the updates
+  for (int r = ty; r < kRB; r += 16)
+    for (int c = tx; c < kRB; c += 16)
+      a[r][c] = (r < nb && c <= r) ? A[(r0 + r) * lda + r0 + c] : (r == c ? 1.0 : 0.0);
   __syncthreads();
   for (int c = 0; c < nb; ++c) {
+    const double d = a[c][c];                   // every thread: the pivot (no extra barrier)
+    const double sd = sqrt(d), inv = 1.0 / sd;
+    __syncthreads();                            // all threads have read the pivot
     if (tid == 0) {
-      const double d = a[c][c];
       if (!(d > 0.0) && *info == 0) *info = (int)(r0 + c + 1);
-      a[c][c] = sqrt(d);
+      a[c][c] = sd;
     }
-    __syncthreads();
-    const double inv = 1.0 / a[c][c];
     for (int r = c + 1 + tid; r < nb; r += 256) a[r][c] *= inv;
     __syncthreads();
-    const int w = nb - c - 1;
-    for (int e = tid; e < w * w; e += 256) {
-      const int r = c + 1 + e / w, s = c + 1 + e % w;
-      if (s <= r) a[r][s] -= a[r][c] * a[s][c];
-    }
+    for (int r = c + 1 + ty; r < nb; r += 16)
+      for (int q = c + 1 + tx; q <= r; q += 16) a[r][q] -= a[r][c] * a[q][c];
     __syncthreads();
   }
-  for (int e = tid; e < nb * nb; e += 256) {
-    const int r = e / nb, c = e % nb;
-    if (c <= r) A[(r0 + r) * lda + r0 + c] = a[r][c];
+  for (int r = ty; r < nb; r += 16)
+    for (int c = tx; c <= r; c += 16) A[(r0 + r) * lda + r0 + c] = a[r][c];
+  // L^{-1}: column j = L^{-1} e_j (rows ≥ j), padded rows/columns (≥ nb) of the identity
+  if (tid < kRB) {
+    const int j = tid;
+    for (int r = 0; r < kRB; ++r) {
+      if (r < j) {
+        x[r][j] = 0.0;
+        continue;
+      }
+      double sum = r == j ? 1.0 : 0.0;
+      for (int t = j; t < r; ++t) sum -= a[r][t] * x[t][j];
+      x[r][j] = sum / a[r][r];
+    }
   }
+  __syncthreads();
+  for (int r = ty; r < kRB; r += 16)
+    for (int c = tx; c < kRB; c += 16) Linv[r * kRB + c] = x[r][c];
 }
 
 // Row block b (rows 64(k + 1 + b) ..) of panel k: X·L_kkᵀ = A_ik, one thread per row, forward over the columns.
@@ -93,30 +110,30 @@ __global__ void __launch_bounds__(kRB) k_chol_panel(double* __restrict__ A, int6
     for (int c = 0; c < kRB; ++c) A[(rb + r) * lda + r0 + c] = X[r][c];
 }
 
-// Trailing update A_ij −= (L·Lᵀ)_ij, i ≥ j, from the GEMM over the panel rows (the GEMM computes the upper tiles
-// (i ≤ j) of the symmetric product; the lower element A[r1 + j][r1 + i] receives it).
+// Trailing update A_ij −= (L·Lᵀ)_ij, j ≤ i, from the GEMM over the panel rows restricted to its lower tiles
+// (tri = 2), so every thread updates row-major elements of the lower triangle.
 struct SimtCholUpd {
   double* A;
   int64_t lda, r1, m;
   __device__ __forceinline__ void operator()(int64_t i, int64_t j, double v) const {
-    if (i < m && j < m && j >= i) A[(r1 + j) * lda + r1 + i] -= v;
+    if (i < m && j <= i) A[(r1 + i) * lda + r1 + j] -= v;
   }
 };
 
-// Forward solve of block k for every right-hand side: z_k = L_kk^{-1} y_k (one warp per right-hand side).
-__global__ void k_trsv_fwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
-                           int64_t ldy, int nrhs) {
-  const int lane = threadIdx.x & 31, rhs = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (rhs >= nrhs) return;
+// Forward solve of block k: z_k = L_kk^{-1} y_k as a triangular product with the inverse from k_chol_diag (one
+// thread per (row, right-hand side)).
+__global__ void __launch_bounds__(256) k_trsv_fwd(const double* __restrict__ Linv, int64_t n, int k,
+                                                  double* __restrict__ Y, int64_t ldy, int nrhs) {
+  __shared__ double y[4][kRB];
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
-  for (int r = 0; r < nb; ++r) {
-    double s = 0.0;
-    for (int t = lane; t < r; t += 32) s += A[(r0 + r) * lda + r0 + t] * Y[(r0 + t) * ldy + rhs];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    if (lane == 0) Y[(r0 + r) * ldy + rhs] = (Y[(r0 + r) * ldy + rhs] - s) / A[(r0 + r) * lda + r0 + r];
-    __syncwarp();
-  }
+  const int r = threadIdx.x & (kRB - 1), w = threadIdx.x >> 6, rhs = blockIdx.x * 4 + w;
+  if (rhs < nrhs) y[w][r] = r < nb ? Y[(r0 + r) * ldy + rhs] : 0.0;
+  __syncthreads();
+  if (rhs >= nrhs || r >= nb) return;
+  double s = 0.0;
+  for (int t = 0; t <= r; ++t) s += Linv[r * kRB + t] * y[w][t];
+  Y[(r0 + r) * ldy + rhs] = s;
 }
 
 // y_i −= L[i][64k .. 64k+64)·z_k for the rows below block k (one warp per row).
@@ -135,20 +152,19 @@ __global__ void k_gemv_fwd(const double* __restrict__ A, int64_t lda, int64_t n,
   }
 }
 
-// Backward solve of block k: α_k = L_kk^{-T} z_k (one warp per right-hand side, rows from the last up).
-__global__ void k_trsv_bwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
-                           int64_t ldy, int nrhs) {
-  const int lane = threadIdx.x & 31, rhs = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (rhs >= nrhs) return;
+// Backward solve of block k: α_k = L_kk^{-T} z_k (the transpose of the inverse from k_chol_diag).
+__global__ void __launch_bounds__(256) k_trsv_bwd(const double* __restrict__ Linv, int64_t n, int k,
+                                                  double* __restrict__ Y, int64_t ldy, int nrhs) {
+  __shared__ double y[4][kRB];
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
-  for (int r = nb - 1; r >= 0; --r) {
-    double s = 0.0;
-    for (int t = r + 1 + lane; t < nb; t += 32) s += A[(r0 + t) * lda + r0 + r] * Y[(r0 + t) * ldy + rhs];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-    if (lane == 0) Y[(r0 + r) * ldy + rhs] = (Y[(r0 + r) * ldy + rhs] - s) / A[(r0 + r) * lda + r0 + r];
-    __syncwarp();
-  }
+  const int r = threadIdx.x & (kRB - 1), w = threadIdx.x >> 6, rhs = blockIdx.x * 4 + w;
+  if (rhs < nrhs) y[w][r] = r < nb ? Y[(r0 + r) * ldy + rhs] : 0.0;
+  __syncthreads();
+  if (rhs >= nrhs || r >= nb) return;
+  double s = 0.0;
+  for (int t = r; t < nb; ++t) s += Linv[t * kRB + r] * y[w][t];
+  Y[(r0 + r) * ldy + rhs] = s;
 }
 
 // z_j −= Σ_{t < nb} L[64k + t][j]·α[64k + t] for the rows j above block k (one thread per j, coalesced along j).

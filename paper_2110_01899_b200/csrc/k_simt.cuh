@@ -52,8 +52,8 @@ struct SimtEq1 {
   }
 };
 
-// grid: (tiles_n, row tiles in [row_tile0, row_tile0 + gridDim.y)); tri ⇒ skip tiles strictly below the diagonal
-// (J < I).  128×128 tiles, 256 threads, 8×8 register micro-tile per thread (rows ty·4 + {0..3} and 64 + ty·4 +
+// grid: (tiles_n, row tiles in [row_tile0, row_tile0 + gridDim.y)); tri = 1 ⇒ skip tiles strictly below the
+// diagonal (J < I), tri = 2 ⇒ strictly above (J > I).  128×128 tiles, 256 threads, 8×8 register micro-tile per thread (rows ty·4 + {0..3} and 64 + ty·4 +
 // {0..3}, columns likewise with tx), K-slices of 16 staged k-major in shared memory (two 16-B loads per operand per
 // k give 64 FMAs), next slice prefetched into registers with 16-B global loads while the current one is consumed.
 // Rows are 16-B aligned (ld·sizeof(T) a multiple of 16 B, validated at the ABI); the K tail is zero-filled.
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) simt_gemm_nt(cons
   constexpr int NV = BM * BK / VEC / 256;                  // vectors per thread per operand per slice
   using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
   const int bi = blockIdx.y + row_tile0, bj = blockIdx.x;
-  if (tri && bj < bi) return;
+  if ((tri == 1 && bj < bi) || (tri == 2 && bj > bi)) return;   // 1: upper tiles (j ≥ i), 2: lower tiles
   __shared__ __align__(16) T As[BK][BM + PAD];
   __shared__ __align__(16) T Bs[BK][BN + PAD];
   const int tid = threadIdx.x;
