@@ -349,7 +349,9 @@ rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ld
  *   Y       device f64, n_train × nrhs row-major (ldy ≥ nrhs): the training targets
  *   alpha   device f64, n_gamma blocks of n_train × nrhs (row-major, ld nrhs), block g for gammas[g]
  *   Yhat    device f64, n_gamma blocks of n_test × nrhs (ld nrhs); may be NULL when n_test = 0
- *   ws      ≥ rf_ridge_workspace_size(n_train) bytes, 256-B aligned (the fp64 factor)
+ *   ws      ≥ rf_ridge_workspace_size(n_train) bytes, 256-B aligned (one fp64 factor and its diagonal-block
+ *           inverses); a workspace of 256 + k·(rf_ridge_workspace_size(n_train) − 256) bytes lets k ≤ 16 γ values
+ *           be factored concurrently (one set of launches per batch)
  * Synchronous at the end (one event wait, through mapped host memory) to report the factorisation:
  * G_train + γI not positive definite (a non-positive pivot) → RF_E_NONFINITE. */
 rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes);

@@ -412,8 +412,10 @@ def rf_ridge(G, n_train: int, gammas, Y, n_test: Optional[int] = None, ws=None, 
     r = Y.shape[1]
     alpha = torch.empty((len(gam), int(n_train), r), dtype=torch.float64, device=G.device)
     Yhat = torch.empty((len(gam), max(n_test, 0), r), dtype=torch.float64, device=G.device)
-    if ws is None:
-        ws = torch.empty(rf_ridge_workspace_size(n_train), dtype=torch.uint8, device=G.device)
+    if ws is None:   # room to factor up to 16 γ at once, within ≈ 2 GB (include/rf.h rf_ridge)
+        one = rf_ridge_workspace_size(n_train)
+        k = max(1, min(len(gam), 16, (2 << 30) // (one - 256)))
+        ws = torch.empty(256 + k * (one - 256), dtype=torch.uint8, device=G.device)
     garr = (ctypes.c_double * len(gam))(*gam)
     _lib.check(load().rf_ridge(ctypes.c_void_p(G.data_ptr()), G.stride(0), int(n_train), n_test, garr, len(gam),
                                ctypes.c_void_p(Y.data_ptr()), Y.stride(0), r, ctypes.c_void_p(alpha.data_ptr()),

@@ -287,12 +287,13 @@ rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b
 
 template <typename T, class Epi>
 rf_status launch_simt(const char* name, const T* A, int64_t lda, const T* B, int64_t ldb, int64_t M, int64_t N,
-                      int64_t K, int tri, int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st) {
+                      int64_t K, int tri, int row_tile0, int row_tile1, const Epi& epi, cudaStream_t st, int zcount = 1,
+                      int64_t zsA = 0, int64_t zsB = 0) {
   const int tn = (int)((N + rfk::kSimtTile - 1) / rfk::kSimtTile);
   if (row_tile1 <= row_tile0 || tn == 0) return RF_OK;
   ProfScope ps(name, st);
-  dim3 grid(tn, row_tile1 - row_tile0);
-  rfk::simt_gemm_nt<T, Epi><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, tri, row_tile0, epi);
+  dim3 grid(tn, row_tile1 - row_tile0, zcount);
+  rfk::simt_gemm_nt<T, Epi><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, tri, row_tile0, epi, zsA, zsB);
   RF_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
   return RF_OK;
@@ -1880,11 +1881,16 @@ int64_t ridge_lda(int64_t n) { return (n + 7) / 8 * 8; }
 
 extern "C" {
 
+// Workspace: [status word, 256 B][per γ of a batch: the fp64 factor (n × lda) | the diagonal-block inverses].
+static size_t ridge_per_gamma(int64_t n) {
+  const size_t nblk = (size_t)((n + rfk::kRB - 1) / rfk::kRB);
+  return align256((size_t)n * ridge_lda(n) * 8) + align256(nblk * rfk::kRB * rfk::kRB * 8);
+}
+
 rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes) {
   if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
   if (n_train <= 0 || n_train > ((int64_t)1 << 31)) return fail(RF_E_INVALID, "rf_ridge: n_train must be in (0, 2^31]");
-  const size_t nblk = (size_t)((n_train + rfk::kRB - 1) / rfk::kRB);
-  *bytes = align256((size_t)n_train * ridge_lda(n_train) * 8) + 256 + nblk * rfk::kRB * rfk::kRB * 8;
+  *bytes = 256 + ridge_per_gamma(n_train);
   return ok();
 }
 
@@ -1913,9 +1919,12 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
   if ((s = check_device(&dev))) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = n_train, lda = ridge_lda(n);
-  double* A = (double*)ws;
-  int* info = (int*)((char*)ws + align256((size_t)n * lda * 8));
-  double* Linv = (double*)((char*)ws + align256((size_t)n * lda * 8) + 256);   // 64×64 inverse per diagonal block
+  const size_t per = ridge_per_gamma(n);
+  const int batch = (int)std::min<size_t>({(size_t)n_gamma, (size_t)rfk::kMaxBatch, (ws_bytes - 256) / per});
+  int* info = (int*)ws;
+  double* A = (double*)((char*)ws + 256);                                   // factor of batch member z at A + z·sA
+  const int64_t sA = (int64_t)(per / 8);
+  double* Linv = A + align256((size_t)n * lda * 8) / 8;                     // inverses of member z at Linv + z·sA
   RF_CUDA_CHECK(cudaMemsetAsync(info, 0, sizeof(int), st));
   RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, rfk::kPanelSmem));
   RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, rfk::kDiagSmem));
@@ -1925,41 +1934,52 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
     ++g_launches;
     return RF_OK;
   };
-  for (int g = 0; g < n_gamma; ++g) {
-    double* al = alpha + (int64_t)g * n * nrhs;
+  for (int g0 = 0; g0 < n_gamma; g0 += batch) {
+    const int nz = std::min(batch, n_gamma - g0);
+    rfk::RidgeBatch bt{};
+    for (int z = 0; z < nz; ++z) bt.gamma[z] = gammas[g0 + z];
+    bt.sA = sA;
+    bt.sL = sA;
+    bt.sY = n * nrhs;
+    bt.sYh = n_test * nrhs;
+    double* al = alpha + (int64_t)g0 * n * nrhs;
     {
       ProfScope ps("KR_build", st);
       const unsigned nt = (unsigned)((n + 31) / 32);
-      rfk::k_ridge_build<<<dim3(nt, nt), 256, 0, st>>>(G, ldg, n, gammas[g], A, lda);
+      rfk::k_ridge_build<<<dim3(nt, nt, nz), 256, 0, st>>>(G, ldg, n, bt, A, lda);
     }
     if ((s = check())) return s;
     for (int k = 0; k < nblk; ++k) {
       {
         ProfScope ps("KR_chol_diag", st);
-        rfk::k_chol_diag<<<1, 256, rfk::kDiagSmem, st>>>(A, lda, n, k, info, Linv + (int64_t)k * rfk::kRB * rfk::kRB);
+        rfk::k_chol_diag<<<dim3(1, 1, nz), 256, rfk::kDiagSmem, st>>>(A, lda, n, k, info,
+                                                                     Linv + (int64_t)k * rfk::kRB * rfk::kRB, bt);
       }
       if ((s = check())) return s;
       const int64_t r0 = (int64_t)k * rfk::kRB, r1 = r0 + rfk::kRB, m = n - r1;
       if (m <= 0) continue;
       {
         ProfScope ps("KR_chol_panel", st);
-        rfk::k_chol_panel<<<(unsigned)((m + rfk::kRB - 1) / rfk::kRB), rfk::kRB, rfk::kPanelSmem, st>>>(A, lda, n, k);
+        rfk::k_chol_panel<<<dim3((unsigned)((m + rfk::kRB - 1) / rfk::kRB), 1, nz), rfk::kRB, rfk::kPanelSmem, st>>>(
+            A, lda, n, k, sA);
       }
       if ((s = check())) return s;
       const double* Pn = A + r1 * lda + r0;                  // panel rows r1.., columns r0 .. r0 + 64
       if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, m, rfk::kRB, 2, 0,
                                    (int)((m + rfk::kSimtTile - 1) / rfk::kSimtTile),
-                                   rfk::SimtCholUpd{A, lda, r1, m}, st)))
+                                   rfk::SimtCholUpd{A, lda, r1, m, sA}, st, nz, sA, sA)))
         return s;
     }
-    // α = L^{-T} L^{-1} Y, in place in alpha (row-major n × nrhs)
-    RF_CUDA_CHECK(cudaMemcpy2DAsync(al, (size_t)nrhs * 8, Y, (size_t)ldy * 8, (size_t)nrhs * 8, (size_t)n,
-                                    cudaMemcpyDeviceToDevice, st));
+    // α = L^{-T} L^{-1} Y, in place in alpha (row-major n × nrhs per γ)
+    for (int z = 0; z < nz; ++z)
+      RF_CUDA_CHECK(cudaMemcpy2DAsync(al + (int64_t)z * n * nrhs, (size_t)nrhs * 8, Y, (size_t)ldy * 8,
+                                      (size_t)nrhs * 8, (size_t)n, cudaMemcpyDeviceToDevice, st));
     const unsigned rw = (unsigned)((nrhs + 3) / 4);   // 4 right-hand sides per CTA of the block solves
     for (int k = 0; k < nblk; ++k) {
       {
         ProfScope ps("KR_trsv", st);
-        rfk::k_trsv_fwd<<<rw, 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs, nrhs);
+        rfk::k_trsv_fwd<<<dim3(rw, 1, nz), 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs,
+                                                         nrhs, bt);
       }
       if ((s = check())) return s;
       const int64_t below = n - (int64_t)(k + 1) * rfk::kRB;
@@ -1967,7 +1987,7 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
         {
           ProfScope ps("KR_gemv", st);
           const unsigned gb = (unsigned)std::min<int64_t>((below + 7) / 8, (int64_t)dev.sms * 8);
-          rfk::k_gemv_fwd<<<gb, 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+          rfk::k_gemv_fwd<<<dim3(gb, 1, nz), 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs, bt);
         }
         if ((s = check())) return s;
       }
@@ -1975,7 +1995,8 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
     for (int k = nblk - 1; k >= 0; --k) {
       {
         ProfScope ps("KR_trsv", st);
-        rfk::k_trsv_bwd<<<rw, 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs, nrhs);
+        rfk::k_trsv_bwd<<<dim3(rw, 1, nz), 256, 0, st>>>(Linv + (int64_t)k * rfk::kRB * rfk::kRB, n, k, al, nrhs,
+                                                         nrhs, bt);
       }
       if ((s = check())) return s;
       const int64_t r0 = (int64_t)k * rfk::kRB;
@@ -1983,7 +2004,7 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
         {
           ProfScope ps("KR_gemv", st);
           const unsigned gb = (unsigned)std::min<int64_t>((r0 + 255) / 256, (int64_t)dev.sms * 4);
-          rfk::k_axpy_bwd<<<gb, 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs);
+          rfk::k_axpy_bwd<<<dim3(gb, 1, nz), 256, 0, st>>>(A, lda, n, k, al, nrhs, nrhs, bt);
         }
         if ((s = check())) return s;
       }
@@ -1992,8 +2013,8 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
       {
         ProfScope ps("KR_predict", st);
         const unsigned gb = (unsigned)std::min<int64_t>((n_test + 127) / 128, (int64_t)dev.sms * 8);
-        rfk::k_ridge_predict<<<gb, 128, 0, st>>>(G, ldg, n_train, n_test, al, nrhs, nrhs,
-                                                 Yhat + (int64_t)g * n_test * nrhs, nrhs);
+        rfk::k_ridge_predict<<<dim3(gb, 1, nz), 128, 0, st>>>(G, ldg, n_train, n_test, al, nrhs, nrhs,
+                                                               Yhat + (int64_t)g0 * n_test * nrhs, nrhs, bt);
       }
       if ((s = check())) return s;
     }

@@ -15,10 +15,17 @@
 namespace rfk {
 
 constexpr int kRB = 64;
+constexpr int kMaxBatch = 16;   // γ values factored concurrently (blockIdx.z)
+struct RidgeBatch {
+  double gamma[kMaxBatch];
+  int64_t sA, sL, sY, sYh;      // per-z strides of the factor, the inverses, α and Ŷ (elements)
+};
 
 __global__ void __launch_bounds__(256) k_ridge_build(const float* __restrict__ G, int64_t ldg, int64_t n,
-                                                     double gamma, double* __restrict__ A, int64_t lda) {
+                                                     RidgeBatch bt, double* __restrict__ A, int64_t lda) {
   __shared__ float t[32][33];
+  A += blockIdx.z * bt.sA;
+  const double gamma = bt.gamma[blockIdx.z];
   const int64_t bi = blockIdx.y, bj = blockIdx.x;          // A block (bi, bj), bj ≤ bi (lower)
   if (bj > bi) return;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 × 8
@@ -44,8 +51,10 @@ __global__ void __launch_bounds__(256) k_ridge_build(const float* __restrict__ G
 // info: first non-positive pivot (1-based).  Dynamic shared memory: kDiagSmem.
 constexpr int kDiagSmem = 2 * kRB * (kRB + 1) * 8;
 __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64_t lda, int64_t n, int k,
-                                                   int* __restrict__ info, double* __restrict__ Linv) {
+                                                   int* __restrict__ info, double* __restrict__ Linv, RidgeBatch bt) {
   extern __shared__ double diag_smem[];
+  A += blockIdx.z * bt.sA;
+  Linv += blockIdx.z * bt.sL;
   double(*a)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(diag_smem);
   double(*x)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(diag_smem + kRB * (kRB + 1));
   const int64_t r0 = (int64_t)k * kRB;
@@ -91,8 +100,10 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64
 
 // Row block b (rows 64(k + 1 + b) ..) of panel k: X·L_kkᵀ = A_ik, one thread per row, forward over the columns.
 constexpr int kPanelSmem = 2 * kRB * (kRB + 1) * 8;     // dynamic shared memory of k_chol_panel (66.5 KB)
-__global__ void __launch_bounds__(kRB) k_chol_panel(double* __restrict__ A, int64_t lda, int64_t n, int k) {
+__global__ void __launch_bounds__(kRB) k_chol_panel(double* __restrict__ A, int64_t lda, int64_t n, int k,
+                                                    int64_t sA) {
   extern __shared__ double panel_smem[];
+  A += blockIdx.z * sA;
   double(*L)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(panel_smem);
   double(*X)[kRB + 1] = reinterpret_cast<double(*)[kRB + 1]>(panel_smem + kRB * (kRB + 1));
   const int64_t r0 = (int64_t)k * kRB, rb = r0 + kRB * (1 + (int64_t)blockIdx.x);
@@ -115,6 +126,7 @@ __global__ void __launch_bounds__(kRB) k_chol_panel(double* __restrict__ A, int6
 struct SimtCholUpd {
   double* A;
   int64_t lda, r1, m;
+  int64_t zstride;      // batched launches: factor z at A + z·zstride
   __device__ __forceinline__ void operator()(int64_t i, int64_t j, double v) const {
     if (i < m && j <= i) A[(r1 + i) * lda + r1 + j] -= v;
   }
@@ -123,8 +135,10 @@ struct SimtCholUpd {
 // Forward solve of block k: z_k = L_kk^{-1} y_k as a triangular product with the inverse from k_chol_diag (one
 // thread per (row, right-hand side)).
 __global__ void __launch_bounds__(256) k_trsv_fwd(const double* __restrict__ Linv, int64_t n, int k,
-                                                  double* __restrict__ Y, int64_t ldy, int nrhs) {
+                                                  double* __restrict__ Y, int64_t ldy, int nrhs, RidgeBatch bt) {
   __shared__ double y[4][kRB];
+  Linv += blockIdx.z * bt.sL;
+  Y += blockIdx.z * bt.sY;
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
   const int r = threadIdx.x & (kRB - 1), w = threadIdx.x >> 6, rhs = blockIdx.x * 4 + w;
@@ -138,7 +152,9 @@ __global__ void __launch_bounds__(256) k_trsv_fwd(const double* __restrict__ Lin
 
 // y_i −= L[i][64k .. 64k+64)·z_k for the rows below block k (one warp per row).
 __global__ void k_gemv_fwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
-                           int64_t ldy, int nrhs) {
+                           int64_t ldy, int nrhs, RidgeBatch bt) {
+  A += blockIdx.z * bt.sA;
+  Y += blockIdx.z * bt.sY;
   const int lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)k * kRB;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -154,8 +170,10 @@ __global__ void k_gemv_fwd(const double* __restrict__ A, int64_t lda, int64_t n,
 
 // Backward solve of block k: α_k = L_kk^{-T} z_k (the transpose of the inverse from k_chol_diag).
 __global__ void __launch_bounds__(256) k_trsv_bwd(const double* __restrict__ Linv, int64_t n, int k,
-                                                  double* __restrict__ Y, int64_t ldy, int nrhs) {
+                                                  double* __restrict__ Y, int64_t ldy, int nrhs, RidgeBatch bt) {
   __shared__ double y[4][kRB];
+  Linv += blockIdx.z * bt.sL;
+  Y += blockIdx.z * bt.sY;
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
   const int r = threadIdx.x & (kRB - 1), w = threadIdx.x >> 6, rhs = blockIdx.x * 4 + w;
@@ -169,7 +187,9 @@ __global__ void __launch_bounds__(256) k_trsv_bwd(const double* __restrict__ Lin
 
 // z_j −= Σ_{t < nb} L[64k + t][j]·α[64k + t] for the rows j above block k (one thread per j, coalesced along j).
 __global__ void k_axpy_bwd(const double* __restrict__ A, int64_t lda, int64_t n, int k, double* __restrict__ Y,
-                           int64_t ldy, int nrhs) {
+                           int64_t ldy, int nrhs, RidgeBatch bt) {
+  A += blockIdx.z * bt.sA;
+  Y += blockIdx.z * bt.sY;
   const int64_t r0 = (int64_t)k * kRB;
   const int nb = (int)(n - r0 < kRB ? n - r0 : kRB);
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < r0; j += (int64_t)gridDim.x * blockDim.x) {
@@ -185,7 +205,9 @@ __global__ void k_axpy_bwd(const double* __restrict__ A, int64_t lda, int64_t n,
 // samples), one thread per test sample, coalesced along t.
 __global__ void k_ridge_predict(const float* __restrict__ G, int64_t ldg, int64_t n_train, int64_t n_test,
                                 const double* __restrict__ alpha, int64_t lda_, int nrhs, double* __restrict__ Yhat,
-                                int64_t ldyh) {
+                                int64_t ldyh, RidgeBatch bt) {
+  alpha += blockIdx.z * bt.sY;
+  Yhat += blockIdx.z * bt.sYh;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_test; t += (int64_t)gridDim.x * blockDim.x) {
     for (int h = 0; h < nrhs; ++h) {
       double s = 0.0;

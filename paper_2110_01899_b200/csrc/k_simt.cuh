@@ -58,10 +58,21 @@ struct SimtEq1 {
 // k give 64 FMAs), next slice prefetched into registers with 16-B global loads while the current one is consumed.
 // Rows are 16-B aligned (ld·sizeof(T) a multiple of 16 B, validated at the ABI); the K tail is zero-filled.
 constexpr int kSimtTile = 128;
+// Batched launches (gridDim.z > 1): operands advance by zsA / zsB elements per z, and an epilogue with a `zstride`
+// member advances its output the same way (rf_ridge factors several γ at once).
+template <class E, class = void>
+struct has_zstride : std::false_type {};
+template <class E>
+struct has_zstride<E, std::void_t<decltype(E::zstride)>> : std::true_type {};
 template <typename T, class Epi>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1) simt_gemm_nt(const T* __restrict__ A, int64_t lda, const T* __restrict__ B,
                                                     int64_t ldb, int64_t M, int64_t N, int64_t K, int tri,
-                                                    int row_tile0, Epi epi) {
+                                                    int row_tile0, Epi epi, int64_t zsA = 0, int64_t zsB = 0) {
+  if (blockIdx.z) {
+    A += blockIdx.z * zsA;
+    B += blockIdx.z * zsB;
+    if constexpr (has_zstride<Epi>::value) epi.A += blockIdx.z * epi.zstride;
+  }
   constexpr int BM = kSimtTile, BN = kSimtTile, BK = 16, PAD = 4;
   constexpr int VEC = 16 / (int)sizeof(T);                 // elements per 16-B vector
   constexpr int NV = BM * BK / VEC / 256;                  // vectors per thread per operand per slice

@@ -20,12 +20,12 @@ for n_tr, n_te, gam in [(1024, 512, [1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3, 1e4]), (16
     G = rf.rf_gram(Xd, Wd, act="relu", prec="bf16", out="upper")
     Y = torch.from_numpy(y[:n_tr]).to(dev)
     ws = torch.empty(rf.rf_ridge_workspace_size(n_tr), dtype=torch.uint8, device=dev)
-    rf.rf_ridge(G, n_tr, gam, Y, n_test=n_te, ws=ws)
+    rf.rf_ridge(G, n_tr, gam, Y, n_test=n_te)
     torch.cuda.synchronize()
     rf.rf_profile_read()
     rf.rf_profile_enable(True)
     t0 = time.perf_counter()
-    rf.rf_ridge(G, n_tr, gam, Y, n_test=n_te, ws=ws)
+    rf.rf_ridge(G, n_tr, gam, Y, n_test=n_te)
     torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) * 1e3
     rf.rf_profile_enable(False)
