@@ -224,3 +224,4 @@ __global__ void k_publish_u32(const int* __restrict__ src, volatile int* dst) {
 }
 
 }  // namespace rfk
+
