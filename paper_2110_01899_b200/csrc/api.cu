@@ -1949,6 +1949,9 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
       rfk::k_ridge_build<<<dim3(nt, nt, nz), 256, 0, st>>>(G, ldg, n, bt, A, lda);
     }
     if ((s = check())) return s;
+    // two-level blocking: 64-column sub-panels inside 256-wide panels; the sub-panel updates stay inside the
+    // panel, and one K = 256 update per panel carries the trailing matrix (4× the arithmetic per byte of C)
+    constexpr int kOuter = 4 * rfk::kRB;
     for (int k = 0; k < nblk; ++k) {
       {
         ProfScope ps("KR_chol_diag", st);
@@ -1964,11 +1967,22 @@ rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test,
             A, lda, n, k, sA);
       }
       if ((s = check())) return s;
-      const double* Pn = A + r1 * lda + r0;                  // panel rows r1.., columns r0 .. r0 + 64
-      if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, m, rfk::kRB, 2, 0,
-                                   (int)((m + rfk::kSimtTile - 1) / rfk::kSimtTile),
-                                   rfk::SimtCholUpd{A, lda, r1, m, sA}, st, nz, sA, sA)))
-        return s;
+      const int64_t c0 = r0 / kOuter * kOuter, c1 = std::min<int64_t>(c0 + kOuter, n);   // this 256-wide panel
+      const double* Pn = A + r1 * lda + r0;                  // sub-panel rows r1.., columns r0 .. r0 + 64
+      if (r1 < c1) {   // inside the panel: columns r1 .. c1
+        if ((s = launch_simt<double>("KR_chol_update", Pn, lda, Pn, lda, m, c1 - r1, rfk::kRB, 2, 0,
+                                     (int)((m + rfk::kSimtTile - 1) / rfk::kSimtTile),
+                                     rfk::SimtCholUpd{A, lda, r1, m, sA, c1 - r1}, st, nz, sA, sA)))
+          return s;
+      }
+      if (r1 == c1 && c1 < n) {   // panel done: the trailing matrix from columns c0 .. c1 (K = 256)
+        const int64_t mt = n - c1;
+        const double* Po = A + c1 * lda + c0;
+        if ((s = launch_simt<double>("KR_chol_update", Po, lda, Po, lda, mt, mt, c1 - c0, 2, 0,
+                                     (int)((mt + rfk::kSimtTile - 1) / rfk::kSimtTile),
+                                     rfk::SimtCholUpd{A, lda, c1, mt, sA, mt}, st, nz, sA, sA)))
+          return s;
+      }
     }
     // α = L^{-T} L^{-1} Y, in place in alpha (row-major n × nrhs per γ)
     for (int z = 0; z < nz; ++z)

@@ -127,8 +127,9 @@ struct SimtCholUpd {
   double* A;
   int64_t lda, r1, m;
   int64_t zstride;      // batched launches: factor z at A + z·zstride
+  int64_t ncols;        // columns j < ncols only (the sub-panel updates stay inside their 256-wide panel)
   __device__ __forceinline__ void operator()(int64_t i, int64_t j, double v) const {
-    if (i < m && j <= i) A[(r1 + i) * lda + r1 + j] -= v;
+    if (i < m && j < ncols && j <= i) A[(r1 + i) * lda + r1 + j] -= v;
   }
 };
 
