@@ -64,14 +64,17 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64
     for (int c = tx; c < kRB; c += 16)
       a[r][c] = (r < nb && c <= r) ? A[(r0 + r) * lda + r0 + c] : (r == c ? 1.0 : 0.0);
   __syncthreads();
+  __shared__ double pinv;
   for (int c = 0; c < nb; ++c) {
-    const double d = a[c][c];                   // every thread: the pivot (no extra barrier)
-    const double sd = sqrt(d), inv = 1.0 / sd;
-    __syncthreads();                            // all threads have read the pivot
-    if (tid == 0) {
+    if (tid == 0) {                             // one fp64 sqrt and division per column, broadcast through smem
+      const double d = a[c][c];
       if (!(d > 0.0) && *info == 0) *info = (int)(r0 + c + 1);
+      const double sd = sqrt(d);
       a[c][c] = sd;
+      pinv = 1.0 / sd;
     }
+    __syncthreads();
+    const double inv = pinv;
     for (int r = c + 1 + tid; r < nb; r += 256) a[r][c] *= inv;
     __syncthreads();
     for (int r = c + 1 + ty; r < nb; r += 16)
@@ -80,17 +83,17 @@ __global__ void __launch_bounds__(256) k_chol_diag(double* __restrict__ A, int64
   }
   for (int r = ty; r < nb; r += 16)
     for (int c = tx; c <= r; c += 16) A[(r0 + r) * lda + r0 + c] = a[r][c];
-  // L^{-1}: column j = L^{-1} e_j (rows ≥ j), padded rows/columns (≥ nb) of the identity
-  if (tid < kRB) {
-    const int j = tid;
-    for (int r = 0; r < kRB; ++r) {
-      if (r < j) {
-        x[r][j] = 0.0;
-        continue;
-      }
-      double sum = r == j ? 1.0 : 0.0;
-      for (int t = j; t < r; ++t) sum -= a[r][t] * x[t][j];
-      x[r][j] = sum / a[r][r];
+  // L^{-1}: column j = L^{-1} e_j (rows ≥ j), padded rows/columns (≥ nb) of the identity.  Four threads per column
+  // split each row's inner product (t ≡ q mod 4) and combine it with two shuffles.
+  {
+    const int j = tid >> 2, q = tid & 3;
+    for (int r = 0; r < kRB; ++r) {   // every lane takes every step (the shuffles need the whole warp)
+      double sum = 0.0;
+      for (int t = j + q; t < r; t += 4) sum += a[r][t] * x[t][j];
+      sum += __shfl_xor_sync(0xFFFFFFFFu, sum, 1);
+      sum += __shfl_xor_sync(0xFFFFFFFFu, sum, 2);
+      if (q == 0) x[r][j] = r < j ? 0.0 : ((r == j ? 1.0 : 0.0) - sum) / a[r][r];
+      __syncwarp();
     }
   }
   __syncthreads();
