@@ -433,7 +433,7 @@ static cudaStream_t side_stream() {
 
 // How many 4-CTA clusters of kernel <Cm, Epi> can be co-resident (clusters must sit inside one GPC).
 template <class Cm, class Epi>
-rf_status max_clusters4(int sms, int* mcl) {
+rf_status max_clusters(int sms, int* mcl) {
   *mcl = 0;
   auto kern = rfk::tc_gemm_kernel<Cm, Epi>;
   RF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cm::SMEM_BYTES));
@@ -443,7 +443,7 @@ rf_status max_clusters4(int sms, int* mcl) {
   cfg.gridDim = dim3(sms);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.x = Cm::CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -461,7 +461,8 @@ rf_status max_clusters4(int sms, int* mcl) {
 template <class Cm, class Cp, class Epi>
 rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tBm,
                              const CUtensorMap& tBp, const CUtensorMap& tO, const rfk::Sched& sm, const rfk::Sched& sp,
-                             const Epi& e, uint32_t* flag, int mc_sms, int tail_sms, cudaStream_t st) {
+                             const Epi& e, uint32_t* flag, int mc_sms, int tail_sms, cudaStream_t st,
+                             const CUtensorMap* tAm = nullptr) {
   PFN_wait32h wfn = wait32_h();
   cudaStream_t st2 = side_stream();
   rf_status s;
@@ -473,7 +474,7 @@ rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUte
   RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
   RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
   RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // inputs ready and the progress words / start flag zeroed
-  if ((s = launch_tc<Cm>(nm_mc, tA, tB, tA, tBm, tO, sm, e, mc_sms, st))) return s;
+  if ((s = launch_tc<Cm>(nm_mc, tA, tB, tAm ? *tAm : tA, tBm, tO, sm, e, mc_sms, st))) return s;
   // the pair kernel: on the side stream, after ev0 and once the multicast kernel has started
   RF_CUDA_CHECK(cudaStreamWaitEvent(st2, ev0, 0));
   CUresult r = wfn((CUstream)st2, (CUdeviceptr)(uintptr_t)flag, 1u, CU_STREAM_WAIT_VALUE_GEQ);
@@ -486,24 +487,24 @@ rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUte
   return s;
 }
 
-template <int kFmt, class Epi>
-rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtensorMap& tO, int64_t n, int kb,
-                           const Epi& e, uint32_t* prog, int lockw, int lockks, int sms, cudaStream_t st,
-                           bool* used) {
+template <int kFmt, int kMcCl, class Epi>
+rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUtensorMap& tSh, const CUtensorMap& tO,
+                              int64_t n, int kb, const Epi& e, uint32_t* prog, int lockw, int lockks, int sms,
+                              cudaStream_t st, bool* used) {
   *used = false;
   const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512);
   if (env_int("RF_K4_HYBRID", 1) == 0 || T < 64 || !wait32_h() || !side_stream()) return RF_OK;
-  using Cm = rfk::TcCfg<kFmt, 1, 512, -1, 4>;
+  using Cm = rfk::TcCfg<kFmt, 1, 512, -1, kMcCl>;
   using Cp = rfk::TcCfg<kFmt, 1, 512>;
   int mcl = 0;
   rf_status s;
-  if ((s = max_clusters4<Cm, Epi>(sms, &mcl))) return s;
-  const int left = sms - 4 * mcl;
+  if ((s = max_clusters<Cm, Epi>(sms, &mcl))) return s;
+  const int left = sms - kMcCl * mcl;
   if (mcl <= 0 || left < 2) return RF_OK;
   // work share of the multicast kernel from the per-SM rate ratio r (measured ≈ 1.11: less L2 traffic per flop
   // buys clock under the power cap for bf16 and bandwidth for fp8); env RF_HYB_FPCT overrides
   const double rate = env_int("RF_HYB_R100", 111) / 100.0;
-  double f = (4.0 * mcl * rate) / (4.0 * mcl * rate + (left & ~1));
+  double f = ((double)kMcCl * mcl * rate) / ((double)kMcCl * mcl * rate + (left & ~1));
   if (env_int("RF_HYB_FPCT", 0) > 0) f = std::min(1.0, env_int("RF_HYB_FPCT", 0) / 100.0);
   double total = 0;
   for (int I = 0; I < T; ++I) total += T2 - I / 2;
@@ -515,7 +516,9 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
   }
   if (2 * S1 >= T) return RF_OK;
   RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
-  rfk::Sched sm = rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
+  // multicast kernel: super rows of 512; CL 4 walks 512-wide column tiles, CL 8 1024-wide super columns
+  rfk::Sched sm = kMcCl == 8 ? rfk::Sched::make(1, 512, 0, S1, (int)((n + 1023) / 1024), kb, 0, raster_gm(4, 4))
+                             : rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
   // tail raster: with 8 pair clusters in flight, groups of 4 row tiles × 2 column tiles re-read the fewest Σᵀ panels
   // (4·32 + 2·64 MB per 8 tiles vs 8·32 + 64 for groups of 8); measured ≈ 0.8 % on the whole K4 (scripts/gpu_tailgm.sh)
   rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, env_int("RF_TAIL_GM", 4));
@@ -526,9 +529,20 @@ rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtens
     sm.lock_ks = sp.lock_ks = lockks;
   }
   sm.started = prog + 255;
-  if ((s = launch_hybrid_pair<Cm, Cp>(name, tS, tS, tS, tS, tO, sm, sp, e, prog + 255, sms, left & ~1, st))) return s;
+  if ((s = launch_hybrid_pair<Cm, Cp>(name, tS, tS, tS, tS, tO, sm, sp, e, prog + 255, sms, left & ~1, st, &tSh)))
+    return s;
   *used = true;
   return RF_OK;
+}
+
+// Hybrid K4 with 4-CTA (B shared) or, RF_K4_CL8=1, 8-CTA clusters (2 × 2 pairs sharing both A and B).
+template <int kFmt, class Epi>
+rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtensorMap& tSh, const CUtensorMap& tO,
+                           int64_t n, int kb, const Epi& e, uint32_t* prog, int lockw, int lockks, int sms,
+                           cudaStream_t st, bool* used) {
+  if (env_int("RF_K4_CL8", 0))
+    return launch_k4_hybrid_cl<kFmt, 8>(name, tS, tSh, tO, n, kb, e, prog, lockw, lockks, sms, st, used);
+  return launch_k4_hybrid_cl<kFmt, 4>(name, tS, tSh, tO, n, kb, e, prog, lockw, lockks, sms, st, used);
 }
 
 // Hybrid K3 (bf16 / tf32 GEMM + σ, 256×256 pair tiles, rectangular): 4-CTA clusters that share each B tile (two
@@ -545,7 +559,7 @@ rf_status launch_k3_hybrid(const char* name, const CUtensorMap& tA, const CUtens
   if (env_int("RF_K3_HYBRID", 1) == 0 || T < 32 || !wait32_h() || !side_stream()) return RF_OK;
   int mcl = 0;
   rf_status s;
-  if ((s = max_clusters4<Cm, Epi>(sms, &mcl))) return s;
+  if ((s = max_clusters<Cm, Epi>(sms, &mcl))) return s;
   const int left = sms - 4 * mcl;
   if (mcl <= 0 || left < 2) return RF_OK;
   const double rate = env_int("RF_HYB3_R100", 120) / 100.0;   // per-SM rate, multicast vs pair kernel
@@ -650,7 +664,9 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   if (!g.pack && lockw > 0 && env_int("RF_K4_MC", 0) == 0) {
     rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
     bool used = false;
-    if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
+    CUtensorMap tSh;   // Σᵀ with a 64-row box (the 8-CTA multicast kernel's A halves)
+    if ((s = make_tmap(&tSh, S0, bf, g.n, g.m_local, g.pl.ldS, 64))) return s;
+    if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tSh, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
                                      &used)))
       return s;
     if (used) return ok();
@@ -1392,9 +1408,13 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
   }
   rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0, tri_T};
   bool hyb = false;
-  if (lockw > 0 && env_int("RF_K4TER_MC", 0) == 0)
-    if ((s = launch_k4_hybrid<3>("K4_ter_syrk", tA, tO, n, kb4, e4, s4.prog, lockw, s4.lock_ks, dev.sms, st, &hyb)))
+  if (lockw > 0 && env_int("RF_K4TER_MC", 0) == 0) {
+    CUtensorMap tSh;   // Σ^terᵀ with a 64-row box (the 8-CTA multicast kernel's A halves)
+    if ((s = make_tmap_es(&tSh, S, 1, n, m_local, pl.ldS, 64))) return s;
+    if ((s = launch_k4_hybrid<3>("K4_ter_syrk", tA, tSh, tO, n, kb4, e4, s4.prog, lockw, s4.lock_ks, dev.sms, st,
+                                 &hyb)))
       return s;
+  }
   if (hyb) {
   } else if (env_int("RF_K4TER_MC", 0)) {
     // 4-CTA clusters, B multicast (DESIGN.md §6 finding 3): the fp8 SYRK runs at full clock and is L2-bound,

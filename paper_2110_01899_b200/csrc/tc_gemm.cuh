@@ -49,7 +49,8 @@ template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)
           int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8>
 struct TcCfg {
   static constexpr int CL = kCl;
-  static_assert(kCl == 2 || (kCl == 4 && kSplit == 1), "4-CTA clusters: one operand split");
+  static_assert(kCl == 2 || (kCl == 4 && kSplit == 1) || (kCl == 8 && kSplit == 1 && kBN == 512),
+                "4-CTA clusters: one operand split; 8-CTA clusters: BN = 512");
   static constexpr int BM = 256, BN = kBN;      // pair tile
   static constexpr int NSUB = kBN / 256;        // N=256 MMAs per K-step
   static constexpr int ESZ = kFmt == 1 ? 2 : (kFmt == 3 ? 1 : 4);
@@ -756,13 +757,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (NOPS == 2 || Cfg::CL == 4) {
+    if (NOPS == 2 || Cfg::CL >= 4) {
       ptx::prefetch_tmap(&tmA_lo);
       ptx::prefetch_tmap(&tmB_lo);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], Cfg::CL / 2);         // released by the MMA commit of every pair reading it
+      // released by the MMA commit of every pair whose smem this CTA's loads fill: itself (CL 2), both pairs
+      // (CL 4), itself + its A partner + its B partner (CL 8)
+      ptx::mbar_init(&empty[s], Cfg::CL == 8 ? 3 : Cfg::CL / 2);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -788,6 +791,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     // so each destination's bytes are counted on its own pair leader's full barrier.
     const uint32_t full_rel0 = ptx::smem_u32(&full[0]) & 0xFEFFFFFFu;
     const uint16_t mc_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
+    // CL 8: pair pi = di + 2·dj computes row tile 2I + di, column tile 2J + dj; A (row tile) is shared with pair
+    // (di, 1 − dj), B (column tile) with pair (1 − di, dj)
+    const uint32_t di = pi & 1u, dj = pi >> 1;
+    const uint16_t mcA8 = (uint16_t)((1u << (2 * di + rank)) | (1u << (2 * (di + 2) + rank)));
+    const uint16_t mcB8 = (uint16_t)((1u << (2 * (2 * dj) + rank)) | (1u << (2 * (1 + 2 * dj) + rank)));
     int stage = 0;
     uint32_t phase = 0;
     uint32_t step = 0;
@@ -797,6 +805,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int ti, tj;
       cur.get(t, ti, tj);
       if (Cfg::CL == 4) ti = 2 * ti + (int)pi;       // the scheduler walks 512-row super tiles
+      if (Cfg::CL == 8) {                            // … and 1024-column super tiles
+        ti = 2 * ti + (int)di;
+        tj = 2 * tj + (int)dj;
+      }
       const int ra = ti * Cfg::BM + (int)rank * 128;
       const int rb = tj * Cfg::BN + (int)rank * 128;
       for (int c = 0; c < nchunks; ++c) {
@@ -821,8 +833,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             const int k = kb * Cfg::BK;
             uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
             uint8_t* b = sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES;
-            ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
-            if (Cfg::CL == 4 && NSUB == 2) {
+            if (Cfg::CL == 8) {
+              // A: the 64-row half dj of this CTA's 128 A rows (tmA_lo: 64-row box) to rank r of pairs (di, 0/1);
+              // B: sub-tile di of the column tile to rank r of pairs (0/1, dj)
+              ptx::tma_load_2d_cg2_mc(a + dj * (Cfg::A_BYTES / 2), &tmA_lo, full_rel0 + stage * 8, k, ra + 64 * (int)dj,
+                                      mcA8, pol);
+              ptx::tma_load_2d_cg2_mc(b + di * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)di, mcB8,
+                                      pol);
+            } else {
+              ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
+            }
+            if (Cfg::CL == 8) {
+            } else if (Cfg::CL == 4 && NSUB == 2) {
               ptx::tma_load_2d_cg2_mc(b + pi * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)pi, mc_mask,
                                       pol);
             } else if (Cfg::CL == 4) {
@@ -856,6 +878,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      uint16_t empty_mask = Cfg::CL == 4 ? 0xF : 0x3;
+      if (Cfg::CL == 8) {   // this pair, its A partner (di, 1 − dj) and its B partner (1 − di, dj)
+        const uint32_t di = pi & 1u, dj = pi >> 1;
+        const uint32_t pa = di + 2 * (1 - dj), pb = (1 - di) + 2 * dj;
+        empty_mask = (uint16_t)((0x3u << (2 * pi)) | (0x3u << (2 * pa)) | (0x3u << (2 * pb)));
+      }
       for (int t = cid; t < sched.num_tiles; t += ncl) {
         for (int c = 0; c < nchunks; ++c, ++it) {
           // K-chunked accumulation: every chunk goes to slot 0; the epilogue keeps the running fp32 sum in slot 1
@@ -896,7 +924,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                   }
                 }
               }
-              ptx::mma_commit_cg2_mc(&empty[stage], Cfg::CL == 4 ? 0xF : 0x3);   // every CTA that fed the stage
+              ptx::mma_commit_cg2_mc(&empty[stage], empty_mask);   // every CTA that fed the stage
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -928,6 +956,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int ti, tj;
       cur.get(t, ti, tj);
       if (Cfg::CL == 4) ti = 2 * ti + (int)pi;
+      if (Cfg::CL == 8) {
+        ti = 2 * ti + (int)(pi & 1u);
+        tj = 2 * tj + (int)(pi >> 1);
+      }
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
       const int64_t colb = (int64_t)tj * Cfg::BN + h * HALF;
       if (Cfg::ACC_SLOTS == 2 && Cfg::EPI_WARPS == 8 && nchunks > 1) {

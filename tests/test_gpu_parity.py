@@ -337,3 +337,19 @@ def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
     ref = oracle.gram(back(Xd.index_select(0, St)), back(Wd), act)
     I, J = upper_idx(len(S))
     assert report(f"G K3-multicast {act} {prec} n={n}", sub[I, J], ref[I, J], S[I], S[J]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("cl8", ["0", "1"])
+def test_k4_hybrid_bit_exact(cl8, monkeypatch):
+    """K4's multicast + pair hybrid (n ≥ 64 row tiles) — 4-CTA clusters sharing B, or (RF_K4_CL8=1) 8-CTA clusters
+    of 2 × 2 pairs sharing A and B — equals the pair-cluster kernel bit for bit (same accumulation order)."""
+    n, p, m = 16384 + 77, 64, 1024
+    rng = np.random.default_rng(5)
+    Xd = dev(rng.standard_normal((n, p)) / math.sqrt(p), "bf16")
+    Wd = dev(rng.standard_normal((m, p)), "bf16")
+    monkeypatch.setenv("RF_K4_CL8", cl8)
+    G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper")
+    monkeypatch.setenv("RF_K4_HYBRID", "0")
+    G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper")
+    torch.cuda.synchronize()
+    assert torch.equal(G1, G0)
