@@ -470,9 +470,16 @@ rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUte
   char nm_mc[32], nm_tail[32];
   std::snprintf(nm_mc, sizeof(nm_mc), "%s_mc", name);
   std::snprintf(nm_tail, sizeof(nm_tail), "%s_tail", name);
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+  struct Events {   // released on every return path
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~Events() {
+      for (cudaEvent_t x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evs;
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&evs.e[0], cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&evs.e[1], cudaEventDisableTiming));
+  cudaEvent_t ev0 = evs.e[0], ev1 = evs.e[1];
   RF_CUDA_CHECK(cudaEventRecord(ev0, st));   // inputs ready and the progress words / start flag zeroed
   if ((s = launch_tc<Cm>(nm_mc, tA, tB, tAm ? *tAm : tA, tBm, tO, sm, e, mc_sms, st))) return s;
   // the pair kernel: on the side stream, after ev0 and once the multicast kernel has started
@@ -482,8 +489,6 @@ rf_status launch_hybrid_pair(const char* name, const CUtensorMap& tA, const CUte
   s = launch_tc<Cp>(nm_tail, tA, tB, tA, tBp, tO, sp, e, tail_sms, st2);
   RF_CUDA_CHECK(cudaEventRecord(ev1, st2));
   RF_CUDA_CHECK(cudaStreamWaitEvent(st, ev1, 0));
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
   return s;
 }
 
