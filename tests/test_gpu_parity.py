@@ -339,17 +339,29 @@ def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
     assert report(f"G K3-multicast {act} {prec} n={n}", sub[I, J], ref[I, J], S[I], S[J]) <= TOL[prec]
 
 
-@pytest.mark.parametrize("cl8", ["0", "1"])
-def test_k4_hybrid_bit_exact(cl8, monkeypatch):
+@pytest.mark.parametrize("cl8,out", [("0", "upper"), ("1", "upper"), ("0", "full"), ("0", "packed_tri")])
+def test_k4_hybrid_bit_exact(cl8, out, monkeypatch):
     """K4's multicast + pair hybrid (n ≥ 64 row tiles) — 4-CTA clusters sharing B, or (RF_K4_CL8=1) 8-CTA clusters
-    of 2 × 2 pairs sharing A and B — equals the pair-cluster kernel bit for bit (same accumulation order)."""
+    of 2 × 2 pairs sharing A and B — equals the pair-cluster kernel bit for bit (same accumulation order), in the
+    dense, mirrored and packed-triangle layouts (the last is what the e2e leg reads back)."""
     n, p, m = 16384 + 77, 64, 1024
     rng = np.random.default_rng(5)
     Xd = dev(rng.standard_normal((n, p)) / math.sqrt(p), "bf16")
     Wd = dev(rng.standard_normal((m, p)), "bf16")
     monkeypatch.setenv("RF_K4_CL8", cl8)
-    G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper")
+    G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out=out)
     monkeypatch.setenv("RF_K4_HYBRID", "0")
-    G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper")
+    G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper" if out == "packed_tri" else out)
     torch.cuda.synchronize()
-    assert torch.equal(G1, G0)
+    if out == "packed_tri":   # the same entries through the packed offsets (include/rf.h), sampled rows
+        T = -(-n // 256)
+        S = synthetic.sample_indices(n, count=300, tile_stride=1024)
+        ii, jj = np.meshgrid(S, S, indexing="ij")
+        lo, hi = np.minimum(ii, jj), np.maximum(ii, jj)
+        It, Jt = lo // 256, hi // 256
+        off = 65536 * (It * T - It * (It - 1) // 2 + Jt - It) + (lo % 256) * 256 + (hi % 256)
+        got = G1[torch.tensor(off.ravel(), device="cuda")].reshape(len(S), len(S))
+        ref = G0[torch.tensor(lo.ravel(), device="cuda"), torch.tensor(hi.ravel(), device="cuda")].reshape(len(S), len(S))
+        assert torch.equal(got, ref)
+    else:
+        assert torch.equal(G1, G0)
