@@ -735,7 +735,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   constexpr int STAGES = Cfg::STAGES, NOPS = Cfg::NOPS, NSUB = Cfg::NSUB;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by an offset from the __shared__ array (not an integer round trip), so the compiler keeps the
+  // shared address space and the epilogue's staging stores compile to STS, not generic ST
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;                                                    // [STAGES][NOPS][A_BYTES]
   uint8_t* sB = sA + (size_t)STAGES * NOPS * Cfg::A_BYTES;               // [STAGES][NOPS][NSUB][B_BYTES]
   uint8_t* sStg = sB + (size_t)STAGES * NOPS * NSUB * Cfg::B_BYTES;      // [EPI_WARPS][STG_BUFS][4096]
