@@ -21,27 +21,43 @@ __global__ void __launch_bounds__(256) k_center_rowsum(const T* __restrict__ A, 
   __shared__ double colpart[8][kCT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = (int64_t)I * kCT, j0 = (int64_t)J * kCT;
+  // All 16 rows of this warp are loaded before any is reduced (16 independent loads in flight per lane); lane l
+  // holds columns j0 + 4l .. 4l + 3, read as one 16-B vector where the row allows it.
+  constexpr int R = kCT / 8;
+  T v[R][4];
+  const int64_t jl = j0 + 4 * lane;
+  const bool vec = sizeof(T) == 4 && (ld & 3) == 0 && jl + 4 <= n && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = i0 + warp + 8 * k;
+    if (i < n && vec) {
+      const float4 q = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A) + i * ld + jl);
+      v[k][0] = (T)q.x; v[k][1] = (T)q.y; v[k][2] = (T)q.z; v[k][3] = (T)q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[k][u] = (i < n && jl + u < n) ? A[i * ld + jl + u] : T(0);
+    }
+  }
   double cacc[4] = {0.0, 0.0, 0.0, 0.0};   // this lane's 4 columns, over this warp's rows
-  for (int rr = warp; rr < kCT; rr += 8) {
-    const int64_t i = i0 + rr;
-    if (i >= n) break;
-    const T* row = A + i * ld;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int64_t i = i0 + warp + 8 * k;
     double racc = 0.0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t j = j0 + lane + 32 * u;
-      if (j < n && j >= i) {
-        const double v = (double)row[j];
-        racc += v;
-        if (j > i) cacc[u] += v;             // mirror entry (j, i) belongs to row j
+      const int64_t j = jl + u;
+      if (i < n && j < n && j >= i) {
+        const double x = (double)v[k][u];
+        racc += x;
+        if (j > i) cacc[u] += x;             // mirror entry (j, i) belongs to row j
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, o);
-    if (lane == 0) atomicAdd(rsum + i, racc);
+    if (lane == 0 && i < n) atomicAdd(rsum + i, racc);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) colpart[warp][lane + 32 * u] = cacc[u];
+  for (int u = 0; u < 4; ++u) colpart[warp][4 * lane + u] = cacc[u];
   __syncthreads();
   if (threadIdx.x < kCT) {
     double s = 0.0;
