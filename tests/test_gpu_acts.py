@@ -85,3 +85,24 @@ def test_trf_thresholds_for_relu_matches_table2_targets():
     sm, sp = rf.rf_trf_thresholds_for("relu", tau)
     t = trf.ternary_moments(sm, sp, tau)
     assert abs(t["d1"] - 0.25) < 1e-10 and abs(t["d2"] - 1 / (8 * math.pi)) < 1e-10
+
+
+def test_phi_eq2_config4_full_size_sampled():
+    """configs[4] (n = 131072, p = 512): EQ2 through the 16-warp K5 epilogue, sampled principal submatrix (tile-boundary
+    rows included) against the oracle's EQ2 with the τ̂ of all rows."""
+    cfg = synthetic.CONFIGS[4]
+    X = synthetic.make_X(cfg)
+    Xd = torch.tensor(X, device="cuda").to(torch.bfloat16)
+    Phi = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec="bf16", out="upper", form=2)
+    torch.cuda.synchronize()
+    S = synthetic.sample_indices(cfg.n, count=768, tile_stride=2048)
+    St = torch.tensor(S, device="cuda")
+    sub = Phi.index_select(0, St).index_select(1, St).double().cpu().numpy()
+    del Phi
+    Xb = Xd.double().cpu().numpy()
+    tau = oracle.tau_hat(Xb)
+    ref = oracle.phi_eq2(Xb[S], cfg.act, tau=tau)
+    I, J = np.triu_indices(len(S))
+    e = _rel(sub[I, J], ref[I, J])
+    print(f"[parity] Φ EQ2 configs[4] sampled |S|={len(S)}: rel-Frobenius {e:.3e}")
+    assert e <= 1e-5
