@@ -536,6 +536,10 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
     sm.lock_ks = sp.lock_ks = lockks;
   }
   sm.started = prog + 255;
+  // evict_last on the operand loads keeps the Σᵀ panel slices of a wave in L2 a little longer: 196.6 → 195.0 ms
+  // over 6 interleaved pairs (5 of 6 faster; scripts/gpu_k4pol2.sh); evict_first on G's stores showed nothing
+  sm.load_pol = sp.load_pol = env_int("RF_K4_LOADPOL", 1);
+  sm.store_pol = sp.store_pol = env_int("RF_K4_STOREPOL", 0);
   if ((s = launch_hybrid_pair<Cm, Cp>(name, tS, tS, tS, tS, tO, sm, sp, e, prog + 255, sms, left & ~1, st, &tSh)))
     return s;
   *used = true;
