@@ -54,8 +54,9 @@ rf_status launch_k3_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, 
       return s;
     if (used) return RF_OK;
   }
-  const rfk::Sched sc =
+  rfk::Sched sc =
       rfk::Sched::make(0, 256, 0, (int)((n + 255) / 256), (int)((m_local + 255) / 256), kb, 0, raster_gm(8, 3));
+  sc.load_pol = env_int("RF_K3_LOADPOL", 1);
   return launch_tc<C3>("K3_ter_features", tA, tB, tA, tB, tA, sc, e, sms, st);
 }
 }  // namespace
