@@ -668,6 +668,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
       rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4,
                        raster_gm(8, 4));
   rfk::Sched s4l = s4;
+  s4l.load_pol = env_int("RF_K4_LOADPOL", 1);   // as the hybrid (evict_last operands)
   const int lockw = env_int("RF_LOCKW", 24);
   if (lockw > 0) {
     s4l.prog = (uint32_t*)(g.w + g.pl.off_prog);
@@ -706,6 +707,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     sp.prog = s4l.prog;
     sp.lock_w = s4l.lock_w;
     sp.lock_ks = s4l.lock_ks;
+    sp.load_pol = s4l.load_pol;
     rfk::EpiSyrkPacked e4{g.pack->send, g.pack->sync, (float)(1.0 / (double)g.m_total), g.pack->world,
                           g.pack->nchunks, kBN4, *g.pack->dev};
     if ((s = launch_tc<C4>("K4_syrk_packed", tA, tB, tAl, tBl, tA, sp, e4, g.sms, g.st))) return s;
