@@ -239,7 +239,7 @@ def main():
         W_host = torch.from_numpy(synthetic.make_W(cfg, rows=np.arange(m0, m0 + m_local))).to(tdt).pin_memory()
         Wd = W_host.to(device)
         if world == 1:
-            G = torch.empty((n, n), dtype=torch.float32, device=device)
+            G = torch.empty((n, n), dtype=torch.float64 if prec == "fp64" else torch.float32, device=device)
             ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
             G_own = G
         else:
@@ -255,7 +255,7 @@ def main():
             G_own = rs.recv
     if do_phi:
         rb, re_ = rf.rf_phi_row_split(n, world, rank)
-        Phi = torch.empty((n, n), dtype=torch.float32, device=device)
+        Phi = torch.empty((n, n), dtype=torch.float64 if prec == "fp64" else torch.float32, device=device)
         ws_p = torch.empty(rf.rf_phi_workspace_size(p, n, prec), dtype=torch.uint8, device=device)
     launches = [0]
 
@@ -369,21 +369,25 @@ def main():
         h2d = X_host.numel() * X_host.element_size() + ((W_host.numel() * W_host.element_size()) if do_gram else 0)
         T = (n + 255) // 256
         tri_off = lambda I: 65536 * (I * T - I * (I - 1) // 2)   # noqa: E731  packed offset of tile row I
+        packed = prec not in ("fp32", "fp64")            # the SIMT modes write dense n × n (include/rf.h)
+        out_mode = "packed_tri" if packed else "upper"
+        odt = torch.float64 if prec == "fp64" else torch.float32
         dev_bufs = [dict(), dict()]
         host = {}
         if do_gram:
             if world == 1:
+                shp = (rf.rf_packed_tri_elems(n),) if packed else (n, n)
                 for b in dev_bufs:
-                    b["G"] = torch.empty(rf.rf_packed_tri_elems(n), dtype=torch.float32, device=device)
-                host["G"] = torch.empty(rf.rf_packed_tri_elems(n), dtype=torch.float32, pin_memory=True)
+                    b["G"] = torch.empty(shp, dtype=odt, device=device)
+                host["G"] = torch.empty(shp, dtype=odt, pin_memory=True)
             else:
                 host["G"] = torch.empty(G_own.shape, dtype=torch.float32, pin_memory=True)
         if do_phi:
-            po0, po1 = tri_off(rb // 256), tri_off(-(-re_ // 256))
+            po0, po1 = (tri_off(rb // 256), tri_off(-(-re_ // 256))) if packed else (rb, re_)
             for b in dev_bufs:
-                b["P"] = torch.empty(rf.rf_packed_tri_elems(n), dtype=torch.float32, device=device)
-            host["P"] = torch.empty(po1 - po0, dtype=torch.float32, pin_memory=True)
-        d2h = sum(h.numel() * 4 for h in host.values())
+                b["P"] = torch.empty((rf.rf_packed_tri_elems(n),) if packed else (n, n), dtype=odt, device=device)
+            host["P"] = torch.empty((po1 - po0,) if packed else (re_ - rb, n), dtype=odt, pin_memory=True)
+        d2h = sum(h.numel() * h.element_size() for h in host.values())
         copy_stream = torch.cuda.Stream(device=device)
         done = [None, None]
         e2e_launches = [0]                               # D2H-finished event of each device buffer
@@ -392,6 +396,7 @@ def main():
 
         def read_back(dst, src, after):
             copy_stream.wait_event(after)
+            dst, src = dst.reshape(-1), src.reshape(-1)
             with torch.cuda.stream(copy_stream):
                 for o in range(0, src.numel(), chunk):
                     dst[o:o + chunk].copy_(src[o:o + chunk], non_blocking=True)
@@ -405,7 +410,7 @@ def main():
             if do_gram:
                 Wd.copy_(W_host, non_blocking=True)
             if do_phi:
-                rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out="packed_tri", row_begin=rb,
+                rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec=prec, out=out_mode, row_begin=rb,
                                       row_end=re_, Phi=b["P"], ws=ws_p)
                 e2e_launches[0] += rf.rf_last_launch_count()
                 ep = torch.cuda.Event()
@@ -413,7 +418,7 @@ def main():
                 read_back(host["P"], b["P"][po0:po1], ep)
             if do_gram:
                 if world == 1:
-                    rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out="packed_tri", m_total=m, G=b["G"], ws=ws_g)
+                    rf.rf_gram(Xd, Wd, act=cfg.act, prec=prec, out=out_mode, m_total=m, G=b["G"], ws=ws_g)
                 else:
                     rs(Xd, Wd)
                 e2e_launches[0] += rf.rf_last_launch_count()
@@ -450,8 +455,9 @@ def main():
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "ms_per_step": ems / args.steps,
                "d2h_gbs": d2h / (ems / args.steps * 1e-3) / 1e9, "gpu_launches": e2e_launches[0],
-               "layout": "G and Φ read back as packed upper-triangle tiles (RF_OUT_PACKED_TRI), D2H of step k "
-                         "overlapped with step k+1 on a copy stream"}
+               "layout": ("G and Φ read back as packed upper-triangle tiles (RF_OUT_PACKED_TRI)" if packed else
+                          "G and Φ read back dense (the SIMT precision modes have no packed layout)")
+                         + ", D2H of step k overlapped with step k+1 on a copy stream"}
         del dev_bufs, host
 
     # ---------------- NEXT-1 (Ternary Random Features) on the same shapes: reported beside the headline
@@ -460,12 +466,13 @@ def main():
         eps = 0.9
         T_host = torch.from_numpy(synthetic.make_T(cfg, eps, rows=np.arange(m0, m0 + m_local))).to(torch.bfloat16)
         Td = T_host.to(device)
-        tau_t = rf.rf_estimate_tau(Xd)
+        Xt = Xd if Xd.dtype == torch.bfloat16 else Xd.to(torch.bfloat16)   # TRF takes bf16 X (include/rf.h)
+        tau_t = rf.rf_estimate_tau(Xt)
         sm, sp = rf.rf_trf_thresholds_for(cfg.act, tau_t)
-        G_t = G if world == 1 else torch.empty((n, n), dtype=torch.float32, device=device)
+        G_t = G if world == 1 and G.dtype == torch.float32 else torch.empty((n, n), dtype=torch.float32, device=device)
         ws_t = torch.empty(rf.rf_gram_ter_workspace_size(p, n, m_local), dtype=torch.uint8, device=device)
         for _ in range(args.warmup):
-            rf.rf_gram_ter(Xd, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
+            rf.rf_gram_ter(Xt, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
         torch.cuda.synchronize()
         barrier()
         rf.rf_profile_read()
@@ -473,7 +480,7 @@ def main():
         ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ta.record(stream)
         for _ in range(args.steps):
-            rf.rf_gram_ter(Xd, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
+            rf.rf_gram_ter(Xt, Td, eps, sm, sp, m_total=m, G=G_t, ws=ws_t)
         tb.record(stream)
         torch.cuda.synchronize()
         rf.rf_profile_enable(False)
