@@ -127,6 +127,20 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
                           double* tau_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * rf_round_bf16 — step G1 for RF_PREC_BF16 (the paper's BF16 inputs):
+ *   dst[r·ldd + c] = bf16(src[r·lds + c]) for r < rows, c < cols, IEEE round to nearest, ties to even;
+ *   ±inf stay ±inf, NaN stays a NaN (canonical payload), overflow past the bf16 range rounds to ±inf.
+ *   src     device fp32, rows × cols, row stride lds ≥ cols elements, 4-B aligned
+ *   dst     device bf16, rows × cols, row stride ldd ≥ cols elements, 2-B aligned; caller-owned
+ *   Enqueued on `stream`; one launch (16-B vector path when cols, lds, ldd are multiples of 4 and the
+ *   bases 16-B / 8-B aligned).  rows = 0 or cols = 0 → RF_OK, no launch.  Negative sizes, NULL
+ *   buffers, ld < cols or misalignment → RF_E_INVALID.  Use it on X and W before rf_gram /
+ *   rf_phi_closed_form in BF16 mode when the data are fp32.
+ */
+rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * rf_gram — G = (1/m_total) Σ_{k < m_local} σ(w_kᵀx_i) σ(w_kᵀx_j)   (Eq. def_Gram)
  *   X       device, n × p (ldx), dtype per `prec`
  *   W_local device, m_local × p (ldw): this rank's rows of W (m_local = m_total on one GPU).  The

@@ -91,6 +91,22 @@ def rf_estimate_tau(X, ws=None, stream=None) -> float:
     return out.value
 
 
+def rf_round_bf16(src, out=None, stream=None):
+    """G1 for BF16 mode (include/rf.h rf_round_bf16): bf16(src) rounded to nearest even, by the library's kernel.
+    src: 2-D float32 CUDA tensor with unit column stride; out: optional bf16 tensor of the same shape."""
+    torch = _torch()
+    _check_tensor("src", src, torch.float32)
+    rows, cols = src.shape
+    if out is None:
+        out = torch.empty((rows, cols), dtype=torch.bfloat16, device=src.device)
+    _check_tensor("out", out, torch.bfloat16)
+    if tuple(out.shape) != (rows, cols):
+        raise RFError(_lib.RF_E_INVALID, f"out has shape {tuple(out.shape)}, need {(rows, cols)}")
+    _lib.check(load().rf_round_bf16(ctypes.c_void_p(src.data_ptr()), src.stride(0), rows, cols,
+                                    ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_ptr(stream)))
+    return out
+
+
 def rf_packed_tri_elems(n: int) -> int:
     """Floats of an out="packed_tri" buffer (include/rf.h RF_OUT_PACKED_TRI)."""
     e = ctypes.c_int64()

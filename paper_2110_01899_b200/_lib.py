@@ -31,7 +31,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_trf_thresholds_for", "rf_ter_features", "rf_gram_ter_workspace_size", "rf_gram_ter",
            "rf_ktilde_workspace_size", "rf_ktilde", "rf_phi_eq2", "rf_gram_packed_p2p", "rf_pack_reduce",
            "rf_ipc_handle", "rf_ipc_open", "rf_ipc_close", "rf_packed_tri_elems", "rf_ridge_workspace_size",
-           "rf_ridge")
+           "rf_ridge", "rf_round_bf16")
 
 RF_PACK_TILE = 256
 RF_PACK_MAX_CHUNKS = 64
@@ -112,6 +112,7 @@ def load() -> ctypes.CDLL:
     lib.rf_gram_packed_p2p.argtypes = [vp, i64, vp, i64, i64, i64, i64, i64, ctypes.c_int, ctypes.c_int, PP, i32,
                                        ctypes.POINTER(vp), i32, vp, sz, vp]
     lib.rf_pack_reduce.argtypes = [PP, vp, vp, vp]
+    lib.rf_round_bf16.argtypes = [vp, i64, i64, i64, vp, i64, vp]
     lib.rf_ipc_handle.argtypes = [vp, ctypes.c_char_p]
     lib.rf_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
     lib.rf_ipc_close.argtypes = [vp]

@@ -148,6 +148,21 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
   return ok();
 }
 
+rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
+                        void* stream) {
+  g_launches = 0;
+  if (rows < 0 || cols < 0) return fail(RF_E_INVALID, "rf_round_bf16: rows, cols must be >= 0");
+  if (rows == 0 || cols == 0) return ok();
+  if (!src || !dst) return fail(RF_E_INVALID, "rf_round_bf16: NULL buffer");
+  if (lds < cols || ldd < cols) return fail(RF_E_INVALID, "rf_round_bf16: leading dimensions must be >= cols");
+  if ((reinterpret_cast<uintptr_t>(src) & 3) || (reinterpret_cast<uintptr_t>(dst) & 1))
+    return fail(RF_E_INVALID, "rf_round_bf16: src must be 4-B and dst 2-B aligned");
+  DevInfo dev;
+  rf_status s;
+  if ((s = check_device(&dev))) return s;
+  return launch_round_bf16(src, lds, rows, cols, dst, ldd, dev.sms, (cudaStream_t)stream);
+}
+
 rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec prec, size_t* bytes) {
   if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
   if (p <= 0 || n <= 0 || m_local <= 0) return fail(RF_E_INVALID, "p, n, m_local must be > 0");

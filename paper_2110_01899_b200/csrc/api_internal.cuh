@@ -313,6 +313,22 @@ rf_status launch_split(const float* src, int64_t lds, int64_t rows, int64_t cols
   return RF_OK;
 }
 
+rf_status launch_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
+                            int sms, cudaStream_t st) {
+  const bool vec = cols % 4 == 0 && lds % 4 == 0 && ldd % 4 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 7) == 0;
+  const int64_t total = rows * (vec ? cols / 4 : cols);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8));
+  ProfScope ps("G1_round_bf16", st);
+  if (vec)
+    rfk::k_round_bf16<true><<<grid, 256, 0, st>>>(src, lds, rows, cols, (__nv_bfloat16*)dst, ldd);
+  else
+    rfk::k_round_bf16<false><<<grid, 256, 0, st>>>(src, lds, rows, cols, (__nv_bfloat16*)dst, ldd);
+  RF_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+  return RF_OK;
+}
+
 rf_status launch_rownorm(const void* X, rf_prec prec, int64_t ldx, int64_t p, int64_t n, double* nrm2,
                          cudaStream_t st) {
   const int grid = (int)((n + 7) / 8);

@@ -1,7 +1,7 @@
 // Small HBM-bound kernels of the path:
 //   K1  row norms ‖x_i‖² (fp64 accumulation, one warp per row, warp-shuffle reduction)
 //       + deterministic τ̂ = (1/n)Σ‖x_i‖² (Lemma 1) + per-row EQ1 coefficients
-//   K2  fp32 → (tf32 hi, fp32 lo) split for the 3×TF32 operands
+//   K2  fp32 → (tf32 hi, fp32 lo) split for the 3×TF32 operands; G1 fp32 → bf16 round-to-nearest-even (BF16 mode)
 #pragma once
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -128,6 +128,28 @@ __global__ void __launch_bounds__(256) k_split_tf32(const float* __restrict__ sr
     const float h = tf32_hi(x);
     hi[r * ldd + c] = h;
     lo[r * ldd + c] = x - h;
+  }
+}
+
+// G1 (BF16 mode): dst = bf16(src), round to nearest, ties to even (cvt.rn.bf16.f32; NaN stays NaN).  kVec: four
+// columns per thread (cols, lds, ldd multiples of 4 and both bases 16-B / 8-B aligned, checked by the caller).
+template <bool kVec>
+__global__ void __launch_bounds__(256) k_round_bf16(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                                    int64_t cols, __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+  const int64_t cv = kVec ? cols / 4 : cols;
+  const int64_t total = rows * cv;
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (int64_t)gridDim.x * 256) {
+    const int64_t r = e / cv, c = e - r * cv;
+    if (kVec) {
+      const float4 x = __ldcs(reinterpret_cast<const float4*>(src + r * lds) + c);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&lo);
+      o.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(dst + r * ldd)[c] = o;
+    } else {
+      dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+    }
   }
 }
 

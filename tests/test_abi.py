@@ -287,3 +287,19 @@ def test_ridge_validation():
     # workspace too small
     s = lib.rf_ridge(vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
     assert s == _lib.RF_E_WORKSPACE
+
+
+def test_round_bf16_validation():
+    """rf_round_bf16 (G1) validates before touching the device: empty sizes are a no-op, bad arguments fail."""
+    lib = rf.load()
+    buf = (ctypes.c_char * 4096)()
+    a = (ctypes.addressof(buf) + 255) // 256 * 256
+    vp = ctypes.c_void_p
+    assert lib.rf_round_bf16(vp(a), 8, 0, 8, vp(a), 8, None) == 0
+    assert lib.rf_round_bf16(vp(a), 8, 8, 0, vp(a), 8, None) == 0
+    assert lib.rf_round_bf16(vp(a), 8, -1, 8, vp(a), 8, None) == _lib.RF_E_INVALID
+    assert lib.rf_round_bf16(None, 8, 2, 8, vp(a), 8, None) == _lib.RF_E_INVALID
+    s = lib.rf_round_bf16(vp(a), 7, 2, 8, vp(a), 8, None)
+    assert s == _lib.RF_E_INVALID and b"leading" in lib.rf_last_error()
+    s = lib.rf_round_bf16(vp(a + 2), 8, 2, 8, vp(a), 8, None)
+    assert s == _lib.RF_E_INVALID and b"aligned" in lib.rf_last_error()
