@@ -127,7 +127,7 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
                           double* tau_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
- * rf_round_bf16 — step G1 for RF_PREC_BF16 (the paper's BF16 inputs):
+ * rf_round_bf16 — step G1 for RF_PREC_BF16 (X, W of P:470 in the north star's BF16 mode):
  *   dst[r·ldd + c] = bf16(src[r·lds + c]) for r < rows, c < cols, IEEE round to nearest, ties to even;
  *   ±inf stay ±inf, NaN stays a NaN (canonical payload), overflow past the bf16 range rounds to ±inf.
  *   src     device fp32, rows × cols, row stride lds ≥ cols elements, 4-B aligned

@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY (same rule as oracle/rf_oracle.py): imported by tests/, __graft_entry__.smoke() and
 bench.py's CPU legs; never by the product path.
 
-The paper runs its BF16 experiments on bf16-stored inputs; bf16 is binary32 with the low 16 fraction bits
+The paper is silent on precision (X, W are real matrices); BF16 is the north star's mode, and bf16 is binary32 with the low 16 fraction bits
 dropped (1 sign, 8 exponent, 7 fraction bits), and the rounding is IEEE 754's default, round to nearest, ties to even.
 Written out on the bit pattern u of the binary32 value:
   keep = u >> 16;  rest = u & 0xFFFF
