@@ -64,8 +64,9 @@ def test_nearest_neighbour_brute_force():
 def test_matches_library_cast():
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(5)
-    x = np.concatenate([rng.standard_normal(50000).astype(np.float32) * 10.0 ** rng.integers(-30, 30, 50000),
-                        f32(rng.integers(0, 2 ** 32, 50000, dtype=np.uint64).astype(np.uint32))])
-    x = x[np.isfinite(x)]
+    a = (rng.standard_normal(50000) * 10.0 ** rng.integers(-30, 30, 50000)).astype(np.float32)
+    b = f32(rng.integers(0, 2 ** 32, 50000, dtype=np.uint64).astype(np.uint32))
+    b = b[np.isfinite(b)]                       # random bit patterns: drop NaN / inf before any float cast
+    x = np.concatenate([a, b]).astype(np.float32)
     ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(round_bf16_bits(x), ref)
