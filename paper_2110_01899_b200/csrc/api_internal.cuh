@@ -774,8 +774,9 @@ rf_status launch_k5(const K5Args& a) {
   struct { int sms; } dev{a.sms};
   rf_status s;
   CUtensorMap tA, tAl, tO;
-  const bool tma_out = a.tri_T > 0 ? make_tmap_out(&tO, Phi, tri_tiles(n) * 256, 256, 256)
-                                   : make_tmap_out(&tO, Phi, n, n, ldphi);
+  const bool tma_out = env_int("RF_K5_TMA", 1) != 0 &&
+                       (a.tri_T > 0 ? make_tmap_out(&tO, Phi, tri_tiles(n) * 256, 256, 256)
+                                    : make_tmap_out(&tO, Phi, n, n, ldphi));
   rfk::EpiEq1<kOdd> e{Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full, tma_out ? 1 : 0, a.tri_T};
   const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
   if (prec == RF_PREC_BF16 || prec == RF_PREC_TF32) {
