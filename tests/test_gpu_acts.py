@@ -10,6 +10,7 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 import paper_2110_01899_b200 as rf  # noqa: E402
 import synthetic  # noqa: E402
+from entry_bounds import check, gram_bound, phi_bound  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 TABLE2 = ["relu", "abs", "sign", "step", "cos", "sin", "ident", "quad", "bump"]
@@ -38,12 +39,15 @@ def test_gram_table2(act, prec):
     Xd, Wd = torch.tensor(X, device="cuda").to(DT[prec]), torch.tensor(W, device="cuda").to(DT[prec])
     G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper")
     torch.cuda.synchronize()
-    ref = oracle.gram(Xd.double().cpu().numpy(), Wd.double().cpu().numpy(), act)
+    Xo, Wo = Xd.double().cpu().numpy(), Wd.double().cpu().numpy()
+    ref = oracle.gram(Xo, Wo, act)
     I, J = np.triu_indices(n)
-    e = _rel(G.double().cpu().numpy()[I, J], ref[I, J])
+    Gc = G.double().cpu().numpy()
+    e = _rel(Gc[I, J], ref[I, J])
     tol = 2e-3 if prec == "bf16" else (2e-5 if act in ("sign", "step") else 1e-5)
     print(f"[parity] G {act} {prec}: rel-Frobenius {e:.3e}")
     assert e <= tol
+    check(f"G {act} {prec}", Gc[I, J], ref[I, J], gram_bound(prec, act, Xo, Wo, ref, I, J))
 
 
 @pytest.mark.parametrize("act", TABLE2)
@@ -57,9 +61,11 @@ def test_phi_table2_eq1_eq2(act, form):
     torch.cuda.synchronize()
     ref = (oracle.phi_eq1 if form == 1 else oracle.phi_eq2)(Xb, act)
     I, J = np.triu_indices(n)
-    e = _rel(Phi.double().cpu().numpy()[I, J], ref[I, J])
+    Pc = Phi.double().cpu().numpy()
+    e = _rel(Pc[I, J], ref[I, J])
     print(f"[parity] Φ EQ{form} {act} bf16: rel-Frobenius {e:.3e}")
     assert e <= 1e-5
+    check(f"Phi EQ{form} {act}", Pc[I, J], ref[I, J], phi_bound("bf16", act, Xb, oracle.tau_hat(Xb), I, J, form=form))
 
 
 @pytest.mark.parametrize("act", ["tanh", "erf", "sigmoid_half"])
@@ -69,12 +75,14 @@ def test_phi_eq2_north_star_acts_3xtf32(act):
     Xd = torch.tensor(X, device="cuda").to(torch.float32)
     Phi = rf.rf_phi_closed_form(Xd, act=act, tau=0.0, prec="3xtf32", out="full", form=2)
     torch.cuda.synchronize()
-    ref = oracle.phi_eq2(Xd.double().cpu().numpy(), act)
+    Xo = Xd.double().cpu().numpy()
+    ref = oracle.phi_eq2(Xo, act)
     I, J = np.triu_indices(n)
     Pc = Phi.double().cpu().numpy()
     e = _rel(Pc[I, J], ref[I, J])
     print(f"[parity] Φ EQ2 {act} 3xtf32: rel-Frobenius {e:.3e}")
     assert e <= 1e-5
+    check(f"Phi EQ2 {act} 3xtf32", Pc[I, J], ref[I, J], phi_bound("3xtf32", act, Xo, oracle.tau_hat(Xo), I, J, form=2))
     assert np.array_equal(Pc, Pc.T)
 
 
@@ -95,7 +103,7 @@ def test_phi_eq2_config4_full_size_sampled():
     Xd = torch.tensor(X, device="cuda").to(torch.bfloat16)
     Phi = rf.rf_phi_closed_form(Xd, act=cfg.act, tau=0.0, prec="bf16", out="upper", form=2)
     torch.cuda.synchronize()
-    S = synthetic.sample_indices(cfg.n, count=768, tile_stride=2048)
+    S = synthetic.sample_indices(cfg.n, count=768, tile_stride=256)     # every row ≡ 0, ±1 (mod 256)
     St = torch.tensor(S, device="cuda")
     sub = Phi.index_select(0, St).index_select(1, St).double().cpu().numpy()
     del Phi
@@ -106,3 +114,4 @@ def test_phi_eq2_config4_full_size_sampled():
     e = _rel(sub[I, J], ref[I, J])
     print(f"[parity] Φ EQ2 configs[4] sampled |S|={len(S)}: rel-Frobenius {e:.3e}")
     assert e <= 1e-5
+    check("Phi EQ2 configs[4]", sub[I, J], ref[I, J], phi_bound("bf16", cfg.act, Xb[S], tau, I, J, form=2))

@@ -12,6 +12,7 @@ from oracle import center as C  # noqa: E402
 from oracle import trf  # noqa: E402
 import paper_2110_01899_b200 as rf  # noqa: E402
 import synthetic  # noqa: E402
+from entry_bounds import center_bound, check, full_pairs, gram_bound, phi_bound  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 SENT = -7.25
@@ -41,12 +42,18 @@ def test_gram_centered(prec, out, tol):
     G = torch.full((n, n), SENT, dtype=torch.float64 if prec == "fp64" else torch.float32, device="cuda")
     rf.rf_gram(Xd, Wd, act="tanh", prec=prec, out=out, G=G)
     torch.cuda.synchronize()
-    ref = C.center(oracle.gram(Xd.double().cpu().numpy(), Wd.double().cpu().numpy(), "tanh"))
+    Xo, Wo = Xd.double().cpu().numpy(), Wd.double().cpu().numpy()
+    A = oracle.gram(Xo, Wo, "tanh")
+    ref = C.center(A)
     Gc = G.double().cpu().numpy()
     I, J = np.triu_indices(n)
     e = _rel(Gc[I, J], ref[I, J])
     print(f"[parity] centred G {prec} {out}: rel-Frobenius {e:.3e}")
     assert e <= tol
+    FI, FJ = full_pairs(n)
+    bA = gram_bound(prec, "tanh", Xo, Wo, A, FI, FJ).reshape(n, n)
+    check(f"centred G {prec}", Gc[I, J], ref[I, J],
+          center_bound(A, bA, I, J, u=2.0 ** -50 if prec == "fp64" else 2.0 ** -21))
     if out.startswith("upper"):
         assert np.all(Gc[np.tril_indices(n, -1)] == SENT)
     else:
@@ -61,10 +68,17 @@ def test_phi_and_gram_ter_centered():
     Phi = rf.rf_phi_closed_form(Xd, act="tanh", tau=0.0, prec="bf16", out="full_centered")
     torch.cuda.synchronize()
     U = np.nan_to_num(oracle.phi_eq1(Xb, "tanh"), nan=0.0)    # upper triangle (pivot = row), R6
-    ref = C.center(U + np.triu(U, 1).T)                          # FULL mirrors the upper triangle
+    A = U + np.triu(U, 1).T                                     # FULL mirrors the upper triangle
+    ref = C.center(A)
     e = _rel(Phi.double().cpu().numpy(), ref)
     print(f"[parity] centred Φ bf16: rel-Frobenius {e:.3e}")
     assert e < 1e-5
+    I, J = np.triu_indices(n)
+    bu = np.zeros((n, n))
+    bu[I, J] = phi_bound("bf16", "tanh", Xb, oracle.tau_hat(Xb), I, J)
+    bA = bu + np.triu(bu, 1).T
+    FI, FJ = full_pairs(n)
+    check("centred Φ bf16", Phi.double().cpu().numpy().ravel(), ref.ravel(), center_bound(A, bA, FI, FJ))
     with pytest.raises(rf.RFError):
         rf.rf_phi_closed_form(Xd, act="tanh", tau=1.0, prec="bf16", out="upper_centered", row_begin=0, row_end=256)
     T = synthetic.make_T(4, eps, m=m, p=p)
@@ -72,11 +86,20 @@ def test_phi_and_gram_ter_centered():
     sm, sp = rf.rf_trf_thresholds_for("tanh", oracle.tau_hat(Xb))
     Gt = rf.rf_gram_ter(Xd, Td, eps, sm, sp, out="upper_centered")
     torch.cuda.synchronize()
-    reft = C.center(trf.gram_ter(Xb, T, eps, sm, sp))
+    At = trf.gram_ter(Xb, T, eps, sm, sp)
+    reft = C.center(At)
     I, J = np.triu_indices(n)
     e2 = _rel(Gt.double().cpu().numpy()[I, J], reft[I, J])
     print(f"[parity] centred G^ter: rel-Frobenius {e2:.3e}")
     assert e2 < 1e-5
+    # G^ter is an exact count / m (test_gpu_trf): only decisions inside the fp32 band of a threshold may differ, each
+    # moving an entry by ≤ 2/m; rows' band counts bound the uncentred error
+    margin = trf.decision_margin(Xb, T, eps, sm, sp)
+    band = (1 - eps) ** -0.5 * (math.ceil(p / 16) + 2) * 2.0 ** -23 * np.sum(np.abs(Xb), axis=1) + \
+        2.0 ** -22 * max(abs(sm), abs(sp))                      # test_gpu_trf._band
+    fr = np.sum(margin <= band[:, None], axis=1).astype(float)   # decisions that may flip, per row
+    bA = (fr[:, None] + fr[None, :]) * 2.0 / m + 2.0 ** -22
+    check("centred G^ter", Gt.double().cpu().numpy()[I, J], reft[I, J], center_bound(At, bA, I, J))
 
 
 def _gmm_stats(n, p, seed):
@@ -110,17 +133,37 @@ def test_ktilde_matches_oracle(prec, out, n, p):
     Kt = torch.full((n, n), SENT, dtype=torch.float32, device="cuda")
     rf.rf_ktilde(Xd, Vd, A, d0, d1, d2, prec=prec, out=out, Kt=Kt)
     torch.cuda.synchronize()
-    ref = C.ktilde(Xd.double().cpu().numpy(), Vd.double().cpu().numpy(), A, d0, d1, d2)
+    Xo, Vo = Xd.double().cpu().numpy(), Vd.double().cpu().numpy()
+    ref = C.ktilde(Xo, Vo, A, d0, d1, d2)
     Kc = Kt.double().cpu().numpy()
     I, J = np.triu_indices(n)
     e = _rel(Kc[I, J], ref[I, J])
     tol = 2e-3 if prec == "tf32" else 1e-5
     print(f"[parity] K̃ {prec} {out} n={n} p={p}: rel-Frobenius {e:.3e}")
     assert e <= tol
+    check(f"K̃ {prec}", Kc[I, J], ref[I, J], _ktilde_bound(prec, Xo, Vo, np.asarray(A, float), d0, d1, d2, I, J))
     if out == "upper":
         assert np.all(Kc[np.tril_indices(n, -1)] == SENT)
     else:
         assert np.array_equal(Kc, Kc.T)
+
+
+def _ktilde_bound(prec, X, V, A, d0, d1, d2, I, J):
+    """Per-entry bound of K̃ = d1·g + d2·u_iᵀv_j + d0·δ_ij − r'_i − r'_j (one fp32 epilogue over the XᵀX mainloop):
+    g's conversion + accumulation error (entry_bounds.acc_rel), the rank-kv term and the row means in fp32."""
+    from entry_bounds import U_OPERAND, acc_rel
+    xn = np.sqrt(np.sum(X * X, axis=1))
+    U = V @ A.T
+    M = d1 * (X @ X.T) + d2 * (U @ V.T) + d0 * np.eye(len(X))
+    r = M.mean(axis=1)
+    s_ = r.mean()
+    dg = (2 * U_OPERAND[prec] + acc_rel(prec, X.shape[1])) * xn[I] * xn[J]
+    uv = np.abs(U[I]) @ np.ones(U.shape[1]) * 0 + np.sum(np.abs(U[I] * V[J]), axis=1)
+    # r' comes from fp32 x̄ and per-row dot products of length p: same accumulation rule, relative to ‖x_i‖‖x̄‖/n
+    xbar = X.sum(axis=0)
+    dr = abs(d1) * (2 * U_OPERAND[prec] + acc_rel(prec, X.shape[1]) + 2.0 ** -20) * xn * np.linalg.norm(xbar) / len(X)
+    return (abs(d1) * dg + abs(d2) * 2.0 ** -20 * uv + dr[I] + dr[J]
+            + 2.0 ** -20 * (np.abs(M[I, J]) + np.abs(r[I]) + np.abs(r[J]) + abs(s_)) + 1e-9)
 
 
 def test_ktilde_without_v_and_errors():

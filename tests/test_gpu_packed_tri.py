@@ -14,6 +14,7 @@ import oracle  # noqa: E402
 import paper_2110_01899_b200 as rf  # noqa: E402
 import synthetic  # noqa: E402
 from paper_2110_01899_b200 import layout  # noqa: E402
+from entry_bounds import check, gram_bound, phi_bound  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 DT = {"bf16": torch.bfloat16, "tf32": torch.float32, "3xtf32": torch.float32}
@@ -45,10 +46,12 @@ def test_gram_packed_tri_equals_upper(n, p, m, prec):
     I, J = np.triu_indices(n)
     Gc = G.cpu().numpy()
     assert np.array_equal(D[I, J], Gc[I, J])
-    ref = oracle.gram(Xd.double().cpu().numpy(), Wd.double().cpu().numpy(), "tanh")
+    Xo, Wo = Xd.double().cpu().numpy(), Wd.double().cpu().numpy()
+    ref = oracle.gram(Xo, Wo, "tanh")
     e = _rel(D[I, J].astype(np.float64), ref[I, J])
     print(f"[parity] packed G {prec} n={n}: rel-Frobenius {e:.3e}")
     assert e <= (2e-3 if prec in ("bf16", "tf32") else 1e-5)
+    check(f"packed G {prec} n={n}", D[I, J], ref[I, J], gram_bound(prec, "tanh", Xo, Wo, ref, I, J))
 
 
 @pytest.mark.parametrize("act", ["sigmoid_half", "relu"])
@@ -63,10 +66,12 @@ def test_phi_packed_tri_equals_upper(act, n):
     D = layout.unpack_tri(P.cpu().numpy(), n, out=np.zeros((n, n), np.float32))
     I, J = np.triu_indices(n)
     assert np.array_equal(D[I, J], Phi.cpu().numpy()[I, J])
-    ref = oracle.phi_eq1(Xd.double().cpu().numpy(), act)
+    Xo = Xd.double().cpu().numpy()
+    ref = oracle.phi_eq1(Xo, act)
     e = _rel(D[I, J].astype(np.float64), ref[I, J])
     print(f"[parity] packed Φ {act} n={n}: rel-Frobenius {e:.3e}")
     assert e <= 1e-5
+    check(f"packed Φ {act} n={n}", D[I, J], ref[I, J], phi_bound("bf16", act, Xo, oracle.tau_hat(Xo), I, J))
 
 
 def test_phi_packed_tri_row_ranges_compose():

@@ -170,3 +170,42 @@ def test_pivot_asymmetry_diagnostic(act):
     Z = rng.standard_normal((6, 16))
     Z /= np.linalg.norm(Z, axis=1, keepdims=True)
     assert oracle.phi_pivot_asymmetry(Z * 1.1, act, tau=1.0) <= 1e-15 < a[2]   # equal norms up to rounding
+
+
+# ------------------------------------------------------------------------------------------------------------------
+# SURVEY.md §8(c)'s 13 survey-computed values (tests/golden/survey_eq1_values.txt): an independent computation of
+# the corrected EQ1 and of the exact kernel, which the oracle must reproduce to ≤ 1e-10 (the values are printed to
+# 12 decimals).  Includes the diagonal-type rows (u_b = 0) and the exact tanh / sigmoid−½ column.
+# ------------------------------------------------------------------------------------------------------------------
+import os  # noqa: E402
+
+_SURVEY = os.path.join(os.path.dirname(__file__), "golden", "survey_eq1_values.txt")
+
+
+def _survey_rows():
+    rows = []
+    for line in open(_SURVEY):
+        if line.startswith("#") or not line.strip():
+            continue
+        f = [x.strip() for x in line.split("|")]
+        rows.append((f[0], *map(float, f[1:])))
+    return rows
+
+
+def test_survey_golden_values_table_complete():
+    rows = _survey_rows()
+    assert len(rows) == 13
+    assert sum(1 for r in rows if r[4] == 0.0) == 3          # one diagonal-type row per σ
+
+
+@pytest.mark.parametrize("row", _survey_rows(), ids=lambda r: f"{r[0]}-{r[1]}-{r[2]}-{r[3]}-{r[4]}")
+def test_oracle_reproduces_survey_golden_values(row):
+    act, tau, u_a, v_b, u_b, want_eq1, want_exact = row
+    mom = oracle.moments(act, tau, 200)
+    got = float(oracle.eq1(mom, u_a, v_b, u_b))
+    assert abs(got - want_eq1) <= 1e-10, (got, want_eq1)
+    ex = oracle.phi_exact_pair(act, u_a, v_b, u_b, N=120)
+    assert abs(ex - want_exact) <= 1e-10, (ex, want_exact)
+    if act == "erf":   # the exact column is the arcsine kernel: x = (u_a, 0), y = (v_b, u_b)
+        arc = 2 / math.pi * math.asin(2 * u_a * v_b / math.sqrt((1 + 2 * u_a ** 2) * (1 + 2 * (v_b ** 2 + u_b ** 2))))
+        assert abs(arc - want_exact) <= 1e-10, (arc, want_exact)
