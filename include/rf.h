@@ -178,8 +178,9 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
  *   ws   ≥ rf_phi_workspace_size(p, n, prec).
  * Pipeline: K1 row norms (fp64) [+ τ̂] → per-row coefficients → K5 fused XᵀX (tcgen05 CTA pairs,
  *           256×256 upper-triangle tiles) + EQ1 epilogue with TMA stores.
- * A zero-norm sample makes v_b undefined: with tau <= 0 it is detected → RF_E_INVALID;
- * with tau > 0 the affected row of Φ is non-finite.
+ * A zero-norm sample makes v_b undefined: with tau <= 0 (the call synchronizes anyway) it is detected →
+ * RF_E_INVALID; with tau > 0 (asynchronous, no host check) a zero pivot x_i = 0 is taken as its Gram–Schmidt limit
+ * (R23: v_b = 0, u_b = ‖x_j‖, diagonal u_a = v_b = u_b = 0), so every entry of Φ stays finite.
  */
 rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes);
 rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,

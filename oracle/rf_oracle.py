@@ -238,10 +238,14 @@ def gram_entries(Xs: np.ndarray, W: np.ndarray, act: str, I: np.ndarray, J: np.n
 # --------------------------------------------------------------------------------------------
 def gram_schmidt(xi_norm2, xj_norm2, g, diag):
     """u_a = ‖x_i‖, v_b = x_iᵀx_j/‖x_i‖, u_b = √(‖x_j‖² − (x_iᵀx_j)²/‖x_i‖²)  (P:1016-1018).
-    Readings R6 (diagonal) and R7 (clamp)."""
+    Readings R6 (diagonal), R7 (clamp) and R23 (a zero pivot x_i = 0: x_j has no component along it, v_b = 0 and
+    u_b = ‖x_j‖)."""
+    xi_norm2 = np.asarray(xi_norm2, dtype=np.float64)
+    zero = xi_norm2 == 0.0
+    safe = np.where(zero, 1.0, xi_norm2)
     u_a = np.sqrt(xi_norm2)
-    v_b = g / u_a
-    u_b = np.sqrt(np.maximum(0.0, xj_norm2 - g * g / xi_norm2))
+    v_b = np.where(zero, 0.0, g / np.sqrt(safe))
+    u_b = np.where(zero, np.sqrt(xj_norm2), np.sqrt(np.maximum(0.0, xj_norm2 - g * g / safe)))
     v_b = np.where(diag, u_a, v_b)
     u_b = np.where(diag, 0.0, u_b)
     return u_a, v_b, u_b

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm
   c.a0 = A0;
   c.a1 = A1;
   c.a2h = 0.5 * m.kd[0][2] * A2;
-  c.c = m.inv_st / ua;                              // ν = g·c
+  c.c = ua > 0.0 ? m.inv_st / ua : 0.0;            // ν = g·c; a zero pivot row (R23): ν = 0, s = ‖x_j‖/√τ
   c.nu_diag = ua * m.inv_st;                        // ν on the diagonal (v_b = u_a)
   c.pad0 = c.pad1 = c.pad2 = 0;
   rc[i] = c;

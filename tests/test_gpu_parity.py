@@ -199,6 +199,11 @@ def test_phi_diagonal_rule_and_zero_norm():
     Xz[5] = 0.0
     with pytest.raises(rf.RFError):
         rf.rf_phi_closed_form(dev(Xz, "bf16"), act="tanh", tau=0.0, prec="bf16")
+    # explicit τ (asynchronous call): the zero pivot row is its Gram–Schmidt limit (R23), every entry finite
+    Pz, refz = _phi_case(Xz, "sigmoid_half", "bf16", tau=1.0)
+    I, J = upper_idx(256)
+    assert np.all(np.isfinite(Pz[I, J]))
+    assert np.all(np.abs(Pz[5, 5:]) < 1e-12)  # odd σ, ν = 0 on the zero row: Φ = ν·A1·C1 = 0
 
 
 def test_estimate_tau_lemma1():

@@ -209,3 +209,20 @@ def test_oracle_reproduces_survey_golden_values(row):
     if act == "erf":   # the exact column is the arcsine kernel: x = (u_a, 0), y = (v_b, u_b)
         arc = 2 / math.pi * math.asin(2 * u_a * v_b / math.sqrt((1 + 2 * u_a ** 2) * (1 + 2 * (v_b ** 2 + u_b ** 2))))
         assert abs(arc - want_exact) <= 1e-10, (arc, want_exact)
+
+
+def test_zero_pivot_reading_r23():
+    """R23: a zero sample x_i = 0 as the Gram–Schmidt pivot has v_b = 0, u_b = ‖x_j‖ (x_j is orthogonal to it), so
+    for odd σ EQ1 gives the exact kernel's value E[σ(0)σ(‖x_j‖ξ)] = 0 (to the quadrature's ⟨0,0⟩ ≈ 1e-17), and Φ is
+    finite everywhere."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((6, 16)) / 4
+    X[2] = 0.0
+    for act in ("tanh", "erf", "sigmoid_half"):
+        P = oracle.phi_eq1(X, act, tau=1.0)
+        I, J = np.triu_indices(6)
+        assert np.all(np.isfinite(P[I, J]))
+        assert np.all(np.abs(P[2, 2:]) < 1e-15)
+        assert abs(oracle.phi_exact_pair(act, 0.0, 0.0, float(np.linalg.norm(X[4])))) < 1e-15
+    u_a, v_b, u_b = oracle.gram_schmidt(np.array([0.0]), np.array([2.25]), np.array([0.0]), np.array([False]))
+    assert u_a[0] == 0.0 and v_b[0] == 0.0 and u_b[0] == 1.5
