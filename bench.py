@@ -44,10 +44,11 @@ def parse():
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
     ap.add_argument("--no-phi4", action="store_true", help="skip the configs[4] Φ-only measurement")
     ap.add_argument("--no-ridge", action="store_true", help="skip the NEXT-4 ridge-regression measurement")
-    ap.add_argument("--g5", default="fused", choices=["fused", "nccl"],
-                    help="N>1: G5 as the fused peer-memory epilogue (default) or chunked NCCL reduce-scatter")
-    ap.add_argument("--comm-sms", type=int, default=8,
-                    help="N>1: SMs left free during K4 for the overlapped reduce-scatter kernels")
+    ap.add_argument("--g5", default="peers", choices=["peers", "nccl"],
+                    help="N>1: G5 as the peer-memory exchange in K4's epilogue (default) or chunked NCCL reduce-scatter")
+    ap.add_argument("--same-gpu", action="store_true",
+                    help="testing only: every rank on cuda:0 with a gloo process group (peer G5 over CUDA IPC), so the "
+                         "N>1 branch runs on a one-GPU box")
     return ap.parse_args()
 
 
@@ -210,13 +211,19 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.same_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 with torch.distributed.run")
+    if args.same_gpu and args.g5 != "peers":
+        raise SystemExit("--same-gpu runs the peer G5 only (NCCL needs one GPU per rank)")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    gloo = args.same_gpu
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     assert rf.rf_device_supported(local), "not an sm_100 device"
 
     cfg = synthetic.CONFIGS[args.config]
@@ -253,15 +260,11 @@ def main():
             ws_g = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, prec), dtype=torch.uint8, device=device)
             G_own = G
         else:
-            if args.g5 == "fused" and prec in ("bf16", "tf32"):
-                # G5 fused: K4's epilogue stores each owned tile into the owner's staging buffer over NVLink
-                # (CUDA-IPC peer memory), overlapped with the SYRK; owners then sum their R slices.
-                rs = collective.GramFusedP2P(n, p, m_local, m, cfg.act, prec, nchunks=16)
-            else:
-                # G5 baseline: packed tiles + chunked NCCL reduce-scatter overlapped on a comm stream
-                rs = collective.GramReduceScatter(n, p, m_local, m, cfg.act, prec, nchunks=16,
-                                                  max_sms=torch.cuda.get_device_properties(device).multi_processor_count
-                                                  - args.comm_sms)
+            # G5 inside the library's collective rf_gram: peers = K4's epilogue stores each owned tile into the
+            # owner's staging buffer over NVLink (CUDA-IPC peer memory), device epoch flags order the owner-side sums;
+            # nccl = packed send buffer + per-chunk counters + chunked reduce-scatter on the context's comm stream
+            mode = args.g5 if prec in ("bf16", "tf32") else "nccl"
+            rs = collective.GramCollective(n, p, m_local, m, cfg.act, prec, mode=mode, device=device)
             G_own = rs.recv
     if do_phi:
         rb, re_ = rf.rf_phi_row_split(n, world, rank)
@@ -294,7 +297,14 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if gloo else dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cpu" if gloo else device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         step()
@@ -317,11 +327,7 @@ def main():
     rf.rf_profile_enable(False)
     recs = rf.rf_profile_read()
     clk = clocks.stop() if clocks else None
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms / args.steps
 
     # ---------------- algorithmic work of one step (whole job)
@@ -468,11 +474,7 @@ def main():
         eb.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems = ea.elapsed_time(eb)
-        if world > 1:
-            t = torch.tensor([ems], device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(ea.elapsed_time(eb))
         e2e = {"value": (g_flops + phi_flops) / (ems / args.steps * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
                "ms_per_step": ems / args.steps,
@@ -674,8 +676,10 @@ def main():
                        "p": p, "n": n, "m": m, "act": cfg.act, "prec": prec,
                        "parallelism": (f"G: W sharded over m ({world} ranks); G5 = "
                                        + ("K4 epilogue storing packed triangle tiles into the owners' buffers over "
-                                          "NVLink peer memory + owner-side sum" if args.g5 == "fused" else
+                                          "NVLink peer memory + owner-side sum, ordered by device epoch flags"
+                                          if args.g5 == "peers" else
                                           "chunked NCCL reduce-scatter of packed triangle tiles overlapped with K4")
+                                       + (" [--same-gpu test run: all ranks on one GPU]" if args.same_gpu else "")
                                        + "; "
                                        f"Φ: row blocks, no collective") if world > 1 else "single GPU",
                        "inputs": ("fp32 X, W rounded to bf16 on the device every step (G1, rf_round_bf16)" if g1

@@ -21,8 +21,14 @@
  *   RF_PREC_TF32   X, W f32 ; output f32 ; tcgen05 kind::tf32, one pass (≈1e-3 class)
  *   RF_PREC_BF16   X, W bf16; output f32 ; tcgen05 kind::f16, Σ stored bf16, fp32 accumulation
  *
+ * CONTEXT: every compute call takes an rf_ctx* first (NULL = this thread's default context of the current device):
+ * it binds the call to a device, carries the tuning options and, once a collective is attached, the rank, the world
+ * and the exchange resources of the multi-GPU G (rf_ctx_* below).  A context is not thread-safe: use one per thread.
+ *
  * OWNERSHIP: the caller allocates every device buffer (inputs, outputs, workspace).  The library never
- * allocates device memory on a call path and keeps no pointer after a call returns.
+ * allocates device memory on a call path and keeps no pointer to a caller buffer after a call returns.  Only
+ * context set-up allocates: rf_ctx_attach_peers (the staging buffer other ranks store G tiles into) and
+ * rf_ctx_init_nccl / rf_ctx_attach_nccl (64 B of chunk counters); rf_ctx_destroy frees them.
  *
  * ASYNC: GPU work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default stream)
  * and the call returns after enqueue, EXCEPT: rf_moments (host-only, synchronous); rf_estimate_tau and
@@ -49,7 +55,7 @@ typedef enum {
   RF_E_UNSUPPORTED = 2,  /* device is not sm_100 (B200) */
   RF_E_NONFINITE = 3,    /* σ non-finite at a quadrature node */
   RF_E_CUDA = 4,         /* a CUDA runtime/driver error (launch failure, earlier async fault) */
-  RF_E_NCCL = 5,         /* reserved for the collective layer */
+  RF_E_NCCL = 5,         /* NCCL missing from the process, or an NCCL call / the communicator's async error failed */
   RF_E_WORKSPACE = 6     /* workspace pointer NULL or smaller than rf_*_workspace_size() */
 } rf_status;
 
@@ -77,7 +83,8 @@ typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_T
  *   copy of G or Φ moves (the e2e path of bench.py).
  */
 typedef enum {
-  RF_OUT_UPPER = 0, RF_OUT_FULL = 1, RF_OUT_UPPER_CENTERED = 2, RF_OUT_FULL_CENTERED = 3, RF_OUT_PACKED_TRI = 4
+  RF_OUT_UPPER = 0, RF_OUT_FULL = 1, RF_OUT_UPPER_CENTERED = 2, RF_OUT_FULL_CENTERED = 3, RF_OUT_PACKED_TRI = 4,
+  RF_OUT_PACKED_TILES = 5   /* multi-GPU G: this rank's owned, SUMMED 256×256 tiles (rf_tile_map); rf_gram only */
 } rf_out;
 #define RF_OUT_CENTER 2
 /* Number of floats of an RF_OUT_PACKED_TRI buffer for n samples (n > 0; else RF_E_INVALID). */
@@ -105,6 +112,104 @@ const char* rf_version(void);
 /* 1 if `device` is an sm_100 part this library's kernels run on, else 0 (no error text). */
 int rf_device_supported(int device);
 
+/* =============================================================================================
+ * CONTEXT.  rf_ctx_create(device): a context bound to `device` (must be sm_100, else
+ * RF_E_UNSUPPORTED); it owns a side stream (the concurrent tail launch of the K3/K4 multicast + pair hybrids) and
+ * the options below.  rf_ctx_destroy releases everything the context allocated (NULL is a no-op); the caller must
+ * have synchronized the streams it passed to calls on this context.
+ * ============================================================================================= */
+typedef struct rf_ctx rf_ctx;
+rf_status rf_ctx_create(int device, rf_ctx** out);
+void rf_ctx_destroy(rf_ctx* ctx);
+
+/* Tuning options.  Defaults are the measured best; the alternatives exist for A/B measurement and
+ * for the bit-exactness tests of the alternative kernels.  Value checks: RF_E_INVALID. */
+typedef enum {
+  RF_OPT_K3_HYBRID = 0,    /* 1: K3 as 4-CTA multicast clusters + pair clusters on the leftover SMs (n ≥ 32 row
+                              tiles); 0: pair clusters only                                          default 1 */
+  RF_OPT_K4_HYBRID = 1,    /* the same for K4 (n ≥ 64 row tiles)                                    default 1 */
+  RF_OPT_K4_CL8 = 2,       /* 1: the K4 hybrid with 8-CTA clusters (2 × 2 pairs sharing A and B)     default 0 */
+  RF_OPT_K4_SPLIT_R100 = 3,/* K4 hybrid work split: per-SM rate ratio multicast/pair × 100          default 111 */
+  RF_OPT_K3_SPLIT_R100 = 4,/* K3 hybrid work split, as above                                        default 120 */
+  RF_OPT_LOCK_W = 5,       /* K4 soft lockstep: allowed lead in K-blocks (0 = off)                  default 24 */
+  RF_OPT_LOCK_KS = 6,      /* K4 soft lockstep: check period in K-blocks                            default 8 */
+  RF_OPT_K5_WIDE = 7,      /* K5 epilogue warps: −1 auto (16 for p ≤ 512, else 8), 0 → 8, 1 → 16     default −1 */
+  RF_OPT_EQ1_GENERAL = 8,  /* 1: the general EQ1 epilogue also for odd σ (A0, A2 kept)               default 0 */
+  RF_OPT_KCHUNK = 9,       /* 3×TF32 K4 accumulation chunk in K-blocks (0 = whole K)                default 4 */
+  RF_OPT_MAX_SMS = 10,     /* ≤ 0: all SMs; else the tensor-core kernels use at most this many       default 0 */
+  RF_OPT_COMM_SMS = 11,    /* NCCL G5: SMs kept free of K4 for the overlapped reduce-scatter         default 8 */
+  RF_OPT_VERBOSE = 12,     /* 1: print launch geometry to stderr                                     default 0 */
+  RF_OPT_G5_PHASES = 13,   /* TEST HOOK, peers: which half of a collective rf_gram to enqueue — 1: K3 + K4 stores +
+                              arrival flags, 2: the arrival waits + owner-side sum + release flags, 3: both (default).
+                              Emulating R ranks on ONE GPU in one process: call phase 1 for every rank, then phase 2,
+                              on one stream, so no stream-memory wait ever heads a queue its producer sits behind */
+  RF_OPT_COUNT = 14
+} rf_opt;
+rf_status rf_ctx_set_option(rf_ctx* ctx, rf_opt opt, int64_t value);
+rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);
+
+/* =============================================================================================
+ * G5 — the multi-GPU G.  G is a sum over the m features (Eq. def_Gram):
+ * rank r holds W rows [m0, m1), computes the partial G_r = (1/m_total) Σ_{k ∈ its rows} σ(Xᵀw_k)σ(w_kᵀX), and
+ * G = Σ_r G_r.  With a collective attached to the context, rf_gram(ctx, …, RF_OUT_PACKED_TILES, G = recv, …) is a
+ * COLLECTIVE (every rank calls it with the same p, n, m_total, act, prec; its own W rows): K3 + K4 run on the rank's
+ * features and K4's epilogue writes each upper-triangle 256×256 tile of the partial straight into its exchange
+ * slot; the call returns (enqueued) with recv = this rank's owned tiles, SUMMED over all ranks.
+ *
+ * Tile ownership (rf_tile_map; a function of n and world only): the T = ⌈n/256⌉ row tiles are cut into C ≤ 16
+ * chunks of whole 8-row-tile groups with near-equal triangle area; inside chunk c the upper 256-tiles (I, J ≥ I) are
+ * numbered row-major, u = 0, 1, …, and tile u goes to owner u mod world at slot u div world.  recv holds, chunk after
+ * chunk, chunk_slots[c] = ⌈tiles_c / world⌉ tiles of 65536 floats (row-major 256 × 256); slot s of the whole buffer
+ * is the pair (I, J) rf_tile_map returns, or (−1, −1) for a padding slot (content unspecified).  Whole tiles are
+ * stored: a diagonal tile also holds the mirror entries below the diagonal, entries with i or j ≥ n are 0.
+ *
+ * Two exchanges, chosen by what is attached:
+ *   PEERS (the product path): each rank's context owns a staging buffer (world × recv floats + flags, one
+ *     cudaMalloc); ranks exchange 64-byte CUDA IPC handles (rf_ctx_peer_handle / rf_ctx_open_peers) or, in one
+ *     process, raw pointers (rf_ctx_peer_base / rf_ctx_connect_peers).  K4's epilogue stores every tile into its
+ *     owner's staging buffer over NVLink as it finishes (the exchange overlaps the SYRK, no collective kernel), then
+ *     device epoch flags (peer-mapped words written with system-scope release by a one-thread kernel, awaited with
+ *     stream-memory waits) order the owner-side sum in rank order (deterministic) and the next call's stores —
+ *     no host synchronization, no barrier.
+ *   NCCL (the baseline): K4 writes a packed send buffer (in the workspace) chunk by chunk and bumps a per-chunk
+ *     counter; on the context's communication stream each chunk's ncclReduceScatter waits (stream-memory wait) for
+ *     its counter, so chunk c is reduced while K4 computes chunk c + 1.  K4 leaves RF_OPT_COMM_SMS SMs free.
+ * rf_gram with RF_OUT_UPPER / RF_OUT_FULL on such a context computes the rank's PARTIAL G (no exchange).
+ * ============================================================================================= */
+#define RF_PACK_TILE 256
+#define RF_MAX_PEERS 16
+/* Host.  *tiles_owned = the receive slots of `rank` (padding included); ij_pairs (nullable, 2·slots int64): (I, J)
+ * of each slot in recv order, (−1, −1) for padding.  tile must be 256.  n > 0, 1 ≤ world ≤ 4096, 0 ≤ rank < world. */
+rf_status rf_tile_map(int64_t n, int32_t tile, int32_t world, int32_t rank, int64_t* tiles_owned, int64_t* ij_pairs);
+
+/* NCCL.  rf_nccl_get_unique_id: a new ncclUniqueId (128 bytes) on one rank, to be broadcast by the caller's process
+ * group; rf_ctx_init_nccl: every rank creates the communicator from it (ncclCommInitRank; owned by the context).
+ * rf_ctx_attach_nccl: use a caller-owned ncclComm_t instead (kept until rf_ctx_destroy, not destroyed by it).
+ * NCCL is taken from the process (dlopen "libnccl.so.2": the copy torch loads); absent → RF_E_NCCL.  Every collective
+ * rf_gram first polls ncclCommGetAsyncError: an error → RF_E_NCCL. */
+rf_status rf_nccl_get_unique_id(uint8_t id128[128]);
+rf_status rf_ctx_init_nccl(rf_ctx* ctx, const uint8_t id128[128], int32_t rank, int32_t world);
+rf_status rf_ctx_attach_nccl(rf_ctx* ctx, void* nccl_comm, int32_t rank, int32_t world);
+
+/* Peers.  rf_ctx_attach_peers: allocate this rank's staging buffer for n ≤ n_max (world ≤ RF_MAX_PEERS; zero-filled).
+ * rf_ctx_peer_handle: its 64-byte CUDA IPC handle (the handle names exactly that allocation).
+ * rf_ctx_open_peers: map the other ranks' buffers from their handles (handles64 = world × 64 bytes, rank order; the
+ *   own entry is ignored).  rf_ctx_peer_base / rf_ctx_connect_peers: the same with raw device pointers, for ranks
+ *   that share one address space (several contexts in one process).  Every rank's context must be attached with
+ *   the same world and n_max. */
+rf_status rf_ctx_attach_peers(rf_ctx* ctx, int32_t rank, int32_t world, int64_t n_max);
+rf_status rf_ctx_peer_handle(const rf_ctx* ctx, uint8_t handle64[64]);
+rf_status rf_ctx_open_peers(rf_ctx* ctx, const uint8_t* handles64);
+rf_status rf_ctx_peer_base(const rf_ctx* ctx, void** base);
+rf_status rf_ctx_connect_peers(rf_ctx* ctx, void* const* bases);
+/* rank, world and exchange of a context: *mode = 0 none, 1 NCCL, 2 peers (NULL outputs skipped). */
+rf_status rf_ctx_collective(const rf_ctx* ctx, int32_t* rank, int32_t* world, int32_t* mode);
+
+/* rf_workspace_size — bytes of workspace a call needs (op 0: rf_gram, 1: rf_phi_closed_form / rf_phi_eq2) for these
+ * sizes on this context: rf_gram with RF_OUT_PACKED_TILES on an NCCL context also holds the packed send buffer. */
+rf_status rf_workspace_size(const rf_ctx* ctx, int32_t op, int64_t p, int64_t n, int64_t m_local, rf_prec prec,
+                            rf_out out, size_t* bytes);
+
 /* ---------------------------------------------------------------------------------------------
  * rf_moments — host, synchronous.  Gauss–Hermite quadrature (probabilists' weight) by Golub–Welsch;
  * nodes = 0 → adaptive (N = 64, 128, 256, 512 until the table changes by < 1e-13, else trapezoid on
@@ -123,7 +228,7 @@ rf_status rf_moments(rf_act act, double tau, int32_t nodes, rf_moments_t* out);
  * Synchronizes `stream` (8-byte D2H copy into *tau_out, a host pointer).
  */
 rf_status rf_tau_workspace_size(int64_t n, size_t* bytes);
-rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n,
+rf_status rf_estimate_tau(rf_ctx* ctx, const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n,
                           double* tau_out, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
@@ -137,7 +242,7 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
  *   buffers, ld < cols or misalignment → RF_E_INVALID.  Use it on X and W before rf_gram /
  *   rf_phi_closed_form in BF16 mode when the data are fp32.
  */
-rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
+rf_status rf_round_bf16(rf_ctx* ctx, const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
                         void* stream);
 
 /* ---------------------------------------------------------------------------------------------
@@ -146,9 +251,13 @@ rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t col
  *   W_local device, m_local × p (ldw): this rank's rows of W (m_local = m_total on one GPU).  The
  *           sum over the rank's features is scaled by 1/m_total so that summing the partial G of all
  *           ranks (reduce-scatter / all-reduce) gives G.
- *   G       device, n × n (ldg), f64 in RF_PREC_FP64 else f32; `out` selects UPPER or FULL.
- *   ws      device workspace ≥ rf_gram_workspace_size(p, n, m_local, prec) bytes, 256-B aligned
- *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode).
+ *   G       device, n × n (ldg), f64 in RF_PREC_FP64 else f32; `out` selects UPPER or FULL (or a centred form,
+ *           or PACKED_TRI).  RF_OUT_PACKED_TILES (context with a collective attached, BF16 / TF32; 3XTF32 on NCCL
+ *           only): G is this rank's receive buffer of rf_tile_map(n, 256, world, rank) slots × 65536 floats, ldg
+ *           ignored, and the call is the collective described under G5 above.
+ *   ws      device workspace ≥ rf_workspace_size(ctx, 0, p, n, m_local, prec, out) bytes, 256-B aligned
+ *           (holds Σᵀ = σ(XᵀW_localᵀ), n × m_local, never written to HBM in fp32 in BF16 mode; and the NCCL send
+ *           buffer).  rf_gram_workspace_size(p, n, m_local, prec) is the same number for a context without NCCL.
  * Pipeline: [3XTF32: K2 split X, W] → K3 fused Σᵀ = σ(X·Wᵀ) (tcgen05 GEMM, σ in the epilogue)
  *           → K4 upper-triangular SYRK G = ΣᵀΣ/m over 256×512 CTA-pair tiles with j ≥ i (3XTF32:
  *           256×256 tiles, K cut into chunks of 128 features whose partial sums are added in fp32, in TMEM, to
@@ -157,7 +266,7 @@ rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t col
  *            size, any ldg ≥ n (16-B vector stores are used where rows allow); ws 256-B aligned.
  */
 rf_status rf_gram_workspace_size(int64_t p, int64_t n, int64_t m_local, rf_prec prec, size_t* bytes);
-rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
+rf_status rf_gram(rf_ctx* ctx, const void* X, int64_t ldx, const void* W_local, int64_t ldw,
                   int64_t p, int64_t n, int64_t m_local, int64_t m_total,
                   rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg,
                   void* ws, size_t ws_bytes, void* stream);
@@ -175,7 +284,7 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
  *   mom  != NULL: used as given (its tau must equal the τ used).  NULL: rf_moments(act, τ, 0).
  *   Phi  device, n × n (ldphi), f64 in RF_PREC_FP64 else f32.  UPPER writes j ≥ i of rows in range;
  *        FULL additionally writes the mirror Φ[j][i] = Φ[i][j] (only rows/cols the range covers).
- *   ws   ≥ rf_phi_workspace_size(p, n, prec).
+ *   ws   ≥ rf_phi_workspace_size(p, n, prec) = rf_workspace_size(ctx, 1, p, n, 0, prec, out).
  * Pipeline: K1 row norms (fp64) [+ τ̂] → per-row coefficients → K5 fused XᵀX (tcgen05 CTA pairs,
  *           256×256 upper-triangle tiles) + EQ1 epilogue with TMA stores.
  * A zero-norm sample makes v_b undefined: with tau <= 0 (the call synchronizes anyway) it is detected →
@@ -183,7 +292,7 @@ rf_status rf_gram(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
  * (R23: v_b = 0, u_b = ‖x_j‖, diagonal u_a = v_b = u_b = 0), so every entry of Φ stays finite.
  */
 rf_status rf_phi_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes);
-rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
+rf_status rf_phi_closed_form(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n,
                              rf_act act, double tau, const rf_moments_t* mom,
                              rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                              void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream);
@@ -192,7 +301,7 @@ rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n,
  * paper carries to Theorem 1 (NEXT-3):
  *   Φ2 = ⟨0,0⟩² + ⟨0,0⟩⟨1,1⟩(α + β) + ⟨1,1⟩²αβ + ⟨0,1⟩⟨1,0⟩ν + ⟨0,2⟩⟨2,0⟩ν²/2.
  * Same arguments, layouts, workspace (rf_phi_workspace_size) and errors. */
-rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+rf_status rf_phi_eq2(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
                      const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                      void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream);
 
@@ -202,90 +311,6 @@ rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act ac
  * area (row i carries n − i entries).  Host only.
  */
 rf_status rf_phi_row_split(int64_t n, int32_t world, int32_t rank, int64_t* row_begin, int64_t* row_end);
-
-/* =============================================================================================
- * G5 — multi-GPU G: feature sharding + reduce-scatter of PACKED TRIANGLE TILES.
- * G is a sum over the m features (Eq. def_Gram), so rank r computes the partial
- * G_r = (1/m_total) Σ_{k ∈ its W rows} σ(Xᵀw_k)σ(w_kᵀX) and G = Σ_r G_r.  Instead of a dense n×n partial,
- * rf_gram_packed has K4 write each 256×256 tile (I, J ≥ I … see below) of the partial straight into a
- * SEND buffer laid out for ncclReduceScatter:
- *
- *   chunk-major:  send = [chunk 0 | chunk 1 | …],  chunk c = [owner 0 | owner 1 | … | owner R−1],
- *                 owner block = chunk_slots[c] tiles of 256×256 fp32, row-major inside a tile (ld 256).
- *
- * Chunks are runs of K4's 256-row raster groups in schedule order, so chunk c is complete early in the
- * launch; within a chunk, the tiles (in K4's schedule order, u = 0, 1, …) are dealt round-robin to owners
- * (owner = u mod R, slot = u div R), which balances the ownership to ±1 tile per chunk.  A reduce-scatter of
- * chunk c (count = chunk_slots[c]·65536 per rank) leaves rank r with the SUMMED tiles of its slots, at
- * chunk_recv_off[c] of its receive buffer.  rf_pack_tile_map says which tile each received slot is.
- * Every tile K4 computes is stored whole, so a slot holds valid G entries everywhere (tiles that straddle
- * the diagonal hold both G[i][j] and its mirror; entries with i or j ≥ n are 0).  The set of tiles covers
- * every entry (i, j) with j ≥ i at least once.
- *
- * Overlap: K4 counts finished tiles per chunk in `chunk_sync` (device uint32[nchunks], zeroed by the caller
- * before the first epoch); rf_stream_wait_chunk enqueues on a (communication) stream a wait until chunk c of
- * call `epoch` (1, 2, … per rf_gram_packed call with the same chunk_sync) is complete, after which that
- * stream may run the reduce-scatter of chunk c while K4 continues with chunk c+1.  Launch K4 on max_sms < all
- * SMs so the collective's kernels have SMs to run on.
- * ============================================================================================= */
-#define RF_PACK_TILE 256
-#define RF_PACK_MAX_CHUNKS 64
-typedef struct {
-  int64_t n;
-  int32_t world, nchunks;
-  int32_t prec;                                   /* rf_prec the plan was made for (K4 tile width) */
-  int32_t tiles_per_pair;                         /* 256×256 tiles per K4 pair tile (2 = 256×512 pair tiles) */
-  int64_t pair_tiles;                             /* K4 pair tiles in the triangle schedule */
-  int64_t send_elems;                             /* fp32 elements of the send buffer */
-  int64_t recv_elems;                             /* fp32 elements each rank receives */
-  int64_t chunk_tile0[RF_PACK_MAX_CHUNKS + 1];    /* first pair tile (schedule index) of chunk c */
-  int64_t chunk_slots[RF_PACK_MAX_CHUNKS];        /* 256×256 slots per owner in chunk c */
-  int64_t chunk_send_off[RF_PACK_MAX_CHUNKS + 1]; /* element offset of chunk c in the send buffer */
-  int64_t chunk_recv_off[RF_PACK_MAX_CHUNKS + 1]; /* element offset of chunk c in a receive buffer */
-} rf_pack_plan_t;
-
-/* Host.  nchunks ≤ RF_PACK_MAX_CHUNKS (clamped to the number of raster groups); prec ∈ {BF16, TF32, 3XTF32}. */
-rf_status rf_pack_plan(int64_t n, int32_t world, int32_t nchunks, rf_prec prec, rf_pack_plan_t* out);
-/* Host.  rc[2·s], rc[2·s+1] = (row tile I, column tile J) of receive slot s of `rank` (256-row/col tiles;
- * entry (i, j) of G is element ((i − 256 I)·256 + (j − 256 J)) of the slot), or (−1, −1) for padding slots.
- * rc holds 2 · recv_elems / 65536 int32. */
-rf_status rf_pack_tile_map(const rf_pack_plan_t* plan, int32_t rank, int32_t* rc);
-/* rf_gram's K3 + K4 with packed output (plan->prec must equal prec, plan->n must equal n).
- *   send        device fp32[plan->send_elems]; every slot that holds a tile is written whole; padding
- *               slots (rf_pack_tile_map gives (−1, −1)) are left untouched (their reduced value is garbage
- *               and must be ignored).
- *   chunk_sync  device uint32[plan->nchunks]; K4 adds 16 per finished pair tile (8 epilogue warps × 2 CTAs).
- *   epoch       1-based count of calls made with this chunk_sync.
- *   max_sms     ≤ 0: all SMs; else K4/K3 use at most this many SMs (rounded down to CTA pairs).
- * ws as rf_gram (rf_gram_workspace_size). */
-rf_status rf_gram_packed(const void* X, int64_t ldx, const void* W_local, int64_t ldw,
-                         int64_t p, int64_t n, int64_t m_local, int64_t m_total, rf_act act, rf_prec prec,
-                         const rf_pack_plan_t* plan, int32_t max_sms, float* send, uint32_t* chunk_sync,
-                         uint32_t epoch, void* ws, size_t ws_bytes, void* stream);
-/* Enqueue on `stream` a wait until chunk_sync[chunk] ≥ 16 · epoch · (pair tiles of chunk) (driver
- * stream-memory wait; wrap-safe comparison).  Returns immediately on the host. */
-rf_status rf_stream_wait_chunk(const rf_pack_plan_t* plan, const uint32_t* chunk_sync, int32_t chunk,
-                               uint32_t epoch, void* stream);
-
-/* Fused G5 over peer memory (the product path for R > 1; the NCCL chunks above are the baseline).
- * rf_gram_packed_p2p runs K3 + K4 with the packed epilogue storing every 256×256 tile of this rank's partial G
- * directly into its OWNER's staging buffer: staging[o] is the device-visible base pointer (this process's mapping,
- * e.g. rf_ipc_open, or its own buffer for o = rank) of rank o's staging buffer of world · plan->recv_elems floats,
- * laid out [source rank][receive slot][65536] — the stores cross NVLink as tiles finish, overlapped with the
- * SYRK, and no collective kernel runs.  After every rank's call has completed (stream synchronize + a barrier of
- * the caller's process group), each owner sums its staging buffer in rank order with rf_pack_reduce into recv
- * (plan->recv_elems floats; same layout and rf_pack_tile_map as the NCCL path; deterministic).
- * BF16 / TF32 only (3XTF32's K-chunked accumulation would read tiles back over NVLink); world ≤ 16. */
-rf_status rf_gram_packed_p2p(const void* X, int64_t ldx, const void* W_local, int64_t ldw, int64_t p, int64_t n,
-                             int64_t m_local, int64_t m_total, rf_act act, rf_prec prec, const rf_pack_plan_t* plan,
-                             int32_t rank, float* const* staging, int32_t max_sms, void* ws, size_t ws_bytes,
-                             void* stream);
-rf_status rf_pack_reduce(const rf_pack_plan_t* plan, const float* staging_self, float* recv, void* stream);
-/* CUDA IPC plumbing for the staging buffers (64-byte handles exchanged by the caller's process group). */
-rf_status rf_ipc_handle(const void* dptr, uint8_t* handle64);
-rf_status rf_ipc_open(const uint8_t* handle64, void** dptr);
-rf_status rf_ipc_close(void* dptr);
-
 
 /* =============================================================================================
  * NEXT-2 — Theorem 1's asymptotic equivalent K̃ (EQ6):
@@ -300,7 +325,7 @@ rf_status rf_ipc_close(void* dptr);
  *   out RF_OUT_UPPER or RF_OUT_FULL;  Kt device f32 n × n (ldk).  ws ≥ rf_ktilde_workspace_size(p, n, prec).
  * Async on `stream`. */
 rf_status rf_ktilde_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* bytes);
-rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv, int32_t kv,
+rf_status rf_ktilde(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv, int32_t kv,
                     const double* A, double d0, double d1, double d2, rf_prec prec, rf_out out, float* Kt, int64_t ldk,
                     void* ws, size_t ws_bytes, void* stream);
 
@@ -327,7 +352,7 @@ rf_status rf_trf_thresholds_for(rf_act act, double tau, double* s_minus, double*
  *   exact) and compared with t± = s±/c rounded to fp32; an entry whose exact z lies within the fp32 rounding
  *   of z of a threshold may decide either way (the tests bound that band).
  *   features: device, 16-B aligned, ldf ≥ m_local bytes, ldf % 16 == 0.  Async on `stream`. */
-rf_status rf_ter_features(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
+rf_status rf_ter_features(rf_ctx* ctx, const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
                           int64_t m_local, double eps, double s_minus, double s_plus, void* features, int64_t ldf,
                           void* stream);
 /* rf_gram_ter — G^ter = (1/m_total) Σ^terᵀ Σ^ter over this rank's m_local features (UPPER / FULL like rf_gram).
@@ -336,7 +361,7 @@ rf_status rf_ter_features(const void* X, int64_t ldx, const void* T, int64_t ldt
  * products and their sums are exact in fp32 (m_local ≤ 2^24), so m_total·G^ter is an exact integer count of the
  * decided features.  ws ≥ rf_gram_ter_workspace_size(p, n, m_local). */
 rf_status rf_gram_ter_workspace_size(int64_t p, int64_t n, int64_t m_local, size_t* bytes);
-rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n, int64_t m_local,
+rf_status rf_gram_ter(rf_ctx* ctx, const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n, int64_t m_local,
                       int64_t m_total, double eps, double s_minus, double s_plus, rf_out out, float* G, int64_t ldg,
                       void* ws, size_t ws_bytes, void* stream);
 
@@ -348,7 +373,7 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
  * in fp32 in the epilogue; 0 = one chunk.  ws ≥ rf_debug_gemm_workspace_size() (3XTF32 split operands).
  */
 rf_status rf_debug_gemm_workspace_size(int64_t M, int64_t N, int64_t K, rf_prec prec, size_t* bytes);
-rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
+rf_status rf_debug_gemm_nt(rf_ctx* ctx, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
                            rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
                            void* stream);
 
@@ -370,7 +395,7 @@ rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ld
  * Synchronous at the end (one event wait, through mapped host memory) to report the factorisation:
  * G_train + γI not positive definite (a non-positive pivot) → RF_E_NONFINITE. */
 rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes);
-rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
+rf_status rf_ridge(rf_ctx* ctx, const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
                    int32_t n_gamma, const double* Y, int64_t ldy, int32_t nrhs, double* alpha, double* Yhat,
                    void* ws, size_t ws_bytes, void* stream);
 

@@ -2,6 +2,12 @@
 // mainloop test hook and Φ's workspace size (include/rf.h).
 #pragma once
 
+namespace {
+rf_status gram_collective(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n, int64_t m_local,
+                          int64_t m_total, rf_act act, rf_prec prec, float* recv, void* ws, size_t ws_bytes,
+                          cudaStream_t st);
+}
+
 // =================================================================================================
 extern "C" {
 
@@ -124,9 +130,10 @@ static rf_status tau_reduce_to_host(const double* nrm2, int64_t n, double* out_d
   return RF_OK;
 }
 
-rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n, double* tau_out, void* ws,
-                          size_t ws_bytes, void* stream) {
+rf_status rf_estimate_tau(rf_ctx* ctx, const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, int64_t n, double* tau_out,
+                          void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_estimate_tau: p, n must be > 0");
   if (!tau_out) return fail(RF_E_INVALID, "rf_estimate_tau: tau_out is NULL");
   if (x_dt < RF_DT_F64 || x_dt > RF_DT_BF16) return fail(RF_E_INVALID, "rf_estimate_tau: bad dtype");
@@ -148,9 +155,10 @@ rf_status rf_estimate_tau(const void* X, rf_dtype x_dt, int64_t ldx, int64_t p, 
   return ok();
 }
 
-rf_status rf_round_bf16(const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
+rf_status rf_round_bf16(rf_ctx* ctx, const float* src, int64_t lds, int64_t rows, int64_t cols, void* dst, int64_t ldd,
                         void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   if (rows < 0 || cols < 0) return fail(RF_E_INVALID, "rf_round_bf16: rows, cols must be >= 0");
   if (rows == 0 || cols == 0) return ok();
   if (!src || !dst) return fail(RF_E_INVALID, "rf_round_bf16: NULL buffer");
@@ -182,7 +190,8 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
     return fail(RF_E_INVALID, "rf_gram: sizes must be < 2^31");
   if (!valid_act(act)) return fail(RF_E_INVALID, "rf_gram: unknown activation %d", (int)act);
   if (!valid_prec(prec)) return fail(RF_E_INVALID, "rf_gram: unknown precision %d", (int)prec);
-  if (!valid_out(out)) return fail(RF_E_INVALID, "rf_gram: unknown output mode %d", (int)out);
+  if (!valid_out(out) || out == RF_OUT_PACKED_TILES)
+    return fail(RF_E_INVALID, "rf_gram: unknown output mode %d", (int)out);
   const size_t es = esize_of(prec);
   rf_status s;
   if ((s = validate_matrix("X", X, ldx, p, es))) return s;
@@ -226,18 +235,18 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
   }
 
   // Tensor-core path: [K2 split] → K3 (pair tiles 256×256, σ epilogue) → K4 (triangle, SYRK epilogue)
-  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, full, (float*)G, ldg, w, pl, dev.sms, st, nullptr, tri_T};
-  if (prec == RF_PREC_BF16) return gram_tc<1, 1, 512, 0>(ga, kchunk_for(prec, 0));
-  if (prec == RF_PREC_TF32) return gram_tc<2, 1, 512, 1>(ga, kchunk_for(prec, 0));
-  // 3×TF32: chunks of 4 K-blocks (128 features) bound the truncating tensor-pipe accumulation to
-  // ≈ 2.6e-6 relative (scripts/accum_experiment.py).
-  return gram_tc<2, 3, 256, 2>(ga, kchunk_for(prec, 4));
-  return ok();
+  GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, full, (float*)G, ldg, w, pl, usable_sms(dev.sms), st,
+                nullptr, tri_T};
+  return gram_tc_dispatch(ga, prec);
 }
 
-rf_status rf_gram(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n, int64_t m_local,
-                  int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg, void* ws,
+rf_status rf_gram(rf_ctx* ctx, const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t p, int64_t n,
+                  int64_t m_local, int64_t m_total, rf_act act, rf_prec prec, rf_out out, void* G, int64_t ldg, void* ws,
                   size_t ws_bytes, void* stream) {
+  RF_CTX_ENTER(ctx);
+  if (out == RF_OUT_PACKED_TILES)   // G5: the collective (abi_ctx.cuh)
+    return gram_collective(X, ldx, W, ldw, p, n, m_local, m_total, act, prec, (float*)G, ws, ws_bytes,
+                           (cudaStream_t)stream);
   rf_status s = rf_gram_core(X, ldx, W, ldw, p, n, m_local, m_total, act, prec, out, G, ldg, ws, ws_bytes, stream);
   if (s || !((int)out & RF_OUT_CENTER)) return s;
   // NEXT-2: K = P·G·P (Eq. (2)).  Centering is linear, so each rank may center its own partial G.
@@ -257,10 +266,11 @@ rf_status rf_debug_gemm_workspace_size(int64_t M, int64_t N, int64_t K, rf_prec 
   return ok();
 }
 
-rf_status rf_debug_gemm_nt(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K,
-                           rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
+rf_status rf_debug_gemm_nt(rf_ctx* ctx, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N,
+                           int64_t K, rf_prec prec, int32_t kchunk, float* C, int64_t ldc, void* ws, size_t ws_bytes,
                            void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   if (M <= 0 || N <= 0 || K <= 0) return fail(RF_E_INVALID, "rf_debug_gemm_nt: M, N, K must be > 0");
   if (prec != RF_PREC_BF16 && prec != RF_PREC_TF32 && prec != RF_PREC_3XTF32)
     return fail(RF_E_INVALID, "rf_debug_gemm_nt: tensor-core precisions only (BF16, TF32, 3XTF32)");

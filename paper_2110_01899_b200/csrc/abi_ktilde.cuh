@@ -37,10 +37,11 @@ rf_status rf_ktilde_workspace_size(int64_t p, int64_t n, rf_prec prec, size_t* b
   return ok();
 }
 
-rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv, int32_t kv,
-                    const double* A, double d0, double d1, double d2, rf_prec prec, rf_out out, float* Kt, int64_t ldk,
-                    void* ws, size_t ws_bytes, void* stream) {
+rf_status rf_ktilde(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n, const float* V, int64_t ldv,
+                    int32_t kv, const double* A, double d0, double d1, double d2, rf_prec prec, rf_out out, float* Kt,
+                    int64_t ldk, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   if (p <= 0 || n <= 0) return fail(RF_E_INVALID, "rf_ktilde: p, n must be > 0");
   if (n >= (int64_t(1) << 31) || p >= (int64_t(1) << 31)) return fail(RF_E_INVALID, "rf_ktilde: sizes must be < 2^31");
   if (kv < 0 || kv > rfk::kMaxKv) return fail(RF_E_INVALID, "rf_ktilde: kv must be in [0, %d]", rfk::kMaxKv);
@@ -111,12 +112,12 @@ rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const floa
     if (bf) {
       using C = rfk::TcCfg<1, 1, 256, 1, 2, 16>;
       rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-      sc.load_pol = env_int("RF_KT_LOADPOL", 1);   // evict_last operands (4.18 → 4.14 ms)
+      sc.load_pol = 1;   // evict_last operands (4.18 → 4.14 ms)
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     } else {
       using C = rfk::TcCfg<2, 1, 256, 1, 2, 16>;
       rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-      sc.load_pol = env_int("RF_KT_LOADPOL", 1);   // evict_last operands (4.18 → 4.14 ms)
+      sc.load_pol = 1;   // evict_last operands (4.18 → 4.14 ms)
       if ((s = launch_tc<C>("KT_ktilde", tA, tA, tA, tA, tO, sc, e, dev.sms, st))) return s;
     }
   } else {
@@ -128,7 +129,7 @@ rf_status rf_ktilde(const void* X, int64_t ldx, int64_t p, int64_t n, const floa
     if ((s = make_tmap(&tAl, Xl, false, n, p, pl.ldp, 128))) return s;
     if (!tma_out) tO = tA;
     rfk::Sched sc = rfk::Sched::make(1, 256, 0, tn, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-      sc.load_pol = env_int("RF_KT_LOADPOL", 1);   // evict_last operands (4.18 → 4.14 ms)
+      sc.load_pol = 1;   // evict_last operands (4.18 → 4.14 ms)
     if ((s = launch_tc<C>("KT_ktilde", tA, tA, tAl, tAl, tO, sc, e, dev.sms, st))) return s;
   }
   return ok();

@@ -38,7 +38,8 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   if (n > (int64_t)1 << 31 || p > (int64_t)1 << 31) return fail(RF_E_INVALID, "rf_phi_closed_form: sizes must be < 2^31");
   if (!valid_act(act)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown activation %d", (int)act);
   if (!valid_prec(prec)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown precision %d", (int)prec);
-  if (!valid_out(out)) return fail(RF_E_INVALID, "rf_phi_closed_form: unknown output mode %d", (int)out);
+  if (!valid_out(out) || out == RF_OUT_PACKED_TILES)
+    return fail(RF_E_INVALID, "rf_phi_closed_form: unsupported output mode %d", (int)out);
   if (row_begin < 0 || row_end > n || row_begin > row_end || (row_begin % 256) != 0 ||
       (row_end != n && (row_end % 256) != 0))
     return fail(RF_E_INVALID, "rf_phi_closed_form: row range [%lld, %lld) must satisfy 0 <= begin <= end <= n, "
@@ -136,8 +137,8 @@ static rf_status rf_phi_core(const void* X, int64_t ldx, int64_t p, int64_t n, r
   const bool odd_act = act == RF_ACT_TANH || act == RF_ACT_ERF || act == RF_ACT_SIGMOID_HALF || act == RF_ACT_SIGN ||
                        act == RF_ACT_SIN || act == RF_ACT_IDENT;
   K5Args ka{X, ldx, p, n, prec, (float*)Phi, ldphi, full, rc, nj, (float)e0, (float)e1, (float)e2, (float)f0,
-            (float)f1, row_begin, row_end, w, pl, dev.sms, st, tri_T};
-  if (odd_act && env_int("RF_EQ1_GENERAL", 0) == 0) return launch_k5<true>(ka);
+            (float)f1, row_begin, row_end, w, pl, usable_sms(dev.sms), st, tri_T};
+  if (odd_act && opt(RF_OPT_EQ1_GENERAL) == 0) return launch_k5<true>(ka);
   return launch_k5<false>(ka);
 }
 
@@ -157,15 +158,17 @@ static rf_status phi_entry(const void* X, int64_t ldx, int64_t p, int64_t n, rf_
   return s ? s : ok();
 }
 
-rf_status rf_phi_closed_form(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+rf_status rf_phi_closed_form(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
                              const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                              void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  RF_CTX_ENTER(ctx);
   return phi_entry(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes, stream, 1);
 }
 
-rf_status rf_phi_eq2(const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
+rf_status rf_phi_eq2(rf_ctx* ctx, const void* X, int64_t ldx, int64_t p, int64_t n, rf_act act, double tau,
                      const rf_moments_t* mom, rf_prec prec, rf_out out, int64_t row_begin, int64_t row_end,
                      void* Phi, int64_t ldphi, void* ws, size_t ws_bytes, void* stream) {
+  RF_CTX_ENTER(ctx);
   return phi_entry(X, ldx, p, n, act, tau, mom, prec, out, row_begin, row_end, Phi, ldphi, ws, ws_bytes, stream, 2);
 }
 

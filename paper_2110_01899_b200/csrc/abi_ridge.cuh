@@ -22,10 +22,11 @@ rf_status rf_ridge_workspace_size(int64_t n_train, size_t* bytes) {
   return ok();
 }
 
-rf_status rf_ridge(const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
+rf_status rf_ridge(rf_ctx* ctx, const float* G, int64_t ldg, int64_t n_train, int64_t n_test, const double* gammas,
                    int32_t n_gamma, const double* Y, int64_t ldy, int32_t nrhs, double* alpha, double* Yhat,
                    void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   if (!G || !Y || !alpha || !gammas) return fail(RF_E_INVALID, "rf_ridge: G, Y, alpha and gammas are required");
   if (n_train <= 0 || n_test < 0 || nrhs <= 0 || n_gamma <= 0)
     return fail(RF_E_INVALID, "rf_ridge: need n_train > 0, n_test >= 0, nrhs > 0, n_gamma > 0");

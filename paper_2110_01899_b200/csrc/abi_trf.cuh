@@ -45,7 +45,7 @@ rf_status launch_k3_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, 
   const double inv_c = std::sqrt(1.0 - eps);   // t± = s± / c, c = (1 − ε)^{-1/2}
   rfk::EpiSigmaTer e{feat, ldf, n, m_local, (float)(s_minus * inv_c), (float)(s_plus * inv_c)};
   const int kb = (int)((p + C3::BK - 1) / C3::BK);
-  if (prog && env_int("RF_K3_MC", 1)) {   // multicast + pair hybrid (workspace progress words available)
+  if (prog && opt(RF_OPT_K3_HYBRID)) {   // multicast + pair hybrid (workspace progress words available)
     using C3m = rfk::TcCfg<1, 1, 256, 0, 4>;
     CUtensorMap tBh;
     if ((s = make_tmap(&tBh, T, true, m_local, p, ldt, 64))) return s;
@@ -56,7 +56,7 @@ rf_status launch_k3_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, 
   }
   rfk::Sched sc =
       rfk::Sched::make(0, 256, 0, (int)((n + 255) / 256), (int)((m_local + 255) / 256), kb, 0, raster_gm(8, 3));
-  sc.load_pol = env_int("RF_K3_LOADPOL", 1);
+  sc.load_pol = 1;
   return launch_tc<C3>("K3_ter_features", tA, tB, tA, tB, tA, sc, e, sms, st);
 }
 }  // namespace
@@ -89,10 +89,11 @@ rf_status rf_gram_ter_workspace_size(int64_t p, int64_t n, int64_t m_local, size
   return ok();
 }
 
-rf_status rf_ter_features(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
+rf_status rf_ter_features(rf_ctx* ctx, const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
                           int64_t m_local, double eps, double s_minus, double s_plus, void* features, int64_t ldf,
                           void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   rf_status s;
   if ((s = ter_validate("rf_ter_features", X, ldx, T, ldt, p, n, m_local, eps, s_minus, s_plus))) return s;
   if (!features || !aligned16(features) || ldf < m_local || (ldf % 16) != 0)
@@ -105,16 +106,18 @@ rf_status rf_ter_features(const void* X, int64_t ldx, const void* T, int64_t ldt
   return ok();
 }
 
-rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n, int64_t m_local,
-                      int64_t m_total, double eps, double s_minus, double s_plus, rf_out out, float* G, int64_t ldg,
-                      void* ws, size_t ws_bytes, void* stream) {
+rf_status rf_gram_ter(rf_ctx* ctx, const void* X, int64_t ldx, const void* T, int64_t ldt, int64_t p, int64_t n,
+                      int64_t m_local, int64_t m_total, double eps, double s_minus, double s_plus, rf_out out, float* G,
+                      int64_t ldg, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
+  RF_CTX_ENTER(ctx);
   rf_status s;
   if ((s = ter_validate("rf_gram_ter", X, ldx, T, ldt, p, n, m_local, eps, s_minus, s_plus))) return s;
   if (m_total < m_local) return fail(RF_E_INVALID, "rf_gram_ter: m_total < m_local");
   if (m_local > (int64_t(1) << 24))
     return fail(RF_E_INVALID, "rf_gram_ter: m_local > 2^24 (fp32 accumulation of ±1 products is exact below that)");
-  if (!valid_out(out)) return fail(RF_E_INVALID, "rf_gram_ter: unknown output mode %d", (int)out);
+  if (!valid_out(out) || out == RF_OUT_PACKED_TILES)
+    return fail(RF_E_INVALID, "rf_gram_ter: unsupported output mode %d", (int)out);
   int64_t tri_T = 0;
   if (out == RF_OUT_PACKED_TRI) {
     if ((s = packed_out_setup("rf_gram_ter", G, n, RF_PREC_BF16, &tri_T))) return s;
@@ -142,35 +145,23 @@ rf_status rf_gram_ter(const void* X, int64_t ldx, const void* T, int64_t ldt, in
   if (!tma_out) tO = tA;
   const int kb4 = (int)((m_local + C4::BK - 1) / C4::BK);
   rfk::Sched s4 = rfk::Sched::make(1, 512, 0, (int)((n + 255) / 256), (int)((n + 511) / 512), kb4, 0, raster_gm(8, 4));
-  const int lockw = env_int("RF_LOCKW", 24);
+  const int lockw = (int)opt(RF_OPT_LOCK_W);
   if (lockw > 0) {
     s4.prog = (uint32_t*)(w + pl.off_prog);
     s4.lock_w = lockw;
-    s4.lock_ks = std::max(1, env_int("RF_LOCKKS", 8));
+    s4.lock_ks = std::max(1, (int)opt(RF_OPT_LOCK_KS));
     RF_CUDA_CHECK(cudaMemsetAsync(s4.prog, 0, 1024, st));
   }
   rfk::EpiSyrk e4{G, ldg, n, (float)(1.0 / (double)m_total), (int)out & 1, tma_out ? 1 : 0, tri_T};
   bool hyb = false;
-  if (lockw > 0 && env_int("RF_K4TER_MC", 0) == 0) {
+  if (lockw > 0) {
     CUtensorMap tSh;   // Σ^terᵀ with a 64-row box (the 8-CTA multicast kernel's A halves)
     if ((s = make_tmap_es(&tSh, S, 1, n, m_local, pl.ldS, 64))) return s;
     if ((s = launch_k4_hybrid<3>("K4_ter_syrk", tA, tSh, tO, n, kb4, e4, s4.prog, lockw, s4.lock_ks, dev.sms, st,
                                  &hyb)))
       return s;
   }
-  if (hyb) {
-  } else if (env_int("RF_K4TER_MC", 0)) {
-    // 4-CTA clusters, B multicast (DESIGN.md §6 finding 3): the fp8 SYRK runs at full clock and is L2-bound,
-    // so a third less L2 → SM traffic matters more than the SMs the GPC packing of 4-clusters leaves idle.
-    using C4m = rfk::TcCfg<3, 1, 512, -1, 4>;
-    rfk::Sched sm = rfk::Sched::make(1, 256, 0, (int)((n + 511) / 512), (int)((n + 511) / 512), kb4, 0, raster_gm(4, 4));
-    sm.prog = s4.prog;
-    sm.lock_w = s4.lock_w;
-    sm.lock_ks = s4.lock_ks;
-    if ((s = launch_tc<C4m>("K4_ter_syrk", tA, tA, tA, tA, tO, sm, e4, dev.sms, st))) return s;
-  } else if ((s = launch_tc<C4>("K4_ter_syrk", tA, tA, tA, tA, tO, s4, e4, dev.sms, st))) {
-    return s;
-  }
+  if (!hyb && (s = launch_tc<C4>("K4_ter_syrk", tA, tA, tA, tA, tO, s4, e4, dev.sms, st))) return s;
   if ((int)out & RF_OUT_CENTER)
     if ((s = center_pass<float>(G, ldg, n, (int)out & 1, (double*)(w + pl.off_cen), st))) return s;
   return ok();

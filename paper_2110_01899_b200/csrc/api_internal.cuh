@@ -18,10 +18,36 @@
 #include "../../include/rf.h"
 #include "k_aux.cuh"
 #include "k_center.cuh"
+#include "k_comm.cuh"
 #include "k_simt.cuh"
 #include "k_ridge.cuh"
 #include "rf_common.cuh"
 #include "tc_gemm.cuh"
+
+// The context (include/rf.h): device, options, the hybrids' side stream, and the G5 exchange resources.
+struct rf_ctx {
+  int device = 0;
+  int64_t opts[RF_OPT_COUNT];
+  cudaStream_t side = nullptr;            // concurrent tail kernel of the K3 / K4 multicast + pair hybrids
+  // collective (G5)
+  int rank = 0, world = 1, mode = 0;      // mode: 0 none, 1 NCCL, 2 peers
+  uint32_t epoch = 0;                     // collective rf_gram calls made on this context
+  // NCCL
+  void* comm = nullptr;
+  bool own_comm = false;
+  cudaStream_t comm_stream = nullptr;
+  uint32_t* sync = nullptr;               // device: per-chunk counters (monotone across calls)
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  bool comm_pending = false;              // ev_done recorded by an earlier call (its reduce-scatters read the send buffer)
+  // peers: [world × recv_cap floats][flags: arrived[RF_MAX_PEERS], freed[RF_MAX_PEERS]] in one cudaMalloc
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  int64_t recv_cap = 0;
+  float* peer[RF_MAX_PEERS] = {};
+  uint32_t* peer_flags[RF_MAX_PEERS] = {};
+  void* opened[RF_MAX_PEERS] = {};
+  bool connected = false;
+};
 
 namespace rfh {
 int compute_moments(rf_act act, double tau, int nodes, rf_moments_t* out);
@@ -122,7 +148,7 @@ const char* prec_name(rf_prec p) {
 }
 bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
 bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_BUMP; }
-bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_PACKED_TRI; }
+bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_PACKED_TILES; }
 int64_t tri_tiles(int64_t n) {
   const int64_t T = (n + 255) / 256;
   return T * (T + 1) / 2;
@@ -225,28 +251,88 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Row tiles per L2 raster group (tc_gemm.cuh Sched).  Env RF_GM<k> (kernel k = 3, 4, 5) or RF_GM overrides
-// (experiments).
+// ---------------------------------------------------------------- context and options (include/rf.h)
+constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3};
+thread_local rf_ctx* g_ctx = nullptr;     // the context of the call in progress on this thread
+int64_t opt(rf_opt o) { return g_ctx ? g_ctx->opts[o] : kOptDefault[o]; }
+
+rf_status ctx_init(rf_ctx* c, int device) {
+  c->device = device;
+  for (int i = 0; i < RF_OPT_COUNT; ++i) c->opts[i] = kOptDefault[i];
+  int prev = 0;
+  RF_CUDA_CHECK(cudaGetDevice(&prev));
+  RF_CUDA_CHECK(cudaSetDevice(device));
+  cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(RF_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  return RF_OK;
+}
+
+// This thread's default context of `device` (ctx = NULL in a call): per thread, so unrelated threads never share a
+// side stream.
+rf_ctx* default_ctx(int device) {
+  static thread_local rf_ctx* dflt[64] = {};
+  if (device < 0 || device >= 64) return nullptr;
+  if (!dflt[device]) {
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    rf_ctx* c = new rf_ctx();
+    if (ctx_init(c, device) != RF_OK) {
+      delete c;
+      return nullptr;
+    }
+    dflt[device] = c;
+  }
+  return dflt[device];
+}
+
+// Entry guard of every compute call: resolves NULL to the default context, makes the context's device current for
+// the call (restored on exit) and publishes the options to the launchers.
+struct CtxScope {
+  rf_status status = RF_OK;
+  rf_ctx* prev = nullptr;
+  int prev_dev = -1;
+  explicit CtxScope(rf_ctx* c) {
+    prev = g_ctx;
+    g_ctx = nullptr;
+    int dev = 0;
+    if (!c) {
+      // the default context; without a usable device the call runs its argument validation on the default options
+      // and then fails in check_device (RF_E_CUDA / RF_E_UNSUPPORTED) — never a CPU fallback
+      if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
+      c = default_ctx(dev);
+      if (!c) return;
+    } else if (cudaGetDevice(&dev) != cudaSuccess) {
+      status = fail(RF_E_CUDA, "cudaGetDevice failed");
+      return;
+    }
+    if (c->device != dev) {
+      prev_dev = dev;
+      if (cudaSetDevice(c->device) != cudaSuccess) {
+        status = fail(RF_E_CUDA, "cudaSetDevice(%d) failed", c->device);
+        return;
+      }
+    }
+    g_ctx = c;
+  }
+  ~CtxScope() {
+    g_ctx = prev;
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);
+  }
+};
+#define RF_CTX_ENTER(ctx)            \
+  CtxScope ctx_scope_(ctx);          \
+  if (ctx_scope_.status) return ctx_scope_.status
+
+// Row tiles per L2 raster group (tc_gemm.cuh Sched) of kernel K3, K4, K5 (measured best).
 int raster_gm(int def, int kernel = 0) {
-  char name[16];
-  std::snprintf(name, sizeof(name), "RF_GM%d", kernel);
-  const char* e = kernel ? std::getenv(name) : nullptr;
-  if (!(e && *e && std::atoi(e) > 0)) e = std::getenv("RF_GM");
-  if (e && *e && std::atoi(e) > 0) return std::atoi(e);
-  return def;
-}
-
-int env_int(const char* name, int def) {
-  const char* e = std::getenv(name);
-  if (e && *e) return std::atoi(e);
-  return def;
-}
-
-// K-blocks per accumulation chunk (0 = whole K in one chunk).  Env RF_KCHUNK overrides (experiments).
-int kchunk_for(rf_prec prec, int def) {
-  const char* e = std::getenv("RF_KCHUNK");
-  if (e && *e) return std::atoi(e);
-  (void)prec;
+  (void)kernel;
   return def;
 }
 
@@ -279,7 +365,7 @@ rf_status launch_tc(const char* name, const CUtensorMap& a, const CUtensorMap& b
   }
   const int clusters = std::max(1, std::min(s.num_tiles, max_cl));
   cfg.gridDim = dim3(Cfg::CL * clusters);
-  if (env_int("RF_DEBUG_LAUNCH", 0))
+  if (opt(RF_OPT_VERBOSE))
     std::fprintf(stderr, "[rf] %s: %d clusters of %d CTAs (%d SMs), %d tiles\n", name, clusters, Cfg::CL,
                  clusters * Cfg::CL, s.num_tiles);
   RF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, a, b, alo, blo, out, s, epi));
@@ -402,23 +488,16 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   return g;
 }
 
-struct PackArgs {
-  float* send;
-  uint32_t* sync;
-  const rfk::PackDev* dev;
-  int world, nchunks;
-};
-
 struct GramTcArgs {
   const void* X; int64_t ldx; const void* W; int64_t ldw;
   int64_t p, n, m_local, m_total;
   rf_act act; int full; float* G; int64_t ldg;
   char* w; GramPlan pl; int sms; cudaStream_t st;
-  const PackArgs* pack;     // non-null: K4 writes packed tiles (rf_gram_packed)
-  int64_t tri_T = 0;        // > 0: RF_OUT_PACKED_TRI (G is the packed triangle)
+  const rfk::PackDev* pack;   // non-null: K4 writes the G5 packed tiles (send buffer or the owners' staging buffers)
+  int64_t tri_T = 0;          // > 0: RF_OUT_PACKED_TRI (G is the packed triangle)
 };
 
-constexpr int kPackGm = 8;  // raster group of rf_gram_packed's K4 (chunks are runs of groups)
+constexpr int kPackGm = 8;  // row tiles per G5 chunk group (chunks are runs of 8-row-tile groups, rf_tile_map)
 
 // Hybrid K4 (bf16 / tf32 / fp8 SYRK, 256×512 pair tiles): 4-CTA clusters with B multicast on the first super
 // rows and, concurrently on a second stream, pair clusters on the remaining row tiles.  Clusters of 4 must sit in
@@ -439,15 +518,8 @@ static PFN_wait32h wait32_h() {
   });
   return fn;
 }
-static cudaStream_t side_stream() {
-  static std::mutex mu;
-  static cudaStream_t s[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (dev >= 0 && dev < 64 && !s[dev]) cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking);
-  return (dev >= 0 && dev < 64) ? s[dev] : nullptr;
-}
+// The call's context owns the side stream (one per context: separate contexts never couple their streams).
+static cudaStream_t side_stream() { return g_ctx ? g_ctx->side : nullptr; }
 
 // How many 4-CTA clusters of kernel <Cm, Epi> can be co-resident (clusters must sit inside one GPC).
 template <class Cm, class Epi>
@@ -516,7 +588,7 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
                               cudaStream_t st, bool* used) {
   *used = false;
   const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512);
-  if (env_int("RF_K4_HYBRID", 1) == 0 || T < 64 || !wait32_h() || !side_stream()) return RF_OK;
+  if (opt(RF_OPT_K4_HYBRID) == 0 || T < 64 || !wait32_h() || !side_stream()) return RF_OK;
   using Cm = rfk::TcCfg<kFmt, 1, 512, -1, kMcCl>;
   using Cp = rfk::TcCfg<kFmt, 1, 512>;
   int mcl = 0;
@@ -526,9 +598,8 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
   if (mcl <= 0 || left < 2) return RF_OK;
   // work share of the multicast kernel from the per-SM rate ratio r (measured ≈ 1.11: less L2 traffic per flop
   // buys clock under the power cap for bf16 and bandwidth for fp8); env RF_HYB_FPCT overrides
-  const double rate = env_int("RF_HYB_R100", 111) / 100.0;
-  double f = ((double)kMcCl * mcl * rate) / ((double)kMcCl * mcl * rate + (left & ~1));
-  if (env_int("RF_HYB_FPCT", 0) > 0) f = std::min(1.0, env_int("RF_HYB_FPCT", 0) / 100.0);
+  const double rate = opt(RF_OPT_K4_SPLIT_R100) / 100.0;
+  const double f = ((double)kMcCl * mcl * rate) / ((double)kMcCl * mcl * rate + (left & ~1));
   double total = 0;
   for (int I = 0; I < T; ++I) total += T2 - I / 2;
   double acc = 0;
@@ -544,7 +615,7 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
                              : rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
   // tail raster: with 8 pair clusters in flight, groups of 4 row tiles × 2 column tiles re-read the fewest Σᵀ panels
   // (4·32 + 2·64 MB per 8 tiles vs 8·32 + 64 for groups of 8); measured ≈ 0.8 % on the whole K4 (scripts/gpu_tailgm.sh)
-  rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, env_int("RF_TAIL_GM", 4));
+  rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, 4);
   if (lockw > 0) {
     sm.prog = prog;
     sp.prog = prog + 128;
@@ -554,8 +625,8 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
   sm.started = prog + 255;
   // evict_last on the operand loads keeps the Σᵀ panel slices of a wave in L2 a little longer: 196.6 → 195.0 ms
   // over 6 interleaved pairs (5 of 6 faster; scripts/gpu_k4pol2.sh); evict_first on G's stores showed nothing
-  sm.load_pol = sp.load_pol = env_int("RF_K4_LOADPOL", 1);
-  sm.store_pol = sp.store_pol = env_int("RF_K4_STOREPOL", 0);
+  sm.load_pol = sp.load_pol = 1;
+  sm.store_pol = sp.store_pol = 0;
   if ((s = launch_hybrid_pair<Cm, Cp>(name, tS, tS, tS, tS, tO, sm, sp, e, prog + 255, sms, left & ~1, st, &tSh)))
     return s;
   *used = true;
@@ -567,7 +638,7 @@ template <int kFmt, class Epi>
 rf_status launch_k4_hybrid(const char* name, const CUtensorMap& tS, const CUtensorMap& tSh, const CUtensorMap& tO,
                            int64_t n, int kb, const Epi& e, uint32_t* prog, int lockw, int lockks, int sms,
                            cudaStream_t st, bool* used) {
-  if (env_int("RF_K4_CL8", 0))
+  if (opt(RF_OPT_K4_CL8))
     return launch_k4_hybrid_cl<kFmt, 8>(name, tS, tSh, tO, n, kb, e, prog, lockw, lockks, sms, st, used);
   return launch_k4_hybrid_cl<kFmt, 4>(name, tS, tSh, tO, n, kb, e, prog, lockw, lockks, sms, st, used);
 }
@@ -583,13 +654,13 @@ rf_status launch_k3_hybrid(const char* name, const CUtensorMap& tA, const CUtens
                            bool* used) {
   *used = false;
   const int T = (int)((n + 255) / 256), T2 = (int)((n + 511) / 512), tn = (int)((m + 255) / 256);
-  if (env_int("RF_K3_HYBRID", 1) == 0 || T < 32 || !wait32_h() || !side_stream()) return RF_OK;
+  if (opt(RF_OPT_K3_HYBRID) == 0 || T < 32 || !wait32_h() || !side_stream()) return RF_OK;
   int mcl = 0;
   rf_status s;
   if ((s = max_clusters<Cm, Epi>(sms, &mcl))) return s;
   const int left = sms - 4 * mcl;
   if (mcl <= 0 || left < 2) return RF_OK;
-  const double rate = env_int("RF_HYB3_R100", 120) / 100.0;   // per-SM rate, multicast vs pair kernel
+  const double rate = opt(RF_OPT_K3_SPLIT_R100) / 100.0;   // per-SM rate, multicast vs pair kernel
   const double f = (4.0 * mcl * rate) / (4.0 * mcl * rate + (left & ~1));
   const int S1 = std::min(T2, (int)std::lround(f * T / 2.0));   // rows are uniform: split by row count
   if (S1 <= 0 || 2 * S1 >= T) return RF_OK;
@@ -598,7 +669,7 @@ rf_status launch_k3_hybrid(const char* name, const CUtensorMap& tA, const CUtens
   rfk::Sched sp = rfk::Sched::make(0, 256, 2 * S1, T, tn, kb, 0, raster_gm(8, 3));
   // evict_last on the operand loads (X and W are re-read by every tile of a row / column): 8.04 → 6.94 ms
   // (5 interleaved pairs, scripts/gpu_k3pol.sh)
-  sm.load_pol = sp.load_pol = env_int("RF_K3_LOADPOL", 1);
+  sm.load_pol = sp.load_pol = 1;
   sm.started = prog + 255;
   if ((s = launch_hybrid_pair<Cm, Cp>(name, tA, tB, tBh, tA, tA, sm, sp, e, prog + 255, sms, left & ~1, st)))
     return s;
@@ -638,12 +709,12 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   const int kb3 = (int)((g.p + C3::BK - 1) / C3::BK);
   rfk::Sched s3 = rfk::Sched::make(0, 256, 0, (int)((g.n + 255) / 256), (int)((g.m_local + 255) / 256), kb3, 0,
                                    raster_gm(8, 3));
-  s3.load_pol = env_int("RF_K3_LOADPOL", 1);
+  s3.load_pol = 1;
   // K3 = the pair kernel, or (bf16 / tf32, large n) the multicast + pair hybrid (launch_k3_hybrid)
   auto run_k3 = [&](const auto& e3) -> rf_status {
     using E3 = std::decay_t<decltype(e3)>;
     if constexpr (kSplit == 1) {
-      if (env_int("RF_K3_MC", 1)) {
+      if (opt(RF_OPT_K3_HYBRID)) {
         using C3m = rfk::TcCfg<kFmt, kSplit, 256, 0, 4>;
         CUtensorMap tBh;   // W with a 64-row box: the multicast kernel's half B tiles
         rf_status r;
@@ -684,54 +755,59 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
       rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4, kchunk4,
                        raster_gm(8, 4));
   rfk::Sched s4l = s4;
-  s4l.load_pol = env_int("RF_K4_LOADPOL", 1);   // as the hybrid (evict_last operands)
-  const int lockw = env_int("RF_LOCKW", 24);
+  s4l.load_pol = 1;   // as the hybrid (evict_last operands)
+  const int lockw = (int)opt(RF_OPT_LOCK_W);
   if (lockw > 0) {
     s4l.prog = (uint32_t*)(g.w + g.pl.off_prog);
     s4l.lock_w = lockw;
-    s4l.lock_ks = std::max(1, env_int("RF_LOCKKS", 8));
+    s4l.lock_ks = std::max(1, (int)opt(RF_OPT_LOCK_KS));
     RF_CUDA_CHECK(cudaMemsetAsync(s4l.prog, 0, 1024, g.st));
   }
+  if (g.pack) {   // G5: every upper 256-tile of the partial into its exchange slot (canonical ownership, no schedule index)
+    rfk::EpiSyrkPacked e4{(float)(1.0 / (double)g.m_total), *g.pack};
+    if constexpr (kBN4 == 512 && kSplit == 1) {
+      if (lockw > 0) {
+        bool used = false;
+        CUtensorMap tSh;
+        if ((s = make_tmap(&tSh, S0, bf, g.n, g.m_local, g.pl.ldS, 64))) return s;
+        if ((s = launch_k4_hybrid<kFmt>("K4_syrk_packed", tA, tSh, tA, g.n, kb4, e4, s4l.prog, lockw, s4l.lock_ks,
+                                         g.sms, g.st, &used)))
+          return s;
+        if (used) return ok();
+      }
+    }
+    if ((s = launch_tc<C4>("K4_syrk_packed", tA, tB, tAl, tBl, tA, s4l, e4, g.sms, g.st))) return s;
+    return ok();
+  }
   if constexpr (kBN4 == 512 && kSplit == 1) {
-  if (!g.pack && lockw > 0 && env_int("RF_K4_MC", 0) == 0) {
-    rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
-    bool used = false;
-    CUtensorMap tSh;   // Σᵀ with a 64-row box (the 8-CTA multicast kernel's A halves)
-    if ((s = make_tmap(&tSh, S0, bf, g.n, g.m_local, g.pl.ldS, 64))) return s;
-    if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tSh, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
-                                     &used)))
-      return s;
-    if (used) return ok();
-  }
-  if (!g.pack && env_int("RF_K4_MC", 0)) {
-    // 4-CTA clusters with B multicast: the scheduler walks 512-row super tiles (super-row I2 covers row tiles
-    // 2·I2 and 2·I2 + 1; both need column tiles J ≥ I2 of width 512).
-    using C4m = rfk::TcCfg<kFmt, kSplit, 512, -1, 4>;
-    rfk::Sched sm = rfk::Sched::make(1, 256, 0, (int)((g.n + 511) / 512), (int)((g.n + 511) / 512), kb4, kchunk4,
-                                     raster_gm(4, 4));
-    sm.prog = s4l.prog;
-    sm.lock_w = s4l.lock_w;
-    sm.lock_ks = s4l.lock_ks;
-    rfk::EpiSyrk em{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
-    if ((s = launch_tc<C4m>("K4_syrk", tA, tB, tAl, tBl, tO, sm, em, g.sms, g.st))) return s;
-    return ok();
-  }
-  }
-  if (g.pack) {
-    rfk::Sched sp = rfk::Sched::make(1, kBN4, 0, (int)((g.n + 255) / 256), (int)((g.n + kBN4 - 1) / kBN4), kb4,
-                                     kchunk4, kPackGm);
-    sp.prog = s4l.prog;
-    sp.lock_w = s4l.lock_w;
-    sp.lock_ks = s4l.lock_ks;
-    sp.load_pol = s4l.load_pol;
-    rfk::EpiSyrkPacked e4{g.pack->send, g.pack->sync, (float)(1.0 / (double)g.m_total), g.pack->world,
-                          g.pack->nchunks, kBN4, *g.pack->dev};
-    if ((s = launch_tc<C4>("K4_syrk_packed", tA, tB, tAl, tBl, tA, sp, e4, g.sms, g.st))) return s;
-    return ok();
+    if (lockw > 0) {
+      rfk::EpiSyrk eh{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
+      bool used = false;
+      CUtensorMap tSh;   // Σᵀ with a 64-row box (the 8-CTA multicast kernel's A halves)
+      if ((s = make_tmap(&tSh, S0, bf, g.n, g.m_local, g.pl.ldS, 64))) return s;
+      if ((s = launch_k4_hybrid<kFmt>("K4_syrk", tA, tSh, tO, g.n, kb4, eh, s4l.prog, lockw, s4l.lock_ks, g.sms, g.st,
+                                       &used)))
+        return s;
+      if (used) return ok();
+    }
   }
   rfk::EpiSyrk e4{g.G, g.ldg, g.n, (float)(1.0 / (double)g.m_total), g.full, tma_out ? 1 : 0, g.tri_T};
   if ((s = launch_tc<C4>("K4_syrk", tA, tB, tAl, tBl, tO, s4l, e4, g.sms, g.st))) return s;
   return ok();
+}
+
+rf_status gram_tc_dispatch(const GramTcArgs& ga, rf_prec prec) {
+  if (prec == RF_PREC_BF16) return gram_tc<1, 1, 512, 0>(ga, 0);
+  if (prec == RF_PREC_TF32) return gram_tc<2, 1, 512, 1>(ga, 0);
+  // 3×TF32: chunks of RF_OPT_KCHUNK K-blocks (default 4 = 128 features) bound the truncating tensor-pipe
+  // accumulation to ≈ 2.6e-6 relative (DESIGN.md §6 finding 4)
+  return gram_tc<2, 3, 256, 2>(ga, (int)opt(RF_OPT_KCHUNK));
+}
+
+// SMs the tensor-core kernels may use (RF_OPT_MAX_SMS; CTA pairs need an even count)
+int usable_sms(int sms) {
+  const int64_t m = opt(RF_OPT_MAX_SMS);
+  return m > 0 ? std::max(2, std::min(sms, (int)m) & ~1) : sms;
 }
 
 struct K5Args {
@@ -752,8 +828,8 @@ template <class C, class E>
 rf_status k5_go(const CUtensorMap& tA, const CUtensorMap& tAl, const CUtensorMap& tO, const E& e, int64_t p, int rt0,
                 int rt1, int tn, int sms, cudaStream_t st) {
   rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, raster_gm(16, 5));
-  sc.load_pol = env_int("RF_K5_LOADPOL", 1);
-  sc.store_pol = env_int("RF_K5_STOREPOL", 1);
+  sc.load_pol = 1;    // evict_last operands (X is re-read by every tile of a row / column)
+  sc.store_pol = 1;   // evict_first on the streamed Φ stores
   return launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, sms, st);
 }
 
@@ -774,8 +850,7 @@ rf_status launch_k5(const K5Args& a) {
   struct { int sms; } dev{a.sms};
   rf_status s;
   CUtensorMap tA, tAl, tO;
-  const bool tma_out = env_int("RF_K5_TMA", 1) != 0 &&
-                       (a.tri_T > 0 ? make_tmap_out(&tO, Phi, tri_tiles(n) * 256, 256, 256)
+  const bool tma_out = (a.tri_T > 0 ? make_tmap_out(&tO, Phi, tri_tiles(n) * 256, 256, 256)
                                     : make_tmap_out(&tO, Phi, n, n, ldphi));
   rfk::EpiEq1<kOdd> e{Phi, ldphi, n, rc, nj, e0, e1, e2, f0, f1, full, tma_out ? 1 : 0, a.tri_T};
   const int rt0 = (int)(row_begin / 256), rt1 = (int)((row_end + 255) / 256), tn = (int)((n + 255) / 256);
@@ -787,7 +862,7 @@ rf_status launch_k5(const K5Args& a) {
     // epilogue warps (four per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages;
     // 96 registers) help: configs[4] 11.3 → 9.54 ms (12 warps: 9.94).  Long K: the MMA sets it and the 8-warp
     // kernel stays ahead (configs[3] shape, p = 1024: 3.63 vs 3.78 ms).  DESIGN.md §7.
-    const bool wide = env_int("RF_K5_WIDE", p <= 512 ? 1 : 0) != 0;
+    const bool wide = opt(RF_OPT_K5_WIDE) < 0 ? p <= 512 : opt(RF_OPT_K5_WIDE) != 0;
     if (bf && wide) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (bf) {

@@ -166,18 +166,4 @@ __global__ void __launch_bounds__(256) k_center_fold(const double* __restrict__ 
   if (i < n) rf[i] = (float)(r[i] - 0.5 * s_ptr[0]);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Fused G5, owner side: recv[e] = Σ_{r < world} staging[r·recv_elems + e] in rank order (deterministic).
-__global__ void __launch_bounds__(256) k_pack_reduce(const float4* __restrict__ staging, int64_t recv4, int world,
-                                                     float4* __restrict__ recv) {
-  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < recv4; e += (int64_t)gridDim.x * 256) {
-    float4 s = staging[e];
-    for (int r = 1; r < world; ++r) {
-      const float4 v = staging[(int64_t)r * recv4 + e];
-      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-    }
-    recv[e] = s;
-  }
-}
-
 }  // namespace rfk

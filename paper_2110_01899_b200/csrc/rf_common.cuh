@@ -9,8 +9,6 @@
 
 namespace rfk {
 
-constexpr int kNumSMs = 148;
-
 // ------------------------------------------------------------------------------------------
 // σ.  sigmoid(x) − 1/2 is evaluated as ½·tanh(x/2) (identical function, no cancellation).
 // ------------------------------------------------------------------------------------------

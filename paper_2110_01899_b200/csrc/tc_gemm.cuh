@@ -336,7 +336,7 @@ struct EpiSigma {
   int64_t M, N;     // n rows (samples), m_local columns (features)
   int act;          // used when kAct < 0
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {};
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
@@ -411,7 +411,7 @@ struct EpiSigmaTer {
   int64_t M, N;     // n rows (samples), m_local columns (features)
   float t_minus, t_plus;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {};
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
@@ -453,7 +453,7 @@ struct EpiSyrk {
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {};
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
@@ -477,51 +477,51 @@ struct EpiSyrk {
   }
 };
 
-// K4 with PACKED output for the multi-GPU reduce-scatter (include/rf.h, G5).  The pair tile t (schedule
-// index; row tile ti) belongs to the chunk whose row-tile range holds ti; its 256×256 sub-tile sub goes to
-// position u = tiles_per_pair·(t − tile0[c]) + sub of the chunk: owner u mod R, slot u div R.  Whole tiles are
-// stored (no triangle mask).
-constexpr int kMaxP2P = 16;                  // ranks reachable by the fused (peer-memory) epilogue
+// K4 with PACKED output: the multi-GPU G5 (include/rf.h).  Tile ownership is canonical (rf_tile_map): the row tiles
+// are cut into chunks (crow[c] .. crow[c+1]); inside chunk c the upper 256-tiles (I, J ≥ I) are numbered row-major
+// from u = 0, and tile u goes to owner u mod world, slot u div world.  Every 256×256 tile of the upper triangle is
+// stored whole; 256-tiles a pair tile covers below the diagonal (J < I) or past the matrix (J ≥ T) are skipped.
+//   NCCL:  send + soff[c] + (owner·slots[c] + slot)·65536         (chunk-major, owner-major: one ReduceScatter per chunk)
+//   PEERS: peer[owner] + self·recv_elems + roff[c] + slot·65536   (the owner's staging buffer, over NVLink)
+constexpr int kMaxP2P = RF_MAX_PEERS;
+constexpr int kMaxChunks = 16;
 struct PackDev {
-  int64_t tile0[RF_PACK_MAX_CHUNKS + 1];
-  int64_t slots[RF_PACK_MAX_CHUNKS];
-  int64_t soff[RF_PACK_MAX_CHUNKS + 1];
-  int64_t roff[RF_PACK_MAX_CHUNKS + 1];     // element offset of chunk c in a receive buffer
-  int32_t rt0[RF_PACK_MAX_CHUNKS + 1];      // first 256-row tile of chunk c
-  // Fused G5 (rf_gram_packed_p2p): when p2p, the tile of owner o goes to peer[o] (o's staging buffer, mapped
-  // into this process; NVLink stores) at [self][recv slot] instead of the local send buffer.
-  int p2p, self;
+  int32_t T;                                 // 256-tiles per side
+  int32_t nchunks, world, self, p2p;
+  int32_t crow[kMaxChunks + 1];              // first row tile of chunk c
+  int64_t slots[kMaxChunks];
+  int64_t soff[kMaxChunks + 1];
+  int64_t roff[kMaxChunks + 1];
   int64_t recv_elems;
+  float* send;                               // NCCL send buffer (workspace)
+  uint32_t* sync;                            // NCCL: per-chunk count of finished (pair tile, epilogue warp)s; else null
   float* peer[kMaxP2P];
 };
 struct EpiSyrkPacked {
-  float* send;
-  uint32_t* sync;
   float scale;
-  int world, nchunks, bn;
   PackDev pk;
-  __device__ __forceinline__ bool chunk_needed(int64_t, int64_t) const { return true; }
+  __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
+    return (col0 >> 8) >= (row_lo >> 8) && (col0 >> 8) < pk.T;
+  }
   struct Pre {};
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   __device__ __forceinline__ int chunk_of(int ti) const {
     int c = 0;
-    while (c + 1 < nchunks && ti >= pk.rt0[c + 1]) ++c;
+    while (c + 1 < pk.nchunks && ti >= pk.crow[c + 1]) ++c;
     return c;
   }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32],
-                                             int, int, long long t, const Pre&) const {
-    const int ti = (int)(row_lo >> 8);
-    const int c = chunk_of(ti);
-    const int64_t tj0 = (col0 / bn) * bn;                          // first column of the pair tile
-    const int sub = (int)((col0 - tj0) >> 8);
-    const int64_t u = (int64_t)(bn >> 8) * (t - pk.tile0[c]) + sub;
-    const int64_t owner = u % world, slot = u / world;
+                                             int, int, long long, const Pre&) const {
+    const int64_t I = row_lo >> 8, J = col0 >> 8;
+    const int c = chunk_of((int)I);
+    const int64_t r0 = pk.crow[c];
+    const int64_t u = (I - r0) * pk.T - (I * (I - 1) - r0 * (r0 - 1)) / 2 + (J - I);   // row-major in the chunk
+    const int64_t owner = u % pk.world, slot = u / pk.world;
     float* tile = pk.p2p ? pk.peer[owner] + (int64_t)pk.self * pk.recv_elems + pk.roff[c] +
                                slot * (int64_t)(RF_PACK_TILE * RF_PACK_TILE)
-                         : send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
-    const int64_t lrow = (row_lo & 255) + cx.lane;
-    float* dst = tile + lrow * RF_PACK_TILE + ((col0 - tj0) & 255);
+                         : pk.send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
+    float* dst = tile + ((row_lo & 255) + cx.lane) * RF_PACK_TILE + (col0 & 255);
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
@@ -529,14 +529,14 @@ struct EpiSyrkPacked {
     for (int q = 0; q < 8; ++q)
       reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
-  // After the warp's last store of pair tile t: publish it (system-scope release) to the chunk counter.
-  __device__ __forceinline__ void tile_done(long long t, uint32_t lane) const {
+  // NCCL: after the warp's last store of a pair tile in row tile ti, publish it to the chunk counter (system-scope
+  // fence, one atomic per epilogue warp: the library waits for 2 · EPI_WARPS · (pair tiles of the chunk)).
+  __device__ __forceinline__ void tile_done(int ti, uint32_t lane) const {
+    if (!pk.sync) return;
     __syncwarp();
-    if (lane == 0 && sync) {
-      int c = 0;
-      while (c + 1 < nchunks && t >= pk.tile0[c + 1]) ++c;
+    if (lane == 0) {
       __threadfence_system();
-      atomicAdd(sync + c, 1u);
+      atomicAdd(pk.sync + chunk_of(ti), 1u);
     }
   }
 };
@@ -556,7 +556,7 @@ struct EpiEq1 {
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   // The row's coefficient record does not depend on the accumulator: loaded before the TMEM wait.
   struct Pre {
     RowCoef c;
@@ -634,7 +634,7 @@ struct EpiKtilde {
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const {
     return col0 < n && row_lo < n && col0 + 31 >= row_lo;
   }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {
     float u[8];
     float r;
@@ -709,7 +709,7 @@ struct EpiRaw {
   float* C;
   int64_t ld, M, N;
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
-  __device__ __forceinline__ void tile_done(long long, uint32_t) const {}
+  __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {};
   __device__ __forceinline__ Pre prefetch(int64_t, int64_t, uint32_t) const { return Pre{}; }
   template <class Ctx>
@@ -1003,7 +1003,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, a, 0, 1, (long long)t, pf);
         }
         cx.flush();
-        epi.tile_done((long long)t, lane);
+        epi.tile_done(ti, lane);
         continue;
       }
       for (int c = 0; c < nchunks; ++c, ++it) {
@@ -1056,7 +1056,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
       }
       cx.flush();
-      epi.tile_done((long long)t, lane);
+      epi.tile_done(ti, lane);
     }
     if (lane == 0) ptx::bulk_wait_all();
   }

@@ -94,28 +94,28 @@ def test_workspace_sizes():
 
 def test_validation_rejects_before_any_launch():
     lib = rf.load()
-    g = lib.rf_gram(None, 64, None, 64, 64, 256, 512, 512, 0, 4, 0, None, 256, None, 0, None)
+    g = lib.rf_gram(None, None, 64, None, 64, 64, 256, 512, 512, 0, 4, 0, None, 256, None, 0, None)
     assert g == _lib.RF_E_INVALID
     assert b"NULL" in lib.rf_last_error()
     buf = (ctypes.c_char * 4096)()
     addr = ctypes.addressof(buf)
     addr16 = (addr + 15) // 16 * 16
     # p = 100 bf16 with ldx = 100 → 200 B rows, not a multiple of 16 B (TMA stride rule)
-    s = lib.rf_gram(ctypes.c_void_p(addr16), 100, ctypes.c_void_p(addr16), 104, 100, 8, 8, 8, 0, 4, 0,
+    s = lib.rf_gram(None, ctypes.c_void_p(addr16), 100, ctypes.c_void_p(addr16), 104, 100, 8, 8, 8, 0, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"16 B" in lib.rf_last_error()
-    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 4, 0, 4, 0,
+    s = lib.rf_gram(None, ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 4, 0, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"m_total" in lib.rf_last_error()
-    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 42, 4, 0,
+    s = lib.rf_gram(None, ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 42, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"activation" in lib.rf_last_error()
     # workspace too small
-    s = lib.rf_gram(ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 0, 4, 0,
+    s = lib.rf_gram(None, ctypes.c_void_p(addr16), 64, ctypes.c_void_p(addr16), 64, 64, 8, 8, 8, 0, 4, 0,
                     ctypes.c_void_p(addr16), 8, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_WORKSPACE
     # Φ row range must start on a 256-row boundary
-    s = lib.rf_phi_closed_form(ctypes.c_void_p(addr16), 64, 64, 512, 0, 1.0, None, 4, 0, 128, 512,
+    s = lib.rf_phi_closed_form(None, ctypes.c_void_p(addr16), 64, 64, 512, 0, 1.0, None, 4, 0, 128, 512,
                                ctypes.c_void_p(addr16), 256, ctypes.c_void_p(addr16), 16, None)
     assert s == _lib.RF_E_INVALID and b"row range" in lib.rf_last_error()
 
@@ -149,15 +149,15 @@ def test_packed_tri_validation():
     buf = (ctypes.c_char * 4096)()
     a16 = (ctypes.addressof(buf) + 15) // 16 * 16
     # fp32 (SIMT) precision cannot write the packed layout
-    s = lib.rf_gram(ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 1, 4,
+    s = lib.rf_gram(None, ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 1, 4,
                     ctypes.c_void_p(a16), 0, ctypes.c_void_p(a16), 16, None)
     assert s == _lib.RF_E_INVALID and b"PACKED_TRI" in lib.rf_last_error()
     # misaligned packed buffer
-    s = lib.rf_phi_closed_form(ctypes.c_void_p(a16), 64, 64, 512, 0, 1.0, None, 4, 4, 0, 512,
+    s = lib.rf_phi_closed_form(None, ctypes.c_void_p(a16), 64, 64, 512, 0, 1.0, None, 4, 4, 0, 512,
                                ctypes.c_void_p(a16 + 4), 0, ctypes.c_void_p(a16), 16, None)
     assert s == _lib.RF_E_INVALID and b"16-byte" in lib.rf_last_error()
     # centering is not defined for the packed layout: 4 | CENTER is not a valid mode
-    s = lib.rf_gram(ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 4, 6,
+    s = lib.rf_gram(None, ctypes.c_void_p(a16), 64, ctypes.c_void_p(a16), 64, 64, 8, 8, 8, 0, 4, 6,
                     ctypes.c_void_p(a16), 8, ctypes.c_void_p(a16), 16, None)
     assert s == _lib.RF_E_INVALID and b"output mode" in lib.rf_last_error()
 
@@ -176,58 +176,41 @@ def test_no_cpu_fallback_without_gpu():
     xa = (ctypes.addressof(x) + 15) // 16 * 16
     out = (ctypes.c_char * (256 * 256 * 4 + 64))()
     oa = (ctypes.addressof(out) + 15) // 16 * 16
-    s = lib.rf_phi_closed_form(ctypes.c_void_p(xa), 64, 64, 256, 0, 1.0, None, 4, 0, 0, 256,
+    s = lib.rf_phi_closed_form(None, ctypes.c_void_p(xa), 64, 64, 256, 0, 1.0, None, 4, 0, 0, 256,
                                ctypes.c_void_p(oa), 256, ctypes.c_void_p(wsa), size, None)
     assert s in (_lib.RF_E_CUDA, _lib.RF_E_UNSUPPORTED)
 
 
-# ------------------------------------------------------------------------------------------ G5 plan (host)
-@pytest.mark.parametrize("n", [1, 255, 256, 600, 4096, 65536])
-@pytest.mark.parametrize("world", [1, 2, 3, 8])
-@pytest.mark.parametrize("prec", ["bf16", "3xtf32"])
-def test_pack_plan_layout_and_coverage(n, world, prec):
-    """Chunk offsets are consistent, every pair tile of K4's triangle schedule is owned by exactly one slot
-    of exactly one rank, and the owned tiles cover the upper triangle (256-tile granularity)."""
-    plan = rf.rf_pack_plan(n, world, 16, prec)
-    T2 = 256 * 256
-    assert 1 <= plan.nchunks <= 16
-    assert plan.chunk_tile0[0] == 0 and plan.chunk_tile0[plan.nchunks] == plan.pair_tiles
-    for c in range(plan.nchunks):
-        tiles = (plan.chunk_tile0[c + 1] - plan.chunk_tile0[c]) * plan.tiles_per_pair
-        assert tiles > 0
-        assert plan.chunk_slots[c] == -(-tiles // world)
-        assert plan.chunk_send_off[c + 1] - plan.chunk_send_off[c] == world * plan.chunk_slots[c] * T2
-        assert plan.chunk_recv_off[c + 1] - plan.chunk_recv_off[c] == plan.chunk_slots[c] * T2
-    assert plan.send_elems == plan.chunk_send_off[plan.nchunks] == world * plan.recv_elems
-    nt = -(-n // 256)
-    seen = {}
-    for r in range(world):
-        for I, J in rf.rf_pack_tile_map(plan, r):
-            if I < 0:
-                continue
-            assert (I, J) not in seen
-            seen[(I, J)] = r
-    assert len(seen) == plan.pair_tiles * plan.tiles_per_pair
-    for I in range(nt):
-        for J in range(I, nt):
-            assert (I, J) in seen, (I, J)
-    counts = np.bincount(np.array(list(seen.values())), minlength=world)
-    assert counts.max() - counts.min() <= plan.nchunks
+# ------------------------------------------------------------------------------------------ context (host side)
+def test_context_api_validation_without_gpu():
+    """The §8(b) context calls validate on the host: options need a context, value ranges are checked, a context on a
+    device that is not an sm_100 part is refused, and rf_workspace_size adds the NCCL send buffer only for a
+    context with NCCL attached (NULL context: none)."""
+    import torch
+    lib = rf.load()
+    v = ctypes.c_int64()
+    assert lib.rf_ctx_set_option(None, 0, 1) == _lib.RF_E_INVALID
+    assert lib.rf_ctx_get_option(None, 0, ctypes.byref(v)) == _lib.RF_E_INVALID
+    lib.rf_ctx_destroy(None)                                # no-op
+    if not torch.cuda.is_available():
+        p = ctypes.c_void_p()
+        assert lib.rf_ctx_create(0, ctypes.byref(p)) == _lib.RF_E_UNSUPPORTED and not p.value
+    assert lib.rf_ctx_attach_peers(None, 0, 2, 1000) == _lib.RF_E_INVALID
+    assert lib.rf_ctx_init_nccl(None, b"\0" * 128, 0, 1) == _lib.RF_E_INVALID
+    a = rf.rf_workspace_size("gram", 64, 1000, 512, "bf16", "packed_tiles")
+    assert a == rf.rf_gram_workspace_size(64, 1000, 512, "bf16")
+    assert rf.rf_workspace_size("phi", 64, 1000, 0, "bf16") == rf.rf_phi_workspace_size(64, 1000, "bf16")
+    with pytest.raises(rf.RFError):
+        rf.rf_workspace_size("gram", 64, 1000, 0, "bf16")
 
 
-def test_pack_plan_rejects_bad_arguments():
-    with pytest.raises(rf.RFError):
-        rf.rf_pack_plan(0, 2, 4, "bf16")
-    with pytest.raises(rf.RFError):
-        rf.rf_pack_plan(1024, 0, 4, "bf16")
-    with pytest.raises(rf.RFError):
-        rf.rf_pack_plan(1024, 2, 4, "fp32")      # SIMT modes have no packed output
-    plan = rf.rf_pack_plan(1024, 2, 4, "bf16")
-    with pytest.raises(rf.RFError):
-        rf.rf_pack_tile_map(plan, 2)
-    plan.chunk_slots[0] += 1                     # a plan not made by rf_pack_plan is refused
-    with pytest.raises(rf.RFError):
-        rf.rf_pack_tile_map(plan, 0)
+def test_tile_map_small_case_by_hand():
+    """n = 600 → T = 3 row tiles, one chunk; the upper tiles row-major are (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) and
+    tile u goes to rank u mod 2 at slot u div 2."""
+    assert rf.rf_tile_map(600, 1, 0).tolist() == [[0, 0], [0, 1], [0, 2], [1, 1], [1, 2], [2, 2]]
+    assert rf.rf_tile_map(600, 2, 0).tolist() == [[0, 0], [0, 2], [1, 2]]
+    assert rf.rf_tile_map(600, 2, 1).tolist() == [[0, 1], [1, 1], [2, 2]]
+    assert rf.rf_tile_map(600, 4, 3).tolist() == [[1, 1], [-1, -1]]
 
 
 # ------------------------------------------------------------------------------------------ TRF thresholds (host)
@@ -276,16 +259,16 @@ def test_ridge_validation():
     g_bad = (ctypes.c_double * 2)(0.5, 0.0)
     vp = ctypes.c_void_p
     # γ must be > 0
-    s = lib.rf_ridge(vp(a), 16, 8, 8, g_bad, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    s = lib.rf_ridge(None, vp(a), 16, 8, 8, g_bad, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
     assert s == _lib.RF_E_INVALID and b"gamma" in lib.rf_last_error()
     # ldg must cover the stacked samples
-    s = lib.rf_ridge(vp(a), 15, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    s = lib.rf_ridge(None, vp(a), 15, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
     assert s == _lib.RF_E_INVALID and b"ldg" in lib.rf_last_error()
     # test predictions need Yhat
-    s = lib.rf_ridge(vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), None, vp(a), 16, None)
+    s = lib.rf_ridge(None, vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), None, vp(a), 16, None)
     assert s == _lib.RF_E_INVALID and b"Yhat" in lib.rf_last_error()
     # workspace too small
-    s = lib.rf_ridge(vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
+    s = lib.rf_ridge(None, vp(a), 16, 8, 8, g_ok, 2, vp(a), 1, 1, vp(a), vp(a), vp(a), 16, None)
     assert s == _lib.RF_E_WORKSPACE
 
 
@@ -295,11 +278,11 @@ def test_round_bf16_validation():
     buf = (ctypes.c_char * 4096)()
     a = (ctypes.addressof(buf) + 255) // 256 * 256
     vp = ctypes.c_void_p
-    assert lib.rf_round_bf16(vp(a), 8, 0, 8, vp(a), 8, None) == 0
-    assert lib.rf_round_bf16(vp(a), 8, 8, 0, vp(a), 8, None) == 0
-    assert lib.rf_round_bf16(vp(a), 8, -1, 8, vp(a), 8, None) == _lib.RF_E_INVALID
-    assert lib.rf_round_bf16(None, 8, 2, 8, vp(a), 8, None) == _lib.RF_E_INVALID
-    s = lib.rf_round_bf16(vp(a), 7, 2, 8, vp(a), 8, None)
+    assert lib.rf_round_bf16(None, vp(a), 8, 0, 8, vp(a), 8, None) == 0
+    assert lib.rf_round_bf16(None, vp(a), 8, 8, 0, vp(a), 8, None) == 0
+    assert lib.rf_round_bf16(None, vp(a), 8, -1, 8, vp(a), 8, None) == _lib.RF_E_INVALID
+    assert lib.rf_round_bf16(None, None, 8, 2, 8, vp(a), 8, None) == _lib.RF_E_INVALID
+    s = lib.rf_round_bf16(None, vp(a), 7, 2, 8, vp(a), 8, None)
     assert s == _lib.RF_E_INVALID and b"leading" in lib.rf_last_error()
-    s = lib.rf_round_bf16(vp(a + 2), 8, 2, 8, vp(a), 8, None)
+    s = lib.rf_round_bf16(None, vp(a + 2), 8, 2, 8, vp(a), 8, None)
     assert s == _lib.RF_E_INVALID and b"aligned" in lib.rf_last_error()

@@ -1,14 +1,18 @@
-"""GPU tests of G5 (include/rf.h): K4 writing packed triangle tiles for the multi-GPU reduce-scatter.
+"""GPU tests of the multi-GPU G (include/rf.h "G5"): the collective rf_gram(ctx, …, RF_OUT_PACKED_TILES).
 
-* Emulated ranks on ONE GPU: rank r's rf_gram_packed runs on its W shard into its own send buffer (no kernel
-  waits on another); the reduce-scatter's sum is taken with torch; each owner's slots are decoded with
-  rf_pack_tile_map and compared with the fp64 oracle G of the full W (north-star tolerances).
-* The real path at world size 1: GramReduceScatter over an NCCL process group of one rank (the collective
-  is a copy), whose result must equal the dense rf_gram bit for bit, and the chunk counters K4 publishes.
+* Emulated ranks on ONE GPU: R contexts in this process, each attached as rank r of R with its own staging buffer,
+  connected by raw device pointers (rf_ctx_connect_peers).  The exchange is the real one: K4's epilogue stores every
+  tile into its owner's staging buffer, one-thread kernels write the device epoch flags with system-scope release,
+  stream-memory waits order the owner-side sums and the next call's stores.  On one GPU in one process the ranks'
+  streams may share a hardware queue, so a wait could head a queue its producer sits behind: the emulation enqueues
+  each call in its two halves (RF_OPT_G5_PHASES test hook: phase 1 of every rank, then phase 2 of every rank) on one
+  stream, where every wait's producer is already ahead of it.  No kernel ever waits on another.  Three calls in a row
+  (epochs 1..3) are bit-identical, and the summed owned tiles match the fp64 oracle G of the full W.
+* world 1, peers and NCCL (the library's own communicator from rf_nccl_get_unique_id): the packed tiles equal the
+  dense K4 bit for bit, in BF16, TF32 and (NCCL) 3×TF32, and the NCCL chunk counters K4 publishes reach their
+  per-epoch targets.
 """
 import math
-import os
-import socket
 
 import numpy as np
 import pytest
@@ -18,6 +22,7 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 import paper_2110_01899_b200 as rf  # noqa: E402
 from paper_2110_01899_b200 import collective  # noqa: E402
+from entry_bounds import check, gram_bound  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -33,84 +38,125 @@ def _gpu():
     yield
 
 
-@pytest.mark.parametrize("n,p,m,world,prec,nchunks", [
-    (600, 64, 384, 2, "bf16", 4),        # ragged n (not a multiple of 256 / 512)
-    (1024, 96, 512, 3, "bf16", 16),      # tile multiple, world not a power of two
-    (777, 784, 1000, 4, "3xtf32", 3),    # fp32-accurate mode (256-wide K4 tiles, K-chunked accumulation)
-    (1300, 128, 640, 2, "tf32", 64),     # more chunks requested than raster groups
+def _emulated(n, p, m, world, prec, act, calls=3, seed=0):
+    rng = np.random.default_rng(seed + n + world)
+    Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(DT[prec])
+    Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(DT[prec])
+    ctxs = [rf.Context(0) for _ in range(world)]
+    for r, c in enumerate(ctxs):
+        c.attach_peers(r, world, n)
+    bases = [c.peer_base() for c in ctxs]
+    for c in ctxs:
+        c.connect_peers(bases)
+    shards = [Wd[slice(*collective.feature_shard(m, world, r))].contiguous() for r in range(world)]
+    recvs = [torch.full((len(rf.rf_tile_map(n, world, r)) * collective.TILE_ELEMS,), float("nan"), device="cuda")
+             for r in range(world)]
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(calls):
+        for phase in (1, 2):         # no host synchronization between the halves or between calls
+            for r in range(world):
+                ctxs[r].set_option("g5_phases", phase)
+                rf.rf_gram(Xd, shards[r], act=act, prec=prec, out="packed_tiles", m_total=m, G=recvs[r], ctx=ctxs[r])
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy().copy() for x in recvs])
+    for c in ctxs:
+        c.destroy()
+    return Xd, Wd, outs
+
+
+@pytest.mark.parametrize("n,p,m,world,prec,act", [
+    (600, 64, 384, 2, "bf16", "tanh"),         # ragged n (not a multiple of 256 / 512)
+    (1024, 96, 512, 3, "bf16", "erf"),         # tile multiple, world not a power of two
+    (2100, 128, 640, 4, "tf32", "sigmoid_half"),
+    (17000, 64, 256, 2, "bf16", "sigmoid_half"),   # ≥ 64 row tiles: K4's multicast + pair hybrid with packed tiles
 ])
-def test_packed_emulated_ranks_match_oracle(n, p, m, world, prec, nchunks):
-    rng = np.random.default_rng(n + world)
-    X = rng.standard_normal((n, p)) / math.sqrt(p)
-    W = rng.standard_normal((m, p))
-    Xd = torch.tensor(X, device="cuda").to(DT[prec])
-    Wd = torch.tensor(W, device="cuda").to(DT[prec])
-    plan = rf.rf_pack_plan(n, world, nchunks, prec)
-    total = torch.zeros(plan.send_elems, dtype=torch.float32, device="cuda")
+def test_peer_exchange_emulated_ranks(n, p, m, world, prec, act):
+    Xd, Wd, outs = _emulated(n, p, m, world, prec, act)
+    for k in range(1, len(outs)):
+        for r in range(world):
+            assert np.array_equal(outs[k][r], outs[0][r]), f"call {k + 1} differs from call 1 on rank {r}"
+    Xo, Wo = Xd.double().cpu().numpy(), Wd.double().cpu().numpy()
+    S = np.arange(n) if n <= 2100 else collective_sample(n)
+    ref = oracle.gram(Xo[S], Wo, act)
+    pos = -np.ones(n, dtype=np.int64)
+    pos[S] = np.arange(len(S))
+    got = np.full((len(S), len(S)), np.nan)
+    cover = np.zeros((len(S), len(S)), dtype=int)
+    T = collective.RF_PACK_TILE
     for r in range(world):
-        m0, m1 = collective.feature_shard(m, world, r)
-        send = torch.full((plan.send_elems,), float("nan"), dtype=torch.float32, device="cuda")
-        sync = torch.zeros(plan.nchunks, dtype=torch.int32, device="cuda")
-        rf.rf_gram_packed(Xd, Wd[m0:m1].contiguous(), plan, send, sync, 1, act="tanh", prec=prec, m_total=m)
-        torch.cuda.synchronize()
-        snd = send.view(-1, collective.TILE_ELEMS).cpu()
-        for c in range(plan.nchunks):
-            nt = (plan.chunk_tile0[c + 1] - plan.chunk_tile0[c]) * plan.tiles_per_pair
-            base = plan.chunk_send_off[c] // collective.TILE_ELEMS
-            for o in range(world):
-                for sl in range(plan.chunk_slots[c]):
-                    used = sl * world + o < nt
-                    k = base + o * plan.chunk_slots[c] + sl
-                    assert bool(torch.isnan(snd[k]).any()) != used, (c, o, sl, used)
-        per_chunk = [16 * (plan.chunk_tile0[c + 1] - plan.chunk_tile0[c]) for c in range(plan.nchunks)]
-        assert sync.cpu().tolist() == per_chunk
-        total += torch.nan_to_num(send, nan=0.0)
-    ref = oracle.gram(Xd.double().cpu().numpy(), Wd.double().cpu().numpy(), "tanh")
-    got = np.full((n, n), np.nan)
-    cover = np.zeros((n, n), dtype=int)
-    tot = total.cpu().numpy()
-    for r in range(world):
-        recv = np.concatenate([tot[plan.chunk_send_off[c] + r * plan.chunk_slots[c] * collective.TILE_ELEMS:
-                                   plan.chunk_send_off[c] + (r + 1) * plan.chunk_slots[c] * collective.TILE_ELEMS]
-                               for c in range(plan.nchunks)])
-        cover += collective.scatter_owned(recv, rf.rf_pack_tile_map(plan, r), n, got)
-    I, J = np.triu_indices(n)
-    assert np.all(cover[I, J] == 1)
-    e = float(np.linalg.norm(got[I, J] - ref[I, J]) / np.linalg.norm(ref[I, J]))
-    print(f"[parity] packed G n={n} world={world} {prec}: rel-Frobenius {e:.3e}")
+        for k, (I, J) in enumerate(rf.rf_tile_map(n, world, r)):
+            if I < 0:
+                continue
+            tile = outs[0][r][k * collective.TILE_ELEMS:(k + 1) * collective.TILE_ELEMS].reshape(T, T)
+            rows = S[(S >= I * T) & (S < (I + 1) * T)]
+            cols = S[(S >= J * T) & (S < (J + 1) * T)]
+            for i in rows:
+                js = cols[cols >= i]
+                got[pos[i], pos[js]] = tile[i - I * T, js - J * T]
+                cover[pos[i], pos[js]] += 1
+    iu = np.triu_indices(len(S))
+    assert np.all(cover[iu] == 1)
+    e = float(np.linalg.norm(got[iu] - ref[iu]) / np.linalg.norm(ref[iu]))
+    print(f"[parity] G5 peers emulated n={n} world={world} {prec}: rel-Frobenius {e:.3e}")
     assert e <= TOL[prec]
+    check(f"G5 peers n={n} world={world} {prec}", got[iu], ref[iu], gram_bound(prec, act, Xo[S], Wo, ref, *iu))
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+def collective_sample(n):
+    import synthetic
+    return synthetic.sample_indices(n, count=200, tile_stride=512)
 
 
-def test_reduce_scatter_world1_nccl_equals_dense_gram():
-    import torch.distributed as dist
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = str(_free_port())
-    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    try:
-        n, p, m = 1500, 128, 1024
-        rng = np.random.default_rng(7)
-        Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(torch.bfloat16)
-        Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(torch.bfloat16)
-        rs = collective.GramReduceScatter(n, p, m, m, "sigmoid_half", "bf16", nchunks=4, max_sms=120)
-        for _ in range(3):                          # epochs 1..3 reuse the counters and buffers
-            recv = rs(Xd, Wd)
-        torch.cuda.synchronize()
-        per = [16 * (rs.plan.chunk_tile0[c + 1] - rs.plan.chunk_tile0[c]) for c in range(rs.plan.nchunks)]
-        assert rs.sync.cpu().tolist() == [3 * x for x in per]
-        G = rf.rf_gram(Xd, Wd, act="sigmoid_half", prec="bf16", out="upper")
-        torch.cuda.synchronize()
-        got = np.full((n, n), np.nan, dtype=np.float32)
-        w = collective.scatter_owned(recv.cpu().numpy(), rs.owned_tiles(), n, got)
-        I, J = np.triu_indices(n)
-        assert w[I, J].all()
-        assert np.array_equal(got[I, J], G.cpu().numpy()[I, J]), "packed path must equal the dense K4 bit for bit"
-    finally:
-        dist.destroy_process_group()
+def _dense_vs_packed(ctx, n, p, m, prec, act, calls=2):
+    rng = np.random.default_rng(7)
+    Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(DT[prec])
+    Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(DT[prec])
+    for _ in range(calls):
+        recv = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="packed_tiles", ctx=ctx)
+    G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper", ctx=ctx)
+    torch.cuda.synchronize()
+    got = np.full((n, n), np.nan, dtype=np.float32)
+    w = collective.scatter_owned(recv.cpu().numpy(), rf.rf_tile_map(n, 1, 0), n, got)
+    I, J = np.triu_indices(n)
+    assert w[I, J].all()
+    assert np.array_equal(got[I, J], G.cpu().numpy()[I, J]), "packed tiles must equal the dense K4 bit for bit"
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+def test_peers_world1_equals_dense(prec):
+    ctx = rf.Context(0)
+    ctx.attach_peers(0, 1, 1500)
+    assert ctx.collective() == (0, 1, 2)
+    _dense_vs_packed(ctx, 1500, 128, 1024, prec, "tanh", calls=3)
+    ctx.destroy()
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32", "3xtf32"])
+def test_nccl_world1_equals_dense(prec):
+    ctx = rf.Context(0)
+    ctx.init_nccl(rf.rf_nccl_get_unique_id(), 0, 1)
+    assert ctx.collective() == (0, 1, 1)
+    _dense_vs_packed(ctx, 1300, 96, 768, prec, "sigmoid_half", calls=3)
+    ctx.destroy()
+
+
+def test_collective_errors():
+    ctx = rf.Context(0)
+    X = torch.zeros((300, 64), dtype=torch.bfloat16, device="cuda")
+    W = torch.zeros((128, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(rf.RFError):      # no collective attached
+        rf.rf_gram(X, W, out="packed_tiles", ctx=ctx, G=torch.zeros(65536 * 4, device="cuda"))
+    ctx.attach_peers(0, 2, 300)
+    with pytest.raises(rf.RFError):      # attached but the peer is not connected
+        rf.rf_gram(X, W, out="packed_tiles", ctx=ctx)
+    with pytest.raises(rf.RFError):      # already attached
+        ctx.attach_peers(0, 2, 300)
+    ctx.connect_peers([ctx.peer_base(), ctx.peer_base()])
+    with pytest.raises(rf.RFError):      # n above the n_max of the attach
+        rf.rf_gram(torch.zeros((5000, 64), dtype=torch.bfloat16, device="cuda"), W, out="packed_tiles", ctx=ctx)
+    with pytest.raises(rf.RFError):      # 3×TF32 reads tiles back: not over peers
+        rf.rf_gram(X.float(), W.float(), prec="3xtf32", out="packed_tiles", ctx=ctx)
+    ctx.destroy()
+    with pytest.raises(rf.RFError):
+        rf.Context(0).set_option("k5_wide", 7)

@@ -132,15 +132,15 @@ def test_gram_zero_size_rejected():
 
 
 # ------------------------------------------------------------------------------------------------ Φ
-def _phi_case(X, act, prec, tau=0.0, out="upper", rows=None):
+def _phi_case(X, act, prec, tau=0.0, out="upper", rows=None, ctx=None):
     n = X.shape[0]
     Xd = dev(X, prec)
     Phi = torch.full((n, n), SENTINEL, dtype=torch.float64 if prec == "fp64" else torch.float32, device="cuda")
     if rows is None:
-        rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, Phi=Phi)
+        rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, Phi=Phi, ctx=ctx)
     else:
         for b, e in rows:
-            rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, row_begin=b, row_end=e, Phi=Phi)
+            rf.rf_phi_closed_form(Xd, act=act, tau=tau, prec=prec, out=out, row_begin=b, row_end=e, Phi=Phi, ctx=ctx)
     torch.cuda.synchronize()
     Xo = back(Xd)
     t_used = tau if tau > 0 else oracle.tau_hat(Xo)
@@ -173,13 +173,14 @@ def test_phi_multi_tile_given_tau_full(prec):
 
 
 @pytest.mark.parametrize("prec", ["3xtf32", "bf16"])
-def test_phi_general_epilogue_matches_odd_form(prec, monkeypatch):
+def test_phi_general_epilogue_matches_odd_form(prec):
     """The general EQ1 epilogue (A0, A2 terms kept, used for non-odd σ) on an odd σ: same parity, and within
     a few fp32 ulps of the odd-σ form the library selects by default."""
     X = synthetic.make_X(4, n=700, p=96)
     P_odd, _ = _phi_case(X, "tanh", prec)
-    monkeypatch.setenv("RF_EQ1_GENERAL", "1")
-    P_gen, _ = _phi_case(X, "tanh", prec)
+    ctx = rf.Context(0)
+    ctx.set_option("eq1_general", 1)
+    P_gen, _ = _phi_case(X, "tanh", prec, ctx=ctx)
     I, J = upper_idx(X.shape[0])
     assert np.max(np.abs(P_gen[I, J] - P_odd[I, J])) <= 1e-6 * np.max(np.abs(P_odd[I, J]))
 
@@ -314,15 +315,16 @@ def test_config4_full_size_phi(prec):
 
 @pytest.mark.parametrize("prec", ["bf16", "tf32"])
 @pytest.mark.parametrize("out", ["upper", "full", "packed_tri"])
-def test_phi_wide_epilogue_bit_exact(prec, out, monkeypatch):
+def test_phi_wide_epilogue_bit_exact(prec, out):
     """K5's 16-warp epilogue (p ≤ 512: four warps per TMEM lane quarter, chunks dealt round-robin) computes every
     entry with the same arithmetic as the 8-warp kernel: the two agree bit for bit, in every output layout."""
     X = synthetic.make_X(4, n=1100, p=200)
     Xd = dev(X, prec)
     res = []
-    for wide in ("1", "0"):
-        monkeypatch.setenv("RF_K5_WIDE", wide)
-        P = rf.rf_phi_closed_form(Xd, act="tanh", prec=prec, out=out)
+    ctx = rf.Context(0)
+    for wide in (1, 0):
+        ctx.set_option("k5_wide", wide)
+        P = rf.rf_phi_closed_form(Xd, act="tanh", prec=prec, out=out, ctx=ctx)
         torch.cuda.synchronize()
         res.append(P.cpu().numpy())
     if out == "packed_tri":
@@ -335,7 +337,7 @@ def test_phi_wide_epilogue_bit_exact(prec, out, monkeypatch):
 
 
 @pytest.mark.parametrize("act,prec", [("erf", "bf16"), ("relu", "bf16"), ("erf", "tf32")])
-def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
+def test_k3_multicast_hybrid_bit_exact(act, prec):
     """K3's multicast + pair hybrid (n ≥ 32 row tiles: 4-CTA clusters sharing each B tile as two multicast 64-row
     halves, pair clusters on the leftover SMs) accumulates in the same order as the pair kernel: G agrees bit for
     bit, and with the oracle.  (TF32 truncates its inputs, so a one-sided σ such as ReLU carries a −2e-3 bias
@@ -346,9 +348,10 @@ def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
     W = rng.standard_normal((m, p))
     Xd, Wd = dev(X, prec), dev(W, prec)
     res = []
-    for mc in ("1", "0"):
-        monkeypatch.setenv("RF_K3_MC", mc)
-        G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper")
+    ctx = rf.Context(0)
+    for mc in (1, 0):
+        ctx.set_option("k3_hybrid", mc)
+        G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper", ctx=ctx)
         torch.cuda.synchronize()
         res.append(G)
     assert torch.equal(res[0], res[1])
@@ -363,7 +366,7 @@ def test_k3_multicast_hybrid_bit_exact(act, prec, monkeypatch):
 
 
 @pytest.mark.parametrize("cl8,out", [("0", "upper"), ("1", "upper"), ("0", "full"), ("0", "packed_tri")])
-def test_k4_hybrid_bit_exact(cl8, out, monkeypatch):
+def test_k4_hybrid_bit_exact(cl8, out):
     """K4's multicast + pair hybrid (n ≥ 64 row tiles) — 4-CTA clusters sharing B, or (RF_K4_CL8=1) 8-CTA clusters
     of 2 × 2 pairs sharing A and B — equals the pair-cluster kernel bit for bit (same accumulation order), in the
     dense, mirrored and packed-triangle layouts (the last is what the e2e leg reads back)."""
@@ -371,10 +374,11 @@ def test_k4_hybrid_bit_exact(cl8, out, monkeypatch):
     rng = np.random.default_rng(5)
     Xd = dev(rng.standard_normal((n, p)) / math.sqrt(p), "bf16")
     Wd = dev(rng.standard_normal((m, p)), "bf16")
-    monkeypatch.setenv("RF_K4_CL8", cl8)
-    G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out=out)
-    monkeypatch.setenv("RF_K4_HYBRID", "0")
-    G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper" if out == "packed_tri" else out)
+    ctx = rf.Context(0)
+    ctx.set_option("k4_cl8", int(cl8))
+    G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out=out, ctx=ctx)
+    ctx.set_option("k4_hybrid", 0)
+    G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper" if out == "packed_tri" else out, ctx=ctx)
     torch.cuda.synchronize()
     if out == "packed_tri":   # the same entries through the packed offsets (include/rf.h), sampled rows
         T = -(-n // 256)

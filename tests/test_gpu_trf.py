@@ -155,16 +155,17 @@ def test_ter_rejects_bad_arguments():
         rf.rf_gram_ter(Xd, Td, 0.5, -0.5, 0.5, m_total=10)  # m_total < m_local
 
 
-def test_gram_ter_k3_multicast_hybrid_bit_exact(monkeypatch):
+def test_gram_ter_k3_multicast_hybrid_bit_exact():
     """At n ≥ 32 row tiles K3^ter runs as the multicast + pair hybrid; its fp8 feature codes and hence G^ter are
     the pair kernel's bit for bit (same accumulation order, same σ^ter decision)."""
     n, p, m, eps = 8448 + 77, 128, 1024 + 40, 0.9
     Xd, Td, Xb, T = _inputs(n, p, m, eps, cfg=1)
     sm, sp = rf.rf_trf_thresholds_for("tanh", 1.0)
     res = []
-    for mc in ("1", "0"):
-        monkeypatch.setenv("RF_K3_MC", mc)
-        G = rf.rf_gram_ter(Xd, Td, eps, sm, sp, out="upper")
+    ctx = rf.Context(0)
+    for mc in (1, 0):
+        ctx.set_option("k3_hybrid", mc)
+        G = rf.rf_gram_ter(Xd, Td, eps, sm, sp, out="upper", ctx=ctx)
         torch.cuda.synchronize()
         res.append(G)
     assert torch.equal(res[0], res[1])

@@ -1,8 +1,8 @@
-"""World-size-2 CPU (gloo) tests of the multi-GPU host logic: feature sharding of W and the chunked
-reduce-scatter of the packed triangle tiles of the partial G (include/rf.h G5: the library's plan and tile
-map, the chunk views of collective.py).  The partial G of each rank
-is produced by the oracle (the CPU stand-in for rf_gram on that rank's W shard) so the collective logic
-runs exactly as in bench.py, over gloo instead of NCCL."""
+"""CPU tests of the multi-GPU host logic (include/rf.h "G5"): the canonical tile ownership rf_tile_map (host-only C ABI
+call, no GPU needed), feature sharding of W, and a world-size-2 gloo run of the exchange layout: each rank's partial
+G over its W rows (the oracle stands in for rf_gram on that rank's shard) is cut into the owners' slots by
+rf_tile_map and summed with a reduce-scatter — the data movement the library's collective rf_gram does on the GPU
+(peer-memory stores into the owners' staging buffers, or NCCL), here over gloo."""
 import os
 import socket
 
@@ -13,7 +13,10 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
+import paper_2110_01899_b200 as rf
 from paper_2110_01899_b200 import collective
+
+T_ = collective.RF_PACK_TILE
 
 
 def _free_port():
@@ -24,29 +27,49 @@ def _free_port():
     return p
 
 
-def pack_host(G, plan):
-    """Test stand-in for K4's packed epilogue: place every slot's 256×256 tile of the (full, symmetric) partial
-    G into the chunk-major / owner-major send layout of include/rf.h (zero padding past n)."""
-    n = G.shape[0]
-    T = collective.RF_PACK_TILE
-    send = np.zeros(plan.send_elems, dtype=np.float32)
-    Gp = np.zeros((((n + 511) // 512) * 512,) * 2)
-    Gp[:n, :n] = G
-    maps = [collective.owned_tiles(plan, o) for o in range(plan.world)]
-    for c in range(plan.nchunks):
-        S = plan.chunk_slots[c]
-        k0 = plan.chunk_recv_off[c] // collective.TILE_ELEMS
-        for o in range(plan.world):
-            for s in range(S):
-                I, J = maps[o][k0 + s]
-                if I < 0:
-                    continue
-                off = plan.chunk_send_off[c] + (o * S + s) * collective.TILE_ELEMS
-                send[off:off + collective.TILE_ELEMS] = Gp[I * T:(I + 1) * T, J * T:(J + 1) * T].reshape(-1)
-    return send
+@pytest.mark.parametrize("n", [1, 255, 256, 600, 1024, 4097, 65536])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_tile_map_covers_upper_triangle_exactly_once(n, world):
+    T = -(-n // T_)
+    seen = np.zeros((T, T), dtype=int)
+    slots = None
+    for r in range(world):
+        ij = rf.rf_tile_map(n, world, r)
+        slots = len(ij) if slots is None else slots
+        assert len(ij) == slots, "every rank receives the same number of slots"
+        for I, J in ij:
+            if I < 0:
+                assert J < 0
+                continue
+            assert 0 <= I <= J < T
+            seen[I, J] += 1
+    iu = np.triu_indices(T)
+    assert np.all(seen[iu] == 1)
+    assert seen.sum() == T * (T + 1) // 2
+    # padding: at most one slot per chunk and rank (≤ 16 chunks)
+    assert slots * world - T * (T + 1) // 2 <= 16 * world
 
 
-def _worker(rank, world, port, n, p, m, prec, q):
+def test_tile_map_chunks_are_row_ordered_and_balanced():
+    """Slots follow chunk order (chunks = runs of 8-row-tile groups, the order K4 finishes them), and inside a chunk
+    the owned tiles go row-major; owners' real tiles differ by at most one per chunk."""
+    n, world = 65536, 8
+    maps = [rf.rf_tile_map(n, world, r) for r in range(world)]
+    for ij in maps:
+        real = ij[ij[:, 0] >= 0]
+        key = real[:, 0] * 10 ** 6 + real[:, 1]
+        assert np.all(np.diff(key) > 0), "slots are in (row, column) order"
+    counts = [int(np.sum(ij[:, 0] >= 0)) for ij in maps]
+    assert max(counts) - min(counts) <= 16
+
+
+def test_tile_map_rejects_bad_arguments():
+    for args in [(0, 1, 0), (100, 0, 0), (100, 2, 2), (100, 2, -1)]:
+        with pytest.raises(rf.RFError):
+            rf.rf_tile_map(*args)
+
+
+def _worker(rank, world, port, n, p, m, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -55,29 +78,36 @@ def _worker(rank, world, port, n, p, m, prec, q):
         X = rng.standard_normal((n, p)) / np.sqrt(p)
         W = rng.standard_normal((m, p))
         m0, m1 = collective.feature_shard(m, world, rank)
-        # partial G of this rank, scaled by 1/m_total (what rf_gram_packed computes on its W rows)
-        Gp = oracle.gram(X, W[m0:m1], "tanh", m_total=m)
-        plan = collective.rf_pack_plan(n, world, 5, prec)
-        send = torch.from_numpy(pack_host(Gp, plan))
-        recv = torch.empty(plan.recv_elems, dtype=torch.float32)
-        for snd, rcv in collective.chunk_views(plan, send, recv):      # the chunked collective of G5
-            dist.reduce_scatter_tensor(rcv, snd, op=dist.ReduceOp.SUM)
+        Gp = oracle.gram(X, W[m0:m1], "tanh", m_total=m)          # this rank's partial, scaled by 1/m_total
+        T = -(-n // T_)
+        Gpad = np.zeros((T * T_, T * T_))
+        Gpad[:n, :n] = Gp
+        maps = [rf.rf_tile_map(n, world, o) for o in range(world)]
+        # the staging layout's content: for every owner o, o's slots cut from this rank's partial (whole tiles)
+        send = np.zeros((world, len(maps[0]), T_ * T_), dtype=np.float32)
+        for o in range(world):
+            for k, (I, J) in enumerate(maps[o]):
+                if I >= 0:
+                    send[o, k] = Gpad[I * T_:(I + 1) * T_, J * T_:(J + 1) * T_].reshape(-1)
+        recv = torch.empty(len(maps[0]) * T_ * T_, dtype=torch.float32)
+        dist.reduce_scatter_tensor(recv, torch.from_numpy(send.reshape(-1)), op=dist.ReduceOp.SUM)
         got = np.full((n, n), np.nan)
-        written = collective.scatter_owned(recv.numpy(), collective.owned_tiles(plan, rank), n, got)
+        written = collective.scatter_owned(recv.numpy(), maps[rank], n, got)
         Gfull = oracle.gram(X, W, "tanh")
         err = float(np.max(np.abs(got[written] - Gfull[written]))) if written.any() else 0.0
-        q.put((rank, written, err))
+        hs = collective.exchange_peer_handles(bytes([rank]) * 64)            # the IPC-handle exchange helper
+        q.put((rank, written, err, hs))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,prec", [(600, "bf16"), (1024, "bf16"), (700, "3xtf32")])
-def test_gram_packed_reduce_scatter_gloo_world2(n, prec):
+@pytest.mark.parametrize("n", [600, 1024, 1300])
+def test_g5_exchange_layout_gloo_world2(n):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     world, p, m = 2, 32, 301
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, m, prec, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, p, m, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=180) for _ in range(world)]
@@ -88,9 +118,10 @@ def test_gram_packed_reduce_scatter_gloo_world2(n, prec):
     cover = res[0][1].astype(int) + res[1][1].astype(int)
     iu = np.triu_indices(n)
     assert np.all(cover[iu] == 1), "owned tiles must cover the upper triangle exactly once"
-    for _, written, err in res:
+    for _, written, err, hs in res:
         assert written.sum() > 0
-        assert err < 1e-6, err       # fp32 send buffer: sums of two fp32-rounded partials
+        assert err < 1e-6, err       # fp32 slots: sums of two fp32-rounded partials
+        assert hs == [bytes([0]) * 64, bytes([1]) * 64]
 
 
 def test_feature_shard_partition():
