@@ -43,13 +43,26 @@ def parse():
     ap.add_argument("--no-phi", action="store_true")
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
     ap.add_argument("--no-phi4", action="store_true", help="skip the configs[4] Φ-only measurement")
-    ap.add_argument("--no-ridge", action="store_true", help="skip the NEXT-4 ridge-regression measurement")
     ap.add_argument("--g5", default="peers", choices=["peers", "nccl"],
                     help="N>1: G5 as the peer-memory exchange in K4's epilogue (default) or chunked NCCL reduce-scatter")
     ap.add_argument("--same-gpu", action="store_true",
                     help="testing only: every rank on cuda:0 with a gloo process group (peer G5 over CUDA IPC), so the "
                          "N>1 branch runs on a one-GPU box")
     return ap.parse_args()
+
+
+def source_hash() -> str:
+    """sha256 (12 hex digits) of the library's sources (csrc/* and include/rf.h): the key of the ncu DRAM-traffic
+    records in profiles/ncu_traffic.json, so a kernel change can never be reported with stale bytes."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2110_01899_b200", "csrc")
+    for f in sorted(os.listdir(csrc)) + ["../../include/rf.h"]:
+        path = os.path.normpath(os.path.join(csrc, f))
+        if os.path.isfile(path):
+            h.update(os.path.basename(path).encode())
+            h.update(open(path, "rb").read())
+    return h.hexdigest()[:12]
 
 
 def peaks():
@@ -88,6 +101,30 @@ def tf32_peak_tflops(device):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+def fp8_peak_tflops(device):
+    """Dense FP8 (e4m3) tensor peak measured in this run for the TRF leg's fp8 SYRK roofline: cuBLASLt through
+    torch._scaled_mm at 8192³ (row-major A, column-major B, unit scales), best of 5 after warm-up; None if the
+    call is unavailable.  Only a roofline denominator."""
+    import torch
+    try:
+        a = torch.randn(8192, 8192, device=device).to(torch.float8_e4m3fn)
+        b = torch.randn(8192, 8192, device=device).to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device=device)
+        for _ in range(3):
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
 def cores_used():
     try:
         from threadpoolctl import threadpool_info
@@ -120,13 +157,58 @@ def oracle_sample(cfg, size, seed=0):
     return time.perf_counter() - t0, flops
 
 
+# |S| of the oracle's principal sample per config (rows i ∈ S: G_SS over all m features + Φ_SS), shared by the
+# reference arm and the cpu_baseline so the two time the same work; about 5-10 s of fp64 work on 16 host cores
+ORACLE_SAMPLE = {0: 256, 1: 1024, 2: 1024, 3: 2048, 4: 4096}
+ORACLE_SAMPLE_1T = {0: 256, 1: 512, 2: 512, 3: 512, 4: 1024}     # the single-thread leg (same work per entry)
+
+
+def blas_threads(k):
+    """Context manager limiting the BLAS pool (NumPy's matmul) to k threads (None: no limit)."""
+    import contextlib
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=k, user_api="blas") if k else contextlib.nullcontext()
+    except Exception:
+        return contextlib.nullcontext()
+
+
+def workload_flops(cfg, do_gram=True, do_phi=True):
+    return ((2.0 * cfg.m * cfg.n * cfg.p + cfg.m * cfg.n * (cfg.n + 1.0)) if (cfg.m and do_gram) else 0.0) + \
+        (cfg.p * cfg.n * (cfg.n + 1.0) if do_phi else 0.0)
+
+
+def cpu_baseline_measure(cfg, cfg_idx):
+    """The oracle as it stands (SURVEY.md §8(d) "Oracle timing"): fp64 NumPy on the host cores at all threads and at
+    one thread, each on a principal sample of the workload, plus the full-matrix time extrapolated from the
+    all-core rate (labelled as such: the oracle is never run at full size)."""
+    S = ORACLE_SAMPLE[cfg_idx]
+    S1 = ORACLE_SAMPLE_1T[cfg_idx]
+    oracle_sample(cfg, 128)                                    # warm the caches / BLAS pool
+    with blas_threads(None):
+        t_all, f_all = oracle_sample(cfg, S, seed=1)
+    with blas_threads(1):
+        t_1, f_1 = oracle_sample(cfg, S1, seed=2)
+    r_all, r_1 = f_all / t_all, f_1 / t_1
+    full = workload_flops(cfg)
+    return {"value": r_all / 1e12, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
+            "sample": f"|S|={S} random rows of configs[{cfg_idx}]: G_SS (σ(W x_i) over all m={cfg.m}) + Φ_SS by the "
+                      f"18-term EQ1, fp64 NumPy, {t_all:.1f} s",
+            "threads_all": {"value": r_all / 1e12, "threads": cores_used(), "seconds": t_all, "sample_rows": S},
+            "threads_1": {"value": r_1 / 1e12, "threads": 1, "seconds": t_1, "sample_rows": S1},
+            "extrapolated_full_s": full / r_all,
+            "extrapolated_full_s_1thread": full / r_1,
+            "extrapolation": "full-matrix oracle time = algorithmic flops of the whole workload / the measured rate "
+                             "(an estimate: the oracle is only ever run on the sample)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import synthetic
     cfg = synthetic.CONFIGS[args.config]
-    size = 512
+    size = ORACLE_SAMPLE[args.config]
     for _ in range(max(args.warmup, 0)):
         oracle_sample(cfg, 128)
     tot_t, tot_f = 0.0, 0.0
@@ -135,14 +217,15 @@ def run_reference(args):
         tot_t += t
         tot_f += f
     v = tot_f / tot_t / 1e12
-    sample = (f"|S|={size} random rows of configs[{args.config}] per step: G_SS (σ(W x_i) over all m) + Φ_SS, "
-              f"fp64 NumPy")
+    sample = (f"|S|={size} random rows of configs[{args.config}] per step (the cpu_baseline sample): G_SS (σ(W x_i) "
+              f"over all m) + Φ_SS, fp64 NumPy")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE.json configs)",
             "config": {"workload": f"configs[{args.config}] {cfg.name} (oracle sample)"},
-            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle", "sample": sample,
+                             "extrapolated_full_s": workload_flops(cfg) / (v * 1e12)},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -349,6 +432,7 @@ def main():
     per_launch_alg = {
         "K3_gemm_sigma": ("tensor", 2.0 * (m // world if do_gram else 0) * n * p),
         "K4_syrk": ("tensor", (m // world if do_gram else 0) * n * (n + 1.0)),
+        "K4_syrk_packed": ("tensor", (m // world if do_gram else 0) * n * (n + 1.0)),
         "K5_xtx_eq1": ("tensor", 2.0 * p * phi_entries_local),
     }
     tf32_like = prec in ("tf32", "3xtf32")
@@ -369,11 +453,14 @@ def main():
             d["frac_of_hbm_peak"] = d["achieved_hbm_gbs"] / pk["hbm_gbs"]
         kernels[name] = d
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"]) if kernels else None
-    traffic = None
+    traffic, traffic_source = None, {"sources_sha": source_hash(), "record": None}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get(f"configs[{args.config}]:{prec}:{dom}")
+            tr = json.load(f).get(traffic_source["sources_sha"], {})
+        key = f"configs[{args.config}]:{prec}:w{world}:{dom}"
+        traffic = tr.get(key)
+        if traffic is not None:
+            traffic_source["record"] = key
     except Exception:
         pass
     roof = None
@@ -381,6 +468,8 @@ def main():
         d = kernels[dom]
         roof = {"bound": "tensor", "kernel": dom, "achieved": d["achieved_tflops"], "peak": peak_tensor,
                 "unit": "TFLOP/s", "frac": d["achieved_tflops"] / peak_tensor, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                "traffic_source": traffic_source,
                 "peak_source": pk["source"] + (" sustained bf16" + (" × 0.5 (tf32 nominal ratio)" if tf32_like else "")),
                 "frac_of_burst_peak": d["achieved_tflops"] / (pk["bf16_tflops"] * (0.5 if tf32_like else 1.0))}
         if tf32_like:
@@ -516,16 +605,18 @@ def main():
         k3t = sum(tk.get("K3_ter_features", [0])) / max(1, len(tk.get("K3_ter_features", [])))
         k4t = sum(tk.get("K4_ter_syrk", [0])) / max(1, len(tk.get("K4_ter_syrk", [])))
         fl_t = 2.0 * m_local * n * p + m_local * n * (n + 1.0)
-        fp8_peak = 2.0 * pk["bf16_tflops"]
+        fp8_meas = fp8_peak_tflops(device)
+        fp8_peak = fp8_meas if fp8_meas else 2.0 * pk["bf16_tflops"]
         trf_line = {"what": "G^ter (Algorithm 1 step 4) on the same X, W^ter sparsity eps=0.9, σ^ter matched to "
                             f"{cfg.act} at the Lemma-1 tau (s-={sm:.4f}, s+={sp:.4f}); per rank",
                     "ms_per_step": tms, "tflops": fl_t / (tms * 1e-3) / 1e12,
                     "K3_ter_ms": k3t, "K3_ter_tflops_bf16": 2.0 * m_local * n * p / (k3t * 1e-3) / 1e12 if k3t else None,
                     "K4_ter_ms": k4t, "K4_ter_tflops_fp8": m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12 if k4t else None,
                     "K4_ter_frac_fp8_peak": (m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12) / fp8_peak if k4t else None,
-                    "fp8_peak": fp8_peak, "fp8_peak_source": "2 × measured burst bf16 (nominal fp8/bf16 ratio); "
-                                                              "ternary operands toggle few bits, so the power cap "
-                                                              "bites less than for the random-bf16 measurement",
+                    "fp8_peak": fp8_peak,
+                    "fp8_peak_source": ("measured in this run: cuBLASLt fp8 e4m3 8192^3 (torch._scaled_mm), burst, "
+                                        "random operands" if fp8_meas else
+                                        "2 × measured burst bf16 (nominal fp8/bf16 ratio; _scaled_mm unavailable)"),
                     "K4_ter_frac_fp8_nominal_4500": (m_local * n * (n + 1.0) / (k4t * 1e-3) / 1e12) / 4500.0 if k4t else None,
                     "speedup_vs_gaussian_G": ((kernels.get("K3_gemm_sigma", {}).get("avg_ms", 0.0) +
                                                kernels.get("K4_syrk", {}).get("avg_ms", 0.0)) / (k3t + k4t)
@@ -585,86 +676,10 @@ def main():
         del Phi4, X4f
         torch.cuda.empty_cache()
 
-    # ---------------- NEXT-4: random-features ridge regression (the paper's downstream task): the
-    # whole solver including the random features (P:761 footnote), ReLU features with Gaussian W vs TRFs (ε = 0.9)
-    # matched to ReLU (Algorithm 1), on the GMM of P:1177 (p = 512, 1024 training + 512 test samples, m = 5·10^4),
-    # over a γ grid; plus the fp64 Cholesky rate at n = 16384.
-    ridge_line = None
-    if world == 1 and args.config == 3 and not args.no_ridge:
-        n_tr, n_te, pr, mr, eps_r = 1024, 512, 512, 50000, 0.9
-        Xr, yr = synthetic.make_ridge_gmm(n_tr, n_te, pr)
-        Xrd = torch.from_numpy(Xr).to(torch.bfloat16).to(device)
-        Wrd = torch.from_numpy(synthetic.make_W(1, m=mr, p=pr)).to(torch.bfloat16).to(device)
-        Trd = torch.from_numpy(synthetic.make_T(1, eps_r, m=mr, p=pr)).to(torch.bfloat16).to(device)
-        Yrd = torch.from_numpy(yr[:n_tr]).to(device)
-        gam = [1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3, 1e4]
-        tau_r = rf.rf_estimate_tau(Xrd)
-
-        def rf_path():
-            G_ = rf.rf_gram(Xrd, Wrd, act="relu", prec="bf16", out="upper")
-            return rf.rf_ridge(G_, n_tr, gam, Yrd)[1]
-
-        def ter_path():
-            sm_, sp_ = rf.rf_trf_thresholds_for("relu", tau_r)
-            G_ = rf.rf_gram_ter(Xrd, Trd, eps_r, sm_, sp_, out="upper")
-            return rf.rf_ridge(G_, n_tr, gam, Yrd)[1]
-
-        def timed(fn, reps=3):
-            fn()
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(reps):
-                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a_.record(stream)
-                out_ = fn()
-                b_.record(stream)
-                torch.cuda.synchronize()
-                ts.append(a_.elapsed_time(b_))
-            return sorted(ts)[len(ts) // 2], out_
-
-        t_rf, yh_rf = timed(rf_path)
-        t_ter, yh_ter = timed(ter_path)
-        y_te = torch.from_numpy(yr[n_tr:]).to(device)
-        mse_rf = [float(((yh_rf[g] - y_te) ** 2).mean()) for g in range(len(gam))]      # test MSE (reported metric)
-        mse_ter = [float(((yh_ter[g] - y_te) ** 2).mean()) for g in range(len(gam))]
-        del Wrd, Trd
-        # fp64 Cholesky rate: one γ on a 16384-sample Gram (n³/3 flops of the factorisation)
-        nc = 16384
-        Xc = torch.from_numpy(synthetic.make_ridge_gmm(nc, 0, pr)[0]).to(torch.bfloat16).to(device)
-        Wc = torch.from_numpy(synthetic.make_W(1, m=4096, p=pr)).to(torch.bfloat16).to(device)
-        Gc = rf.rf_gram(Xc, Wc, act="relu", prec="bf16", out="upper")
-        Yc = torch.ones((nc, 1), dtype=torch.float64, device=device)
-        wsc = torch.empty(rf.rf_ridge_workspace_size(nc), dtype=torch.uint8, device=device)
-        t_ch, _ = timed(lambda: rf.rf_ridge(Gc, nc, [1.0], Yc, n_test=0, ws=wsc), reps=2)
-        ridge_line = {"what": "NEXT-4 ridge regression, whole solver incl. random features (P:761): ReLU features, "
-                              f"Gaussian W vs TRF ε={eps_r} matched to ReLU; GMM of P:1177, p={pr}, n_train={n_tr}, "
-                              f"n_test={n_te}, m={mr}; {len(gam)} γ values per solve",
-                      "gammas": gam, "test_mse_relu_rf": mse_rf, "test_mse_trf": mse_ter,
-                      "ms_relu_rf": t_rf, "ms_trf": t_ter,
-                      "cholesky_n": nc, "cholesky_ms": t_ch,
-                      "cholesky_fp64_tflops": nc ** 3 / 3.0 / (t_ch * 1e-3) / 1e12}
-        del Gc, Xc, Wc, wsc
-        torch.cuda.empty_cache()
-
     # ---------------- CPU baseline (oracle, rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # a probe at |S| = 1024, then |S| sized for ≈ 10–30 s of CPU work (time ~ |S|^1.5 between the linear
-        # σ(WX) part and the quadratic G_SS part), capped by host memory (≈ 3 fp64 |S| × m arrays)
-        size = 1024
-        t, f = oracle_sample(cfg, size)
-        try:
-            import psutil
-            mem_cap = int(psutil.virtual_memory().available * 0.5 / (3 * 8 * max(m, 1)))
-        except Exception:
-            mem_cap = 4096
-        target = min(8192, mem_cap, int(size * (15.0 / max(t, 1e-3)) ** (1 / 1.5)))
-        if target > size:
-            size = target // 256 * 256
-            t, f = oracle_sample(cfg, size, seed=1)
-        cpu = {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores_used(), "kind": "oracle",
-               "sample": f"|S|={size} random rows of configs[{args.config}]: G_SS (σ(W x_i) over all m={m}) + "
-                         f"Φ_SS by the 18-term EQ1, fp64 NumPy, {t:.1f} s"}
+        cpu = cpu_baseline_measure(cfg, args.config)
 
     if rank == 0:
         line = {
@@ -688,7 +703,6 @@ def main():
             "entries_per_s": entries, "pct_tensor_peak_sustained": (roof or {}).get("frac"),
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches[0], "clocks": clk, "peaks": pk, "trf": trf_line, "phi_configs4": phi4_line,
-            "ridge": ridge_line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

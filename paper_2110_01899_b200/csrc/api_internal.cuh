@@ -478,7 +478,7 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   g.off_nrm2 = off; off = align256(off + (size_t)n * 8);
   g.off_tau = off; off = align256(off + 16);
   g.off_rc = off; off = align256(off + (size_t)n * (prec == RF_PREC_FP64 ? sizeof(rfk::RowCoefD) : sizeof(rfk::RowCoef)));
-  g.off_nrm2o = off; off = align256(off + (size_t)n * 8);
+  g.off_nrm2o = off; off = align256(off + (size_t)round_up(n, 256) * 8);   // ‖x_j‖²/τ, padded to whole tiles (K5)
   if (prec == RF_PREC_3XTF32) {
     g.off_xhi = off; off = align256(off + (size_t)n * g.ldp * 4);
     g.off_xlo = off; off = align256(off + (size_t)n * g.ldp * 4);

@@ -97,7 +97,10 @@ template <typename RC, typename NT>
 __global__ void __launch_bounds__(256) k_row_coef(const double* __restrict__ nrm2, int64_t n, RowMoments m,
                                                   RC* __restrict__ rc, NT* __restrict__ njt_out) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n) {   // the grid covers whole 256-column tiles: zero the padding K5 stages with each tile
+    njt_out[i] = (NT)0;
+    return;
+  }
   const double r2 = nrm2[i];
   const double ua = sqrt(r2);                       // u_a = ‖x_i‖
   const double al = ua * m.inv_st - 1.0;            // α = u_a/√τ − 1

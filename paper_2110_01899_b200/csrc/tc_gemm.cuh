@@ -14,7 +14,7 @@
 // K-block = one 128-byte swizzle row (64 bf16 / 32 fp32).
 //
 // Warp roles (128 + 32·kEpiW threads per CTA): w0 TMA producer, w1 MMA issuer (leader CTA, one thread), w2 TMEM
-// allocator, w3 idle, w4.. epilogue (warp w: TMEM lane quarter w%4; with 8 epilogue warps column half (w-4)/4,
+// allocator, w3 column-vector loader (kColVec epilogues; else idle), w4.. epilogue (warp w: TMEM lane quarter w%4; with 8 epilogue warps column half (w-4)/4,
 // with 12 / 16 the 32-column chunks ≡ (w-4)/4 mod 3 / 4).
 // Pipelines: smem ring (full barrier in the leader, empty barriers in both CTAs) TMA→MMA; TMEM
 // accumulator slots (2 × 256 columns for BN = 256, 1 × 512 for BN = 512) MMA→epilogue.
@@ -69,11 +69,33 @@ struct TcCfg {
   static constexpr int THREADS = 128 + 32 * kEpiW;
   static constexpr int STG_BUFS = kStg >= 0 ? kStg : ((kSplit == 3 || kBN == 512) ? 1 : 2);   // per epi warp
   static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
-  static constexpr int STAGES = (225 * 1024 - STG_BYTES) / STAGE_BYTES;
-  static constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + STG_BYTES + 256;
+  // per-column vector of the tile (epilogues with kColVec, e.g. ‖x_j‖²/τ of K5), double-buffered with the accumulator
+  static constexpr int COL_BYTES = kBN == 256 ? 2 * 256 * 4 : 0;
+  static constexpr int BAR_BYTES = 256;             // mbarriers (2·STAGES + 6) + the TMEM address word
+  static constexpr int SMEM_MAX = 227 * 1024;       // opt-in dynamic shared memory per CTA
+  static constexpr int STAGES = (SMEM_MAX - STG_BYTES - COL_BYTES - BAR_BYTES) / STAGE_BYTES;
+  // room left to align the dynamic window to 1024 B (the base is 1024-aligned in practice: the kernel checks)
+  static constexpr int SLACK = SMEM_MAX - STAGES * STAGE_BYTES - STG_BYTES - COL_BYTES - BAR_BYTES < 1024
+                                   ? SMEM_MAX - STAGES * STAGE_BYTES - STG_BYTES - COL_BYTES - BAR_BYTES
+                                   : 1024;
+  static constexpr size_t SMEM_BYTES = (size_t)SLACK + (size_t)STAGES * STAGE_BYTES + STG_BYTES + COL_BYTES + BAR_BYTES;
+  static_assert(8 * (2 * STAGES + 6) + 4 <= BAR_BYTES, "barrier area");
   static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt == 3 ? 0u : (uint32_t)kFmt, 256, 256);
   static_assert(STAGES >= 2, "pipeline too shallow");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
+};
+
+// Epilogues that read a per-column vector (one float per accumulator column, e.g. K5's ‖x_j‖²/τ) declare
+// kColVec = 1 and `col_src` (global, padded to whole tiles): the TMA producer of each CTA bulk-copies the tile's slice
+// into shared memory (double-buffered like the accumulator) when the tile starts, so the epilogue reads it with
+// LDS.128 broadcasts instead of waiting on a global load per 32-column chunk.
+template <class E, class = void>
+struct ColVecOf {
+  static constexpr bool value = false;
+};
+template <class E>
+struct ColVecOf<E, decltype(void(E::kColVec))> {
+  static constexpr bool value = E::kColVec != 0;
 };
 
 // Pair-tile scheduler.  Rows of 256, columns of BN.  Rectangular: row tiles [row_tile0, row_tile1) × all
@@ -113,7 +135,7 @@ struct Sched {
     int I0, I1, J0, Jf;
     long long P, cnt;
   };
-  __host__ __device__ Group group(int I0) const {
+  __host__ __device__ __forceinline__ Group group(int I0) const {
     Group g;
     g.I0 = I0;
     g.I1 = I0 + gm < row_tile1 ? I0 + gm : row_tile1;
@@ -133,7 +155,7 @@ struct Sched {
     return g;
   }
   // tile (ti, tj) of index u inside group g
-  __host__ __device__ void in_group(const Group& g, long long u, int& ti, int& tj) const {
+  __host__ __device__ __forceinline__ void in_group(const Group& g, long long u, int& ti, int& tj) const {
     if (u < g.P) {
       int J = g.J0;
       for (;;) {
@@ -176,22 +198,43 @@ struct Sched {
 };
 
 // Monotone cursor over the tile order (each cluster visits t = cid, cid + ncl, … in increasing order, so
-// advancing group by group is amortised O(1)).
+// advancing group by group is amortised O(1)).  The group is held in scalar registers (a struct passed by reference
+// was placed in local memory: 8 STL + 8 LDL per tile and warp).
 struct TileCursor {
   const Sched* s;
-  Sched::Group g;
-  long long base;
+  int I0, I1, J0, Jf;
+  long long P, cnt, base;
+  __device__ __forceinline__ void load(int i0) {
+    const Sched::Group g = s->group(i0);
+    I0 = g.I0; I1 = g.I1; J0 = g.J0; Jf = g.Jf; P = g.P; cnt = g.cnt;
+  }
   __device__ __forceinline__ void init(const Sched* sp) {
     s = sp;
     base = 0;
-    g = s->group(s->row_tile0);
+    load(s->row_tile0);
   }
   __device__ __forceinline__ void get(long long t, int& ti, int& tj) {
-    while (t >= base + g.cnt) {
-      base += g.cnt;
-      g = s->group(g.I1);
+    while (t >= base + cnt) {
+      base += cnt;
+      load(I1);
     }
-    s->in_group(g, t - base, ti, tj);
+    long long u = t - base;
+    if (u < P) {   // partial columns [J0, Jf): column J holds rows I0 .. min(I1, (J + 1)·2^shift) − 1
+      int J = J0;
+      for (;;) {
+        const long long rv = ((long long)(J + 1) << s->shift) - I0;
+        if (u < rv) break;
+        u -= rv;
+        ++J;
+      }
+      ti = I0 + (int)u;
+      tj = J;
+      return;
+    }
+    u -= P;
+    const int rows = I1 - I0;
+    tj = Jf + (int)(u / rows);
+    ti = I0 + (int)(u % rows);
   }
 };
 
@@ -202,6 +245,8 @@ template <int kBufs>
 struct EpiCtx {
   const CUtensorMap* tm;   // fp32 output map: box 32 × 32, 128-B swizzle, bounds = the n×n matrix
   uint8_t* sbuf;           // this warp's staging buffers (kBufs × 4 KB, 1024-B aligned)
+  uint32_t sbuf_s;         // … as a 32-bit shared address (STS, never a generic store)
+  uint32_t col_s;          // kColVec epilogues: shared address of the current tile's column vector
   int cur;
   uint32_t lane;
   int hint;                // 1: stores carry the L2 evict_first hint `pol`
@@ -219,11 +264,10 @@ struct EpiCtx {
     else
       ptx::tma_store_2d(tm, b, c0, r0);
   }
-  __device__ __forceinline__ void stage(uint8_t* b, const float (&v)[32]) {
+  __device__ __forceinline__ void stage(uint32_t b, const float (&v)[32]) {
+    const uint32_t row = b + lane * 128;
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      *reinterpret_cast<float4*>(b + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-          make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    for (int c = 0; c < 8; ++c) ptx::sts128(row + ((c ^ (lane & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
   }
   __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
     static_assert(kBufs >= 1, "store_block needs staging buffers");
@@ -231,12 +275,12 @@ struct EpiCtx {
       if (nst == 0) {
         if (lane == 0) ptx::bulk_wait_read<0>();       // the previous batch has been read out of smem
         __syncwarp();
-        stage(sbuf, v);
+        stage(sbuf_s, v);
         pc0 = (int32_t)col0;
         pr0 = (int32_t)row_lo;
         nst = 1;
       } else {
-        stage(sbuf + 4096, v);
+        stage(sbuf_s + 4096, v);
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -251,7 +295,7 @@ struct EpiCtx {
     uint8_t* b = sbuf + cur * 4096;
     if (lane == 0) ptx::bulk_wait_read<kBufs - 1>();
     __syncwarp();
-    stage(b, v);
+    stage(sbuf_s + cur * 4096, v);
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -545,10 +589,11 @@ struct EpiSyrkPacked {
 // pairs (eq1_pair); kOdd selects the odd-σ form Φ = ν·A1(α)·C1(s) (A0 = A2 = 0 for odd σ).
 template <bool kOdd>
 struct EpiEq1 {
+  static constexpr int kColVec = 1;   // ‖x_j‖²/τ staged per tile in shared memory by the producer (ColVecOf)
   float* Phi;
   int64_t ld, n;
   const RowCoef* rc;     // per row
-  const float* njt;      // ‖x_j‖²/τ per column
+  const float* col_src;  // ‖x_j‖²/τ per column, padded to whole 256-column tiles
   float e0, e1, e2, f0, f1;
   int full;
   int use_tma;
@@ -570,18 +615,20 @@ struct EpiEq1 {
                                              int, long long, const Pre& pf) const {
     const int64_t row = row_lo + cx.lane;
     const RowCoef& c = pf.c;
-    float nj[32];
-    if (col0 + 32 <= n) {
+    float nj[32];   // columns past n hold padding; their results are never stored
+    const uint32_t ca = cx.col_s + (uint32_t)(col0 & 255) * 4;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(njt + col0) + q);
-        nj[4 * q] = t.x; nj[4 * q + 1] = t.y; nj[4 * q + 2] = t.z; nj[4 * q + 3] = t.w;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e) nj[e] = (col0 + e < n) ? __ldg(njt + col0 + e) : 1.f;
+    for (int q = 0; q < 8; ++q) {
+      const float4 t = ptx::lds128(ca + 16 * q);
+      nj[4 * q] = t.x; nj[4 * q + 1] = t.y; nj[4 * q + 2] = t.z; nj[4 * q + 3] = t.w;
     }
     float v[32];
+#if defined(K5_EXP) && K5_EXP == 3
+    if (true) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) + nj[e];
+    } else
+#endif
     if (col0 + 31 >= row_lo && col0 <= row_lo + 31) {   // chunk holds diagonal entries (warp-uniform)
 #pragma unroll
       for (int e = 0; e < 32; ++e)
@@ -601,6 +648,29 @@ struct EpiEq1 {
         eq1_pair<kOdd>(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, a0_2, a1_2, a2h_2, e0_2,
                        e1_2, e2_2, f0_2, f1_2, v[e], v[e + 1]);
     }
+#if defined(K5_EXP)   // timing experiments only (scripts): 1 = no store at all, 2 = STS staging but no TMA store
+    if (K5_EXP == 1 || K5_EXP == 2) {
+      if (K5_EXP == 2) {
+        cx.stage(cx.sbuf_s, v);
+        ptx::fence_proxy_async_smem();
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) acc += v[e];
+      if (acc == 1.2345e-30f) Phi[0] = acc;
+      return;
+    }
+#endif
+#if defined(K5_EXP) && K5_EXP == 6   // timing experiment: each lane stores its row's 32 floats as four full sectors
+    if (tri_T == 0 && !full && col0 >= row_lo + 31 && col0 + 32 <= n && row < n && ((ld & 7) == 0)) {
+      float* dst = Phi + row * ld + col0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        ptx::stg256(dst + 8 * q, v[8 * q], v[8 * q + 1], v[8 * q + 2], v[8 * q + 3], v[8 * q + 4], v[8 * q + 5],
+                    v[8 * q + 6], v[8 * q + 7]);
+      return;
+    }
+#endif
     if (tri_T > 0) {
       tri_store(cx, Phi, n, tri_T, use_tma, row_lo, col0, v);
       return;
@@ -737,15 +807,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment by an offset from the __shared__ array (not an integer round trip), so the compiler keeps the
   // shared address space and the epilogue's staging stores compile to STS, not generic ST
-  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
+  if (pad > (uint32_t)Cfg::SLACK) __trap();   // never seen: the dynamic window starts 1024-aligned
+  uint8_t* smem = smem_raw + pad;
   uint8_t* sA = smem;                                                    // [STAGES][NOPS][A_BYTES]
   uint8_t* sB = sA + (size_t)STAGES * NOPS * Cfg::A_BYTES;               // [STAGES][NOPS][NSUB][B_BYTES]
   uint8_t* sStg = sB + (size_t)STAGES * NOPS * NSUB * Cfg::B_BYTES;      // [EPI_WARPS][STG_BUFS][4096]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Cfg::STG_BYTES);
+  float* sCol = reinterpret_cast<float*>(sStg + Cfg::STG_BYTES);          // [2][BN] column vectors (kColVec)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Cfg::STG_BYTES + Cfg::COL_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* colfull = tempty + 2;
+  uint64_t* colempty = colfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colempty + 2);
+  constexpr bool kCol = ColVecOf<Epi>::value;
+  static_assert(!kCol || (Cfg::COL_BYTES > 0 && Cfg::CL == 2), "column vectors: 256-wide pair tiles, clusters of 2");
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -772,6 +849,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS);
+      ptx::mbar_init(&colfull[a], 1);
+      ptx::mbar_init(&colempty[a], Cfg::EPI_WARPS);
     }
     ptx::fence_mbarrier_init();
   }
@@ -828,9 +907,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               __nanosleep(256);
             }
           }
+#if defined(K5_EXP) && K5_EXP == 5
+          constexpr bool kSkipA = kCol;   // timing experiment: no A operand loads (stale smem, wrong results)
+#else
+          constexpr bool kSkipA = false;
+#endif
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);   // both CTAs' bytes
+            if (rank == 0)   // both CTAs' bytes
+              ptx::mbar_arrive_expect_tx(&full[stage], 2 * (Cfg::STAGE_BYTES - (kSkipA ? Cfg::A_BYTES : 0)));
             const uint32_t fb = full0 + stage * 8;
             const int k = kb * Cfg::BK;
             uint8_t* a = sA + (size_t)(stage * NOPS) * Cfg::A_BYTES;
@@ -842,7 +927,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                                       mcA8, pol);
               ptx::tma_load_2d_cg2_mc(b + di * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)di, mcB8,
                                       pol);
-            } else {
+            } else if (!kSkipA) {
               ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
             }
             if (Cfg::CL == 8) {
@@ -936,6 +1021,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
       }
     }
+  } else if (warp == 3) {
+    if constexpr (kCol) {
+      // ===== Column-vector loader: tile k's slice of the per-column vector into sCol[k & 1] once the epilogue has
+      // released the buffer (tile k − 2), a 1-D bulk copy completing on colfull.  A warp of its own, so the operand
+      // producer never waits on the epilogue.
+      TileCursor cur;
+      cur.init(&sched);
+      int tcount = 0;
+      for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {
+        int ti, tj;
+        cur.get(t, ti, tj);
+        if (lane == 0) {
+          const int cs = tcount & 1;
+          ptx::mbar_wait(&colempty[cs], ((tcount >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&colfull[cs], Cfg::BN * 4);
+          ptx::bulk_load_1d(sCol + cs * Cfg::BN, epi.col_src + (int64_t)tj * Cfg::BN, Cfg::BN * 4, &colfull[cs]);
+        }
+        __syncwarp();
+      }
+    }
   } else if (warp >= 4) {
     // ===== Epilogue: TMEM → registers → fused op → global (8 warps) =====
     const uint32_t q = warp & 3;               // TMEM lane quarter this warp may access
@@ -943,6 +1048,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     EpiCtx<Cfg::STG_BUFS> cx;
     cx.tm = &tmOut;
     cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
+    cx.sbuf_s = ptx::smem_u32(cx.sbuf);
+    cx.col_s = 0;
     cx.cur = 0;
     cx.nst = 0;
     cx.pc0 = cx.pr0 = 0;
@@ -954,13 +1061,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     int it = 0;
     TileCursor cur;
     cur.init(&sched);
-    for (int t = cid; t < sched.num_tiles; t += ncl) {
+    int tcount = 0;
+    for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {
       int ti, tj;
       cur.get(t, ti, tj);
       if (Cfg::CL == 4) ti = 2 * ti + (int)pi;
       if (Cfg::CL == 8) {
         ti = 2 * ti + (int)(pi & 1u);
         tj = 2 * tj + (int)(pi >> 1);
+      }
+      if constexpr (kCol) {   // the tile's column vector (bulk-copied by this CTA's producer when the tile started)
+        ptx::mbar_wait(&colfull[tcount & 1], (tcount >> 1) & 1);
+        cx.col_s = ptx::smem_u32(sCol + (tcount & 1) * Cfg::BN);
       }
       const int64_t row_lo = (int64_t)ti * Cfg::BM + rank * 128 + q * 32;
       const int64_t colb = (int64_t)tj * Cfg::BN + h * HALF;
@@ -1004,6 +1116,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         cx.flush();
         epi.tile_done(ti, lane);
+        if constexpr (kCol) {
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&colempty[tcount & 1]);
+        }
         continue;
       }
       for (int c = 0; c < nchunks; ++c, ++it) {
@@ -1018,16 +1134,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           ptx::mbar_wait(&tfull[slot], acc_phase);
           ptx::tc_fence_after();
           uint32_t ra[32];
+          constexpr int STEP = Cfg::EPI_WARPS / 4;
 #pragma unroll 1
-          for (int cc = (int)h; cc < Cfg::ACC_COLS / 32; cc += Cfg::EPI_WARPS / 4) {
+          for (int cc = (int)h; cc < Cfg::ACC_COLS / 32; cc += STEP) {
             ptx::tmem_ld_32x32b_x32(tb + cc * 32, ra);
             ptx::tmem_ld_wait();
+            if (cc + STEP >= Cfg::ACC_COLS / 32) {
+              // the warp's last chunk is in registers: hand the accumulator back to the MMA now, before its
+              // transform and store, so the next tile's MMAs into this slot start one chunk earlier
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
+            }
             const int64_t col0 = col_t + cc * 32;
             if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, ra, c, nchunks, (long long)t, pf);
           }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
           continue;
         }
         const typename Epi::Pre pf = epi.prefetch(row_lo, colb, lane);   // per-row inputs: before the wait
@@ -1042,7 +1163,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         auto step = [&](int cc, uint32_t(&cur)[32], uint32_t(&nxt)[32]) __attribute__((always_inline)) {
           const int64_t col0 = colb + cc * 32;
           ptx::tmem_ld_wait();
-          if (cc + 1 < NCH) ptx::tmem_ld_32x32b_x32(tbase + (cc + 1) * 32, nxt);
+          if (cc + 1 < NCH) {
+            ptx::tmem_ld_32x32b_x32(tbase + (cc + 1) * 32, nxt);
+          } else {   // all of the warp's accumulator columns are in registers: release the slot before the last chunk
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
+          }
           if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, cur, c, nchunks, (long long)t, pf);
         };
         ptx::tmem_ld_32x32b_x32(tbase, ra);
@@ -1051,12 +1178,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           step(cc, ra, rb);
           step(cc + 1, rb, ra);
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
       }
       cx.flush();
       epi.tile_done(ti, lane);
+      if constexpr (kCol) {   // done reading this tile's column vector
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&colempty[tcount & 1]);
+      }
     }
     if (lane == 0) ptx::bulk_wait_all();
   }
