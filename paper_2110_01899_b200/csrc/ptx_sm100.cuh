@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace rfk {
 namespace ptx {
@@ -50,10 +51,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// RF_DEBUG builds (-DRF_DEBUG): a wait that has not completed after ~2^26 try_wait rounds (seconds) reports the
+// barrier and the parity it expected and traps — a phase-tracking bug shows up as an error instead of a hang.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+#if defined(RF_DEBUG)
+  uint32_t spins = 0;
+  while (!mbar_try_wait(a, parity)) {
+    if (++spins == (1u << 26)) {
+      printf("[rf debug] mbarrier wait timeout: block %d thread %d smem 0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, a, parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(a, parity)) {
   }
+#endif
 }
 
 // ---------------------------------------------------------------- global progress words (soft lockstep)

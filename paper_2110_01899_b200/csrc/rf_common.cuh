@@ -7,6 +7,25 @@
 
 #include "../../include/rf.h"
 
+// RF_DEBUG builds: device-side bounds / invariant checks on the store paths (compute-sanitizer is not available on
+// this GPU pool; these asserts stand in for memcheck on the hand-written epilogues).  Release builds: no code.
+#if defined(RF_DEBUG)
+#include <cstdio>
+#define RF_DCHECK(cond, ...)                                                                              \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("[rf debug] check failed: %s (block %d thread %d) ", #cond, (int)blockIdx.x, (int)threadIdx.x); \
+      printf(__VA_ARGS__);                                                                                \
+      printf("\n");                                                                                      \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define RF_DCHECK(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+
 namespace rfk {
 
 // ------------------------------------------------------------------------------------------

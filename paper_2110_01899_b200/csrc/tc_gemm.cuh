@@ -321,6 +321,8 @@ struct EpiCtx {
 // Direct masked stores of row `row`, columns [col0, col0+32) ∩ [lo, n) into a row-major fp32 matrix.
 __device__ __forceinline__ void store_row_masked(float* M, int64_t ld, int64_t n, int64_t row, int64_t col0, int64_t lo,
                                                  const float (&v)[32]) {
+  RF_DCHECK(row >= 0 && col0 >= 0 && col0 < n && ld >= n, "row %lld col0 %lld n %lld ld %lld", (long long)row,
+            (long long)col0, (long long)n, (long long)ld);   // n: the column bound (rows are bounded by the caller)
   float* dst = M + row * ld + col0;
   if (col0 >= lo && col0 + 32 <= n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
@@ -352,6 +354,8 @@ __device__ __forceinline__ void tri_store(Ctx& cx, float* P, int64_t n, int64_t 
                                           int64_t col0, const float (&v)[32]) {
   const int64_t ti = row_lo >> 8, tj = col0 >> 8;
   const int64_t u = tri_tile_index(ti, tj, T);
+  RF_DCHECK(tj >= ti && tj < T && u < T * (T + 1) / 2, "packed tile (%lld, %lld) of T %lld", (long long)ti, (long long)tj,
+            (long long)T);
   const int64_t lr = row_lo & 255, lc = col0 & 255;
   if (use_tma && col0 >= row_lo + 31) {
     cx.store_block(u * 256 + lr, lc, v);
@@ -388,6 +392,7 @@ struct EpiSigma {
                                              int, long long, const Pre&) const {
     const int64_t row = row_lo + cx.lane;
     if (row >= M) return;
+    RF_DCHECK(col0 >= 0 && col0 < N, "K3 col0 %lld N %lld", (long long)col0, (long long)N);
     float s[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e)
@@ -562,6 +567,10 @@ struct EpiSyrkPacked {
     const int64_t r0 = pk.crow[c];
     const int64_t u = (I - r0) * pk.T - (I * (I - 1) - r0 * (r0 - 1)) / 2 + (J - I);   // row-major in the chunk
     const int64_t owner = u % pk.world, slot = u / pk.world;
+    RF_DCHECK(J >= I && J < pk.T && c >= 0 && c < pk.nchunks && I >= pk.crow[c] && I < pk.crow[c + 1] && u >= 0 &&
+                  slot < pk.slots[c] && (!pk.p2p || pk.peer[owner] != nullptr),
+              "G5 tile (%lld, %lld) chunk %d u %lld slot %lld", (long long)I, (long long)J, c, (long long)u,
+              (long long)slot);
     float* tile = pk.p2p ? pk.peer[owner] + (int64_t)pk.self * pk.recv_elems + pk.roff[c] +
                                slot * (int64_t)(RF_PACK_TILE * RF_PACK_TILE)
                          : pk.send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
@@ -860,6 +869,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+#if defined(RF_DEBUG)
+  // the pair allocates all 512 columns of each CTA's TMEM: the base must be lane 0, column 0 (a leaked or
+  // concurrent allocation would show up here)
+  if (tmem_base != 0u) {
+    printf("[rf debug] TMEM allocation base 0x%x (expected 0) block %d\n", tmem_base, (int)blockIdx.x);
+    __trap();
+  }
+#endif
   const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
 
   if (warp == 0) {
