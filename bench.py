@@ -159,8 +159,8 @@ def oracle_sample(cfg, size, seed=0):
 
 # |S| of the oracle's principal sample per config (rows i ∈ S: G_SS over all m features + Φ_SS), shared by the
 # reference arm and the cpu_baseline so the two time the same work; about 5-10 s of fp64 work on 16 host cores
-ORACLE_SAMPLE = {0: 256, 1: 1024, 2: 1024, 3: 2048, 4: 4096}
-ORACLE_SAMPLE_1T = {0: 256, 1: 512, 2: 512, 3: 512, 4: 1024}     # the single-thread leg (same work per entry)
+ORACLE_SAMPLE = {0: 256, 1: 1024, 2: 2048, 3: 4096, 4: 4096}
+ORACLE_SAMPLE_1T = {0: 256, 1: 512, 2: 1024, 3: 1024, 4: 1024}     # the single-thread leg (same work per entry)
 
 
 def blas_threads(k):
