@@ -1,8 +1,8 @@
-"""Experiment: K3/K4 device time, SM clock and board power on configs[3]-shaped inputs, swept over
-the L2 raster group size (env RF_GM) and over operand data (random vs all-zero Σ, to see how much of
-the power-capped clock is data-dependent).  Not part of the product path; run under gpurun.
+"""Experiment: K3/K4 device time, SM clock and board power on configs[3]-shaped inputs, swept over the K4 soft
+lockstep window (context option lock_w) and over operand data (random vs all-zero Σ, to see how much of the
+power-capped clock is data-dependent).  Not part of the product path; run under gpurun.
 
-  python scripts/k4_energy.py [--gm 1,4,8,16] [--reps 3]
+  python scripts/k4_energy.py [--lockw 0,24] [--zero] [--reps 3]
 """
 import argparse
 import os
@@ -16,7 +16,6 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gm", default="1,4,8,16")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--m", type=int, default=65536)
@@ -35,20 +34,20 @@ def main():
     G = torch.empty(a.n, ldg, device=dev)[:, :a.n]
     ws = torch.empty(rf.rf_gram_workspace_size(a.p, a.n, a.m, "bf16"), dtype=torch.uint8, device=dev)
     rf.rf_profile_enable(True)
-    cases = [("rand", W, gm, lw) for gm in a.gm.split(",") for lw in a.lockw.split(",")]
+    ctx = rf.Context(0)
+    cases = [("rand", W, lw) for lw in a.lockw.split(",")]
     if a.zero:
-        cases.append(("zero", torch.zeros_like(W), a.gm.split(",")[-1], a.lockw.split(",")[-1]))
-    for tag, Wc, gm, lw in cases:
-        os.environ["RF_GM"] = str(gm)
-        os.environ["RF_LOCKW"] = str(lw)
-        rf.rf_gram(X, Wc, act="sigmoid_half", prec="bf16", G=G, ws=ws)
+        cases.append(("zero", torch.zeros_like(W), a.lockw.split(",")[-1]))
+    for tag, Wc, lw in cases:
+        ctx.set_option("lock_w", int(lw))
+        rf.rf_gram(X, Wc, act="sigmoid_half", prec="bf16", G=G, ws=ws, ctx=ctx)
         torch.cuda.synchronize()
         rf.rf_profile_read()
         smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits",
                                 "-lms", "100"], stdout=subprocess.PIPE, text=True)
         time.sleep(0.3)
         for _ in range(a.reps):
-            rf.rf_gram(X, Wc, act="sigmoid_half", prec="bf16", G=G, ws=ws)
+            rf.rf_gram(X, Wc, act="sigmoid_half", prec="bf16", G=G, ws=ws, ctx=ctx)
         torch.cuda.synchronize()
         smi.terminate()
         out = smi.communicate()[0]
@@ -62,7 +61,7 @@ def main():
         med = lambda x: x[len(x) // 2] if x else float("nan")
         fl4 = a.m * a.n * (a.n + 1)
         fl3 = 2.0 * a.m * a.n * a.p
-        print(f"[{tag} gm={gm} lockw={lw}] K3 {med(sorted(k3)):.2f} ms ({fl3 / med(sorted(k3)) / 1e9:.0f} TF/s)  "
+        print(f"[{tag} lockw={lw}] K3 {med(sorted(k3)):.2f} ms ({fl3 / med(sorted(k3)) / 1e9:.0f} TF/s)  "
               f"K4 {med(sorted(k4)):.2f} ms ({fl4 / med(sorted(k4)) / 1e9:.0f} TF/s)  "
               f"sm_mhz med {med(busy):.0f} (min {busy[0] if busy else 0:.0f})  power med {med(pw):.0f} W max "
               f"{pw[-1] if pw else 0:.0f} W  samples {len(clk)}", flush=True)

@@ -2,14 +2,13 @@
 """Per-rank work of the R-GPU step, measured one rank at a time on ONE B200.
 
 For R in {1, 2, 4, 8} and every rank r < R this runs exactly what rank r runs in `bench.py --gpus R` with the
-fused G5 (collective.GramFusedP2P), minus the NVLink transfer itself:
-  * rf_gram_packed_p2p on W's rows [r·m/R, (r+1)·m/R) with the R-rank pack plan, every owner's staging buffer
-    being a local allocation (so the peer stores land in local HBM instead of crossing NVLink);
-  * rf_pack_reduce of the rank's own R staging slices;
-  * rf_phi_closed_form over the rank's Φ row block (rf_phi_row_split).
-No kernel waits on another (the phases are separate launches), so this is not a multi-rank emulation on one GPU
-in the sense the profiling guide forbids.  The predicted R-GPU step time is the max over ranks; the NVLink
-volume each rank would send, (R−1)/R of its partial triangle, is printed beside the SYRK time it must hide under.
+peer-memory G5 (the collective rf_gram on a context attached as rank r of R), minus the NVLink transfer itself: R
+contexts in this process are connected by raw pointers (rf_ctx_connect_peers), so the peer stores of K4's epilogue
+land in local HBM instead of crossing NVLink.  Each call is enqueued in its two halves (RF_OPT_G5_PHASES test hook):
+phase 1 (K3 + K4 with the packed stores + arrival flags) of every rank, each timed, then phase 2 (arrival waits +
+owner-side sum + release flags) of every rank, each timed; then Φ over the rank's row block (rf_phi_row_split).  No
+kernel waits on another.  The predicted R-GPU step time is the max over ranks; the NVLink volume each rank would
+send, (R−1)/R of its partial triangle, is printed beside the SYRK time it must hide under.
 
   python scripts/rank_emulation.py [--config 3] [--ranks 1,2,4,8] [--reps 3]
 """
@@ -63,32 +62,55 @@ def main():
 
     out = []
     for R in [int(s) for s in args.ranks.split(",")]:
-        plan = rf.rf_pack_plan(n, R, 16, args.prec)
-        staging = [torch.empty(R * plan.recv_elems, dtype=torch.float32, device=dev) for _ in range(R)]
-        ptrs = [s.data_ptr() for s in staging]
-        recv = torch.empty(plan.recv_elems, dtype=torch.float32, device=dev)
+        ctxs = [rf.Context(0) for _ in range(R)]
+        for r, c in enumerate(ctxs):
+            c.attach_peers(r, R, n)
+        bases = [c.peer_base() for c in ctxs]
+        for c in ctxs:
+            c.connect_peers(bases)
         m_local = m // R
-        ws = torch.empty(rf.rf_gram_workspace_size(p, n, m_local, args.prec), dtype=torch.uint8, device=dev)
+        Ws = [Wfull[r * m_local:(r + 1) * m_local] for r in range(R)]
+        slots = len(rf.rf_tile_map(n, R, 0))
+        recv = torch.empty(slots * 65536, dtype=torch.float32, device=dev)
+        ws = torch.empty(rf.rf_workspace_size("gram", p, n, m_local, args.prec, "packed_tiles", ctx=ctxs[0]),
+                         dtype=torch.uint8, device=dev)
+        t_g = [[] for _ in range(R)]
+        t_r = [[] for _ in range(R)]
+
+        def call(r, phase):
+            ctxs[r].set_option("g5_phases", phase)
+            rf.rf_gram(X, Ws[r], act=cfg.act, prec=args.prec, out="packed_tiles", m_total=m, G=recv, ws=ws,
+                       ctx=ctxs[r])
+
+        for rep in range(args.reps + 1):   # the first epoch is a warm-up
+            for phase, acc in ((1, t_g), (2, t_r)):
+                for r in range(R):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    call(r, phase)
+                    b.record()
+                    b.synchronize()
+                    if rep:
+                        acc[r].append(a.elapsed_time(b))
         ranks = []
         for r in range(R):
-            W = Wfull[r * m_local:(r + 1) * m_local]
             rb, re_ = rf.rf_phi_row_split(n, R, r)
-            t_g = timed(lambda: rf.rf_gram_packed_p2p(X, W, plan, r, ptrs, act=cfg.act, prec=args.prec, m_total=m,
-                                                      ws=ws))
-            t_r = timed(lambda: rf.rf_pack_reduce(plan, staging[r], recv)) if R > 1 else 0.0
-            t_p = timed(lambda: rf.rf_phi_closed_form(X, act=cfg.act, tau=0.0, prec=args.prec, out="upper",
-                                                      row_begin=rb, row_end=re_, Phi=Phi, ws=ws_p))
-            ranks.append({"rank": r, "gram_ms": t_g, "reduce_ms": t_r, "phi_ms": t_p, "step_ms": t_g + t_r + t_p})
+            tp = timed(lambda: rf.rf_phi_closed_form(X, act=cfg.act, tau=0.0, prec=args.prec, out="upper",
+                                                     row_begin=rb, row_end=re_, Phi=Phi, ws=ws_p))
+            g, red = min(t_g[r]), (min(t_r[r]) if R > 1 else 0.0)
+            ranks.append({"rank": r, "gram_ms": g, "reduce_ms": red, "phi_ms": tp, "step_ms": g + red + tp})
         step = max(x["step_ms"] for x in ranks)
-        # bytes each rank would store into peers: the tiles it does not own, (R-1)/R of its partial triangle
-        send_gb = (R - 1) * plan.recv_elems * 4 / 1e9
+        # bytes each rank stores into peers: the tiles it does not own, (R-1)/R of its partial triangle
+        send_gb = (R - 1) * slots * 65536 * 4 / 1e9
         row = {"R": R, "predicted_step_ms": step, "predicted_tflops": flops / (step * 1e-3) / 1e12,
                "gram_ms_max": max(x["gram_ms"] for x in ranks), "reduce_ms_max": max(x["reduce_ms"] for x in ranks),
                "phi_ms_max": max(x["phi_ms"] for x in ranks), "nvlink_send_gb_per_rank": send_gb,
                "nvlink_gbs_needed": send_gb / (max(x["gram_ms"] for x in ranks) * 1e-3), "ranks": ranks}
         out.append(row)
         print(json.dumps({k: v for k, v in row.items() if k != "ranks"}), flush=True)
-        del staging, recv, ws
+        for c in ctxs:
+            c.destroy()
+        del recv, ws
         torch.cuda.empty_cache()
     base = out[0]["predicted_step_ms"] if out and out[0]["R"] == 1 else None
     if base:
