@@ -68,6 +68,16 @@ typedef enum {
   RF_ACT_RELU = 3, RF_ACT_ABS = 4, RF_ACT_SIGN = 5, RF_ACT_STEP = 6, RF_ACT_COS = 7, RF_ACT_SIN = 8,
   RF_ACT_IDENT = 9, RF_ACT_QUAD = 10, RF_ACT_BUMP = 11
 } rf_act;
+/* Table 2's two parametrised rows, registered at run time; the returned id is a valid rf_act for every
+ * call (G through K3's runtime σ, moments through Stein as for the other Table-2 rows, Φ, TRF thresholds):
+ *   rf_act_leaky_relu: σ(t) = a₊·max(0, t) + a₋·max(0, −t)   (ReLU: 1, 0;  |t|: 1, 1;  leaky ReLU slope s: 1, −s)
+ *   rf_act_quadratic:  σ(t) = a₂t² + a₁t + a₀
+ * Ids are RF_ACT_PARAM_BASE + k, process-wide and immutable; the same coefficients return the same id; at most
+ * RF_ACT_PARAM_MAX registrations (then RF_E_INVALID).  Non-finite coefficients → RF_E_INVALID. */
+#define RF_ACT_PARAM_BASE 64
+#define RF_ACT_PARAM_MAX 64
+rf_status rf_act_leaky_relu(double a_plus, double a_minus, rf_act* act);
+rf_status rf_act_quadratic(double a0, double a1, double a2, rf_act* act);
 typedef enum { RF_DT_F64 = 0, RF_DT_F32 = 1, RF_DT_BF16 = 2 } rf_dtype;
 typedef enum { RF_PREC_FP64 = 0, RF_PREC_FP32 = 1, RF_PREC_3XTF32 = 2, RF_PREC_TF32 = 3, RF_PREC_BF16 = 4 } rf_prec;
 /* UPPER: write only entries j >= i (the rest of the buffer is untouched).

@@ -4,6 +4,8 @@
 TEST INFRASTRUCTURE ONLY (same rule as oracle/rf_oracle.py).
 
   TABLE2 ............................. relu, abs, sign, step (1_{t>0}), cos, sin, ident (t), quad (t²), bump (e^{−t²/2})
+  parametrised rows .... "leaky_relu(a₊,a₋)" = a₊·max(0,t) + a₋·max(0,−t),
+                                       "quadratic(a₀,a₁,a₂)" = a₂t² + a₁t + a₀ (the library's activation names)
   sigma2(act, t) ..................... the activation, written literally
   moments_stein(act, τ) .............. ⟨k,d⟩ = E[(√τξ)^k σ^{(d)}(√τξ)], k ≤ 4, d ≤ 2, from M_j = E[ξ^j σ(√τξ)] only:
                                          ⟨k,0⟩ = τ^{k/2} M_k
@@ -25,8 +27,25 @@ TABLE2 = ("relu", "abs", "sign", "step", "cos", "sin", "ident", "quad", "bump")
 ODD = ("sign", "sin", "ident")          # σ(−t) = −σ(t): ⟨k,d⟩ = 0 for k + d even
 
 
+def parse_param_act(act: str):
+    """("leaky_relu", (a₊, a₋)) or ("quadratic", (a₀, a₁, a₂)) for a parametrised Table-2 name, else None."""
+    for kind, k in (("leaky_relu", 2), ("quadratic", 3)):
+        if act.startswith(kind + "(") and act.endswith(")"):
+            vals = tuple(float(v) for v in act[len(kind) + 1:-1].split(","))
+            if len(vals) == k:
+                return kind, vals
+    return None
+
+
 def sigma2(act: str, t):
     t = np.asarray(t, dtype=np.float64)
+    pa = parse_param_act(act)
+    if pa is not None and pa[0] == "leaky_relu":        # Table 2, P:1115
+        ap, am = pa[1]
+        return ap * np.maximum(t, 0.0) + am * np.maximum(-t, 0.0)
+    if pa is not None:                                  # Table 2, P:1119
+        a0, a1, a2 = pa[1]
+        return a2 * t * t + a1 * t + a0
     if act == "relu":
         return np.maximum(t, 0.0)
     if act == "abs":

@@ -51,9 +51,16 @@ _TABLE2 = ("relu", "abs", "sign", "step", "cos", "sin", "ident", "quad", "bump")
 # --------------------------------------------------------------------------------------------
 # Activations (north star: σ ∈ {tanh, erf, sigmoid − 1/2}); written literally.
 # --------------------------------------------------------------------------------------------
+def _is_table2(act) -> bool:
+    if not isinstance(act, str):
+        return False
+    from .acts import parse_param_act
+    return act in _TABLE2 or parse_param_act(act) is not None
+
+
 def sigma(act: str, x):
     x = np.asarray(x, dtype=np.float64)
-    if act in _TABLE2:                      # NEXT-3 activations (oracle/acts.py)
+    if _is_table2(act):                     # NEXT-3 activations (oracle/acts.py)
         from .acts import sigma2
         return sigma2(act, x)
     if act == "tanh":
@@ -161,7 +168,7 @@ def gauss_expect(f: Callable, N: int = 128) -> float:
 def moments(act, tau: float, N: int = 200) -> Dict[str, object]:
     if not (tau > 0.0):
         raise ValueError("tau must be > 0")
-    if isinstance(act, str) and act in _TABLE2:   # weak derivatives through Stein (oracle/acts.py)
+    if _is_table2(act):                           # weak derivatives through Stein (oracle/acts.py)
         from .acts import moments_stein
         return moments_stein(act, tau)
     s0, s1, s2 = derivs(act)

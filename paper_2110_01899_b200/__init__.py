@@ -19,7 +19,8 @@ __all__ = ["Context", "rf_moments", "rf_estimate_tau", "rf_gram", "rf_phi_closed
            "rf_gram_workspace_size", "rf_phi_workspace_size", "rf_workspace_size", "rf_version", "rf_device_supported",
            "rf_last_launch_count", "rf_tile_map", "rf_trf_thresholds", "rf_trf_thresholds_for", "rf_ter_features",
            "rf_gram_ter", "rf_gram_ter_workspace_size", "rf_ktilde", "rf_ktilde_workspace_size", "rf_packed_tri_elems",
-           "rf_ridge", "rf_ridge_workspace_size", "rf_round_bf16", "rf_nccl_get_unique_id", "RFError", "PREC", "ACT",
+           "rf_ridge", "rf_ridge_workspace_size", "rf_round_bf16", "rf_nccl_get_unique_id", "rf_act_leaky_relu",
+           "rf_act_quadratic", "RFError", "PREC", "ACT",
            "OPT"]
 
 
@@ -148,6 +149,25 @@ class Context:
         r, w, m = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _lib.check(load().rf_ctx_collective(self._handle(), ctypes.byref(r), ctypes.byref(w), ctypes.byref(m)))
         return r.value, w.value, m.value
+
+
+def rf_act_leaky_relu(a_plus: float, a_minus: float) -> str:
+    """Register Table 2's a₊·max(0, t) + a₋·max(0, −t) (include/rf.h) and return its activation name
+    "leaky_relu(a₊,a₋)", usable as `act=` everywhere (the oracle reads the same name)."""
+    v = ctypes.c_int()
+    _lib.check(load().rf_act_leaky_relu(float(a_plus), float(a_minus), ctypes.byref(v)))
+    name = f"leaky_relu({float(a_plus)!r},{float(a_minus)!r})"
+    ACT[name] = v.value
+    return name
+
+
+def rf_act_quadratic(a0: float, a1: float, a2: float) -> str:
+    """Register Table 2's a₂t² + a₁t + a₀ (include/rf.h) and return its name "quadratic(a₀,a₁,a₂)"."""
+    v = ctypes.c_int()
+    _lib.check(load().rf_act_quadratic(float(a0), float(a1), float(a2), ctypes.byref(v)))
+    name = f"quadratic({float(a0)!r},{float(a1)!r},{float(a2)!r})"
+    ACT[name] = v.value
+    return name
 
 
 def rf_nccl_get_unique_id() -> bytes:

@@ -32,7 +32,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_ridge", "rf_round_bf16", "rf_ctx_create", "rf_ctx_destroy", "rf_ctx_set_option", "rf_ctx_get_option",
            "rf_tile_map", "rf_nccl_get_unique_id", "rf_ctx_init_nccl", "rf_ctx_attach_nccl", "rf_ctx_attach_peers",
            "rf_ctx_peer_handle", "rf_ctx_open_peers", "rf_ctx_peer_base", "rf_ctx_connect_peers", "rf_ctx_collective",
-           "rf_workspace_size")
+           "rf_workspace_size", "rf_act_leaky_relu", "rf_act_quadratic")
 
 RF_PACK_TILE = 256
 RF_MAX_PEERS = 16
@@ -114,6 +114,8 @@ def load() -> ctypes.CDLL:
     lib.rf_ctx_connect_peers.argtypes = [vp, ctypes.POINTER(vp)]
     lib.rf_ctx_collective.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.rf_workspace_size.argtypes = [vp, i32, i64, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(sz)]
+    lib.rf_act_leaky_relu.argtypes = [dbl, dbl, ctypes.POINTER(ctypes.c_int)]
+    lib.rf_act_quadratic.argtypes = [dbl, dbl, dbl, ctypes.POINTER(ctypes.c_int)]
     for name in SYMBOLS:
         if name not in ("rf_last_error", "rf_version", "rf_device_supported", "rf_ctx_destroy", "rf_last_launch_count"):
             getattr(lib, name).restype = ctypes.c_int

@@ -79,6 +79,28 @@ rf_status rf_moments(rf_act act, double tau, int32_t nodes, rf_moments_t* out) {
   return ok();
 }
 
+rf_status rf_act_leaky_relu(double a_plus, double a_minus, rf_act* act) {
+  if (!act) return fail(RF_E_INVALID, "rf_act_leaky_relu: act is NULL");
+  if (!std::isfinite(a_plus) || !std::isfinite(a_minus))
+    return fail(RF_E_INVALID, "rf_act_leaky_relu: coefficients must be finite");
+  const double a[3] = {a_plus, a_minus, 0.0};
+  const int id = rfh::register_param_act(1, a);
+  if (id < 0) return fail(RF_E_INVALID, "rf_act_leaky_relu: more than %d parametrised activations", RF_ACT_PARAM_MAX);
+  *act = (rf_act)id;
+  return ok();
+}
+
+rf_status rf_act_quadratic(double a0, double a1, double a2, rf_act* act) {
+  if (!act) return fail(RF_E_INVALID, "rf_act_quadratic: act is NULL");
+  if (!std::isfinite(a0) || !std::isfinite(a1) || !std::isfinite(a2))
+    return fail(RF_E_INVALID, "rf_act_quadratic: coefficients must be finite");
+  const double a[3] = {a0, a1, a2};
+  const int id = rfh::register_param_act(2, a);
+  if (id < 0) return fail(RF_E_INVALID, "rf_act_quadratic: more than %d parametrised activations", RF_ACT_PARAM_MAX);
+  *act = (rf_act)id;
+  return ok();
+}
+
 rf_status rf_tau_workspace_size(int64_t n, size_t* bytes) {
   if (!bytes) return fail(RF_E_INVALID, "bytes is NULL");
   if (n <= 0) return fail(RF_E_INVALID, "n must be > 0");
@@ -214,7 +236,7 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
   if (prec == RF_PREC_FP64 || prec == RF_PREC_FP32) {
     if (prec == RF_PREC_FP64) {
       double* S = (double*)(w + pl.off_s0);
-      rfk::SimtSigma<double> e1{S, pl.ldS, n, m_local, (int)act};
+      rfk::SimtSigma<double> e1{S, pl.ldS, n, m_local, (int)act, act_rt(act)};
       if ((s = launch_simt<double>("K6_simt_gemm_sigma", (const double*)X, ldx, (const double*)W, ldw, n, m_local, p, 0, 0,
                                    (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e1, st)))
         return s;
@@ -223,7 +245,7 @@ static rf_status rf_gram_core(const void* X, int64_t ldx, const void* W, int64_t
         return s;
     } else {
       float* S = (float*)(w + pl.off_s0);
-      rfk::SimtSigma<float> e1{S, pl.ldS, n, m_local, (int)act};
+      rfk::SimtSigma<float> e1{S, pl.ldS, n, m_local, (int)act, act_rt(act)};
       if ((s = launch_simt<float>("K6_simt_gemm_sigma", (const float*)X, ldx, (const float*)W, ldw, n, m_local, p, 0, 0,
                                   (int)((n + rfk::kSimtTile - 1) / rfk::kSimtTile), e1, st)))
         return s;

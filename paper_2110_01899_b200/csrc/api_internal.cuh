@@ -51,6 +51,9 @@ struct rf_ctx {
 
 namespace rfh {
 int compute_moments(rf_act act, double tau, int nodes, rf_moments_t* out);
+// parametrised Table-2 activations (moments.cpp): id ≥ RF_ACT_PARAM_BASE → kind 1 (leaky ReLU) / 2 (quadratic)
+int register_param_act(int kind, const double a[3]);
+bool param_act(int id, int* kind, double a[3]);
 int solve_ternary_thresholds(double d1, double d2, double tau, int sign2, double* s_minus, double* s_plus,
                              double* resid);
 }
@@ -147,7 +150,24 @@ const char* prec_name(rf_prec p) {
   return "?";
 }
 bool valid_prec(int p) { return p >= RF_PREC_FP64 && p <= RF_PREC_BF16; }
-bool valid_act(int a) { return a >= RF_ACT_TANH && a <= RF_ACT_BUMP; }
+bool valid_act(int a) {
+  int kind;
+  double p[3];
+  return (a >= RF_ACT_TANH && a <= RF_ACT_BUMP) || rfh::param_act(a, &kind, p);
+}
+// device-side description of σ for the runtime-σ epilogues (kind 0: a fixed rf_act)
+rfk::ActRt act_rt(int a) {
+  rfk::ActRt r{0, 0.0, 0.0, 0.0};
+  double p[3];
+  int kind = 0;
+  if (rfh::param_act(a, &kind, p)) {
+    r.kind = kind;
+    r.a0 = p[0];
+    r.a1 = p[1];
+    r.a2 = p[2];
+  }
+  return r;
+}
 bool valid_out(int o) { return o >= RF_OUT_UPPER && o <= RF_OUT_PACKED_TILES; }
 int64_t tri_tiles(int64_t n) {
   const int64_t T = (n + 255) / 256;
@@ -729,13 +749,14 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
     return launch_tc<C3>("K3_gemm_sigma", tA, tB, tAl, tBl, tA, s3, e3, g.sms, g.st);
   };
   if (g.act == RF_ACT_TANH) {
-    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_TANH>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_TANH>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act, act_rt(g.act)});
   } else if (g.act == RF_ACT_ERF) {
-    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_ERF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_ERF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act, act_rt(g.act)});
   } else if (g.act == RF_ACT_SIGMOID_HALF) {
-    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
+    s = run_k3(rfk::EpiSigma<kOut, RF_ACT_SIGMOID_HALF>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act,
+                                                        act_rt(g.act)});
   } else {   // NEXT-3 Table-2 activations: one instantiation, σ chosen at run time
-    s = run_k3(rfk::EpiSigma<kOut, -1>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act});
+    s = run_k3(rfk::EpiSigma<kOut, -1>{S0, S1, g.pl.ldS, g.n, g.m_local, (int)g.act, act_rt(g.act)});
   }
   if (s) return s;
 

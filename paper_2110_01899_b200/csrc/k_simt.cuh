@@ -15,8 +15,9 @@ struct SimtSigma {
   T* S;
   int64_t ld, M, N;
   int act;
+  ActRt ap;   // parametrised σ (ap.kind > 0) instead of act
   __device__ __forceinline__ void operator()(int64_t i, int64_t j, T v) const {
-    if (i < M && j < N) S[i * ld + j] = act_t<T>(act, v);
+    if (i < M && j < N) S[i * ld + j] = ap.kind ? act_param<T>(ap, v) : act_t<T>(act, v);
   }
 };
 

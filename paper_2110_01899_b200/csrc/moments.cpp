@@ -186,8 +186,40 @@ static void fill(const double table[16], double tau, rf_moments_t* out) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Parametrised Table-2 rows, registered at run time: ids RF_ACT_PARAM_BASE + k.  Entries are
+// immutable once registered; the same coefficients give the same id.
+struct ParamAct {
+  int kind;        // 1: a₊max(0,t) + a₋max(0,−t) (a[0] = a₊, a[1] = a₋); 2: a₂t² + a₁t + a₀ (a[0..2] = a₀, a₁, a₂)
+  double a[3];
+};
+static std::mutex g_param_mu;
+static ParamAct g_param[RF_ACT_PARAM_MAX];
+static int g_nparam = 0;
+
+int register_param_act(int kind, const double a[3]) {
+  std::lock_guard<std::mutex> lk(g_param_mu);
+  for (int k = 0; k < g_nparam; ++k)
+    if (g_param[k].kind == kind && g_param[k].a[0] == a[0] && g_param[k].a[1] == a[1] && g_param[k].a[2] == a[2])
+      return RF_ACT_PARAM_BASE + k;
+  if (g_nparam >= RF_ACT_PARAM_MAX) return -1;
+  g_param[g_nparam] = ParamAct{kind, {a[0], a[1], a[2]}};
+  return RF_ACT_PARAM_BASE + g_nparam++;
+}
+bool param_act(int id, int* kind, double a[3]) {
+  const int k = id - RF_ACT_PARAM_BASE;
+  std::lock_guard<std::mutex> lk(g_param_mu);
+  if (k < 0 || k >= g_nparam) return false;
+  *kind = g_param[k].kind;
+  for (int i = 0; i < 3; ++i) a[i] = g_param[k].a[i];
+  return true;
+}
+
 // NEXT-3 (Table-2 activations, weak derivatives by Stein): σ only.
 static inline double act_value(rf_act act, double t) {
+  int kind;
+  double a[3];
+  if ((int)act >= RF_ACT_PARAM_BASE && rfh::param_act((int)act, &kind, a))
+    return kind == 1 ? a[0] * (t > 0.0 ? t : 0.0) + a[1] * (t < 0.0 ? -t : 0.0) : (a[2] * t + a[1]) * t + a[0];
   switch (act) {
     case RF_ACT_RELU: return t > 0.0 ? t : 0.0;
     case RF_ACT_ABS: return std::fabs(t);

@@ -46,6 +46,18 @@ __device__ __forceinline__ T act_table2(int act, T x) {
     default: return exp(T(-0.5) * x * x);   // RF_ACT_BUMP
   }
 }
+// Parametrised Table-2 rows, registered at run time (rf_act_leaky_relu / rf_act_quadratic):
+// kind 1: a₊·max(0, t) + a₋·max(0, −t) with (a0, a1) = (a₊, a₋);  kind 2: a₂t² + a₁t + a₀.  kind 0: a fixed rf_act.
+struct ActRt {
+  int kind;
+  double a0, a1, a2;
+};
+template <typename T>
+__device__ __forceinline__ T act_param(const ActRt& p, T x) {
+  if (p.kind == 1) return T(p.a0) * (x > T(0) ? x : T(0)) + T(p.a1) * (x < T(0) ? -x : T(0));
+  return fma(fma(T(p.a2), x, T(p.a1)), x, T(p.a0));
+}
+
 __device__ __forceinline__ float act_f32(int act, float x) {
   if (act == RF_ACT_TANH) return tanhf(x);
   if (act == RF_ACT_ERF) return erff(x);

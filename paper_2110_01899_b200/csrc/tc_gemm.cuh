@@ -383,6 +383,7 @@ struct EpiSigma {
   int64_t ld;       // elements
   int64_t M, N;     // n rows (samples), m_local columns (features)
   int act;          // used when kAct < 0
+  ActRt ap;         // kAct < 0 and ap.kind > 0: a parametrised Table-2 σ (leaky ReLU, quadratic)
   __device__ __forceinline__ bool chunk_needed(int64_t row_lo, int64_t col0) const { return col0 < N && row_lo < M; }
   __device__ __forceinline__ void tile_done(int, uint32_t) const {}
   struct Pre {};
@@ -396,7 +397,7 @@ struct EpiSigma {
     float s[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e)
-      s[e] = kAct < 0 ? act_f32(act, __uint_as_float(r[e]))
+      s[e] = kAct < 0 ? (ap.kind ? act_param<float>(ap, __uint_as_float(r[e])) : act_f32(act, __uint_as_float(r[e])))
                       : (kOut == 0 ? act_bf16out<kAct>(__uint_as_float(r[e])) : act_fixed<kAct>(__uint_as_float(r[e])));
     const bool full = col0 + 32 <= N;
     if (kOut == 0) {

@@ -65,11 +65,18 @@ def gram_bound(prec: str, act: str, Xs: np.ndarray, W: np.ndarray, Gref: np.ndar
     xn = np.sqrt(np.sum(np.asarray(Xs, float) ** 2, axis=1))
     dz = (2 * U_OPERAND[prec] + acc_rel(prec, p)) * xn * wmax
     extra = 0.0
-    if act in ("quad", "sign", "step"):
+    from oracle.acts import parse_param_act
+    pa = parse_param_act(act) if isinstance(act, str) else None
+    quad = (0.0, 0.0, 1.0) if act == "quad" else (pa[1] if pa and pa[0] == "quadratic" else None)
+    if quad is not None or act in ("sign", "step"):
         Z = np.asarray(Xs, float) @ np.asarray(W, float).T            # |S| × m, fp64
-    if act == "quad":        # σ' = 2t is not bounded: the local Lipschitz constant on each row's range of z
-        L = 2.0 * (np.max(np.abs(Z), axis=1) + dz)
-        e = L * dz + E_EVAL[prec] * (1.0 + np.max(Z * Z, axis=1))
+    if quad is not None:     # σ' = 2a₂t + a₁ is not bounded: the local Lipschitz constant on each row's range of z
+        a0, a1, a2 = quad
+        zmax = np.max(np.abs(Z), axis=1) + dz
+        L = 2.0 * abs(a2) * zmax + abs(a1)
+        e = L * dz + E_EVAL[prec] * (1.0 + abs(a2) * zmax * zmax + abs(a1) * zmax + abs(a0))
+    elif pa is not None:     # leaky ReLU: Lipschitz max(|a₊|, |a₋|)
+        e = max(abs(pa[1][0]), abs(pa[1][1])) * dz + E_EVAL[prec] * max(1.0, abs(pa[1][0]), abs(pa[1][1]))
     else:
         e = LIP.get(act, 1.0) * dz + E_EVAL[prec]
     bound = rel * d[I] * d[J] + e[I] * d[J] + e[J] * d[I] + e[I] * e[J]

@@ -286,3 +286,39 @@ def test_round_bf16_validation():
     assert s == _lib.RF_E_INVALID and b"leading" in lib.rf_last_error()
     s = lib.rf_round_bf16(None, vp(a + 2), 8, 2, 8, vp(a), 8, None)
     assert s == _lib.RF_E_INVALID and b"aligned" in lib.rf_last_error()
+
+
+# ------------------------------------------------------------------------------------------ parametrised Table-2 σ
+@pytest.mark.parametrize("spec", [("leaky", 1.0, -0.2), ("leaky", 0.5, 2.0), ("quad", 0.4, -1.3, 0.7),
+                                  ("quad", -1.0, 0.0, 2.0)])
+@pytest.mark.parametrize("tau", [0.5, 1.0833, 2.0])
+def test_param_act_moments_match_oracle_and_table2(spec, tau):
+    """rf_act_leaky_relu / rf_act_quadratic (include/rf.h): the library's Stein-form moments of the registered σ
+    equal the oracle's and Table 2's closed forms."""
+    if spec[0] == "leaky":
+        name = rf.rf_act_leaky_relu(spec[1], spec[2])
+        ap, am = spec[1], spec[2]
+        want = (tau * (ap + am) ** 2 * (math.pi - 2) / (4 * math.pi), (ap - am) ** 2 / 4,
+                (ap + am) ** 2 / (8 * math.pi * tau))
+    else:
+        name = rf.rf_act_quadratic(*spec[1:])
+        a0, a1, a2 = spec[1:]
+        want = (2 * tau ** 2 * a2 ** 2, a1 ** 2, a2 ** 2)
+    got = rf.rf_moments(name, tau)
+    ref = oracle.moments(name, tau)
+    assert np.max(np.abs(np.array(got["kd"]) - ref["kd"])) < 1e-11 * max(1.0, np.max(np.abs(ref["kd"])))
+    for k, w in zip(("d0", "d1", "d2"), want):
+        assert abs(got[k] - w) < 1e-11 * max(1.0, abs(w)), (k, got[k], w)
+
+
+def test_param_act_registration():
+    a = rf.rf_act_leaky_relu(1.0, -0.1)
+    b = rf.rf_act_leaky_relu(1.0, -0.1)
+    assert a == b and rf.ACT[a] == rf.ACT[b] >= 64
+    assert rf.ACT[rf.rf_act_quadratic(0.0, 0.0, 1.0)] != rf.ACT[a]
+    lib = rf.load()
+    v = ctypes.c_int()
+    assert lib.rf_act_leaky_relu(float("nan"), 0.0, ctypes.byref(v)) == _lib.RF_E_INVALID
+    assert lib.rf_act_quadratic(0.0, float("inf"), 0.0, ctypes.byref(v)) == _lib.RF_E_INVALID
+    m = ctypes.c_int()
+    assert lib.rf_moments(200, 1.0, 0, None) == _lib.RF_E_INVALID      # an id never registered

@@ -115,3 +115,49 @@ def test_phi_eq2_config4_full_size_sampled():
     print(f"[parity] Φ EQ2 configs[4] sampled |S|={len(S)}: rel-Frobenius {e:.3e}")
     assert e <= 1e-5
     check("Phi EQ2 configs[4]", sub[I, J], ref[I, J], phi_bound("bf16", cfg.act, Xb[S], tau, I, J, form=2))
+
+
+# ------------------------------------------------------------------------------------------ Table 2's parametrised rows
+def _param_acts():
+    return [rf.rf_act_leaky_relu(1.0, -0.2), rf.rf_act_leaky_relu(0.5, 2.0), rf.rf_act_quadratic(0.4, -1.3, 0.7)]
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+@pytest.mark.parametrize("prec", ["bf16", "3xtf32", "fp32"])
+def test_gram_param_acts(k, prec):
+    """G for Table 2's a₊max(0,t) + a₋max(0,−t) and a₂t² + a₁t + a₀ through K3's runtime σ (tensor
+    core) and the SIMT K6, against the oracle's σ written literally; per-entry bounds."""
+    act = _param_acts()[k]
+    n, p, m = 300, 72, 400
+    rng = np.random.default_rng(17 + k)
+    Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(DT[prec])
+    Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(DT[prec])
+    G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper")
+    torch.cuda.synchronize()
+    Xo, Wo = Xd.double().cpu().numpy(), Wd.double().cpu().numpy()
+    ref = oracle.gram(Xo, Wo, act)
+    I, J = np.triu_indices(n)
+    Gc = G.double().cpu().numpy()
+    e = _rel(Gc[I, J], ref[I, J])
+    print(f"[parity] G {act} {prec}: rel-Frobenius {e:.3e}")
+    assert e <= (2e-3 if prec == "bf16" else 1e-5)
+    check(f"G {act} {prec}", Gc[I, J], ref[I, J], gram_bound(prec, act, Xo, Wo, ref, I, J))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+@pytest.mark.parametrize("form", [1, 2])
+def test_phi_param_acts(k, form):
+    act = _param_acts()[k]
+    n, p = 520, 96
+    X = synthetic.make_X(4, n=n, p=p)
+    Xd = torch.tensor(X, device="cuda").to(torch.bfloat16)
+    Xb = Xd.double().cpu().numpy()
+    Phi = rf.rf_phi_closed_form(Xd, act=act, tau=0.0, prec="bf16", out="upper", form=form)
+    torch.cuda.synchronize()
+    ref = (oracle.phi_eq1 if form == 1 else oracle.phi_eq2)(Xb, act)
+    I, J = np.triu_indices(n)
+    Pc = Phi.double().cpu().numpy()
+    e = _rel(Pc[I, J], ref[I, J])
+    print(f"[parity] Φ EQ{form} {act} bf16: rel-Frobenius {e:.3e}")
+    assert e <= 1e-5
+    check(f"Phi EQ{form} {act}", Pc[I, J], ref[I, J], phi_bound("bf16", act, Xb, oracle.tau_hat(Xb), I, J, form=form))

@@ -29,6 +29,7 @@ def _golden_rows():
 
 
 A2, A1, A0 = 0.7, -1.3, 0.4
+AP, AM = 1.0, -0.2          # leaky ReLU of slope 0.2 in Table 2's a₊·max(0,t) + a₋·max(0,−t) form
 TEST_ACTS = {
     "cos": (np.cos, lambda x: -np.sin(x), lambda x: -np.cos(x)),
     "sin": (np.sin, np.cos, lambda x: -np.sin(x)),
@@ -82,11 +83,15 @@ def test_paper_printed_gaussian_moments(tau):
     """Table 2 and the draft tables — values printed in the paper."""
     rows = _golden_rows()
     assert len(rows) >= 25
-    env = {"exp": math.exp, "sqrt": math.sqrt, "pi": math.pi, "tau": tau, "a0": A0, "a1": A1, "a2": A2}
+    env = {"exp": math.exp, "sqrt": math.sqrt, "pi": math.pi, "tau": tau, "a0": A0, "a1": A1, "a2": A2, "ap": AP,
+           "am": AM}
     for act, q, expr, cite in rows:
         # analytic derivatives by Gauss–Hermite where the golden row's σ is defined locally; the Table-2
-        # activations with kinks/jumps (|t|, ReLU, sign, 1_{t>0}) go through the oracle's Stein-form moments
-        mom = oracle.moments(TEST_ACTS[act], tau, N=128) if act in TEST_ACTS else oracle.moments(act, tau)
+        # activations with kinks/jumps (|t|, ReLU, sign, 1_{t>0}, leaky) go through the oracle's Stein-form moments
+        if act == "leaky":
+            mom = oracle.moments(f"leaky_relu({AP!r},{AM!r})", tau)
+        else:
+            mom = oracle.moments(TEST_ACTS[act], tau, N=128) if act in TEST_ACTS else oracle.moments(act, tau)
         kd = mom["kd"]
         got = {"d0": mom["d0"], "d1": mom["d1"], "d2": mom["d2"], "E_s": kd[0, 0], "E_s1": kd[0, 1],
                "E_s2": kd[0, 2], "E_sq": mom["e_sigma_sq"]}[q]
@@ -160,3 +165,30 @@ def test_tau_hat_lemma1():
     rng = np.random.default_rng(3)
     Xs = rng.standard_normal((4096, 4096)) / 64.0
     assert abs(oracle.tau_hat(Xs) - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("tau", [0.3, 1.0, 2.5])
+def test_parametrised_quadratic_rows_through_stein(tau):
+    """The oracle's parametrised "quadratic(a0,a1,a2)" (Stein-form moments from σ alone) against the same printed
+    Table-2 / draft rows the analytic-derivative quad above meets."""
+    env = {"exp": math.exp, "sqrt": math.sqrt, "pi": math.pi, "tau": tau, "a0": A0, "a1": A1, "a2": A2}
+    mom = oracle.moments(f"quadratic({A0!r},{A1!r},{A2!r})", tau)
+    kd = mom["kd"]
+    n = 0
+    for act, q, expr, cite in _golden_rows():
+        if act != "quad":
+            continue
+        got = {"d0": mom["d0"], "d1": mom["d1"], "d2": mom["d2"], "E_s": kd[0, 0], "E_s1": kd[0, 1],
+               "E_s2": kd[0, 2], "E_sq": mom["e_sigma_sq"]}[q]
+        want = eval(expr, {"__builtins__": {}}, env)
+        assert abs(got - want) < 1e-11 * max(1.0, abs(want)), (q, cite, got, want)
+        n += 1
+    assert n == 7
+
+
+def test_parametrised_leaky_reduces_to_relu_and_abs():
+    """Table 2's leaky row at (a₊, a₋) = (1, 0) is the ReLU row and at (1, 1) the |t| row."""
+    for tau in (0.5, 1.7):
+        for name, ref in (("leaky_relu(1.0,0.0)", "relu"), ("leaky_relu(1.0,1.0)", "abs")):
+            a, b = oracle.moments(name, tau), oracle.moments(ref, tau)
+            assert np.max(np.abs(a["kd"] - b["kd"])) < 1e-13 and abs(a["d0"] - b["d0"]) < 1e-13
