@@ -153,7 +153,9 @@ typedef enum {
                               arrival flags, 2: the arrival waits + owner-side sum + release flags, 3: both (default).
                               Emulating R ranks on ONE GPU in one process: call phase 1 for every rank, then phase 2,
                               on one stream, so no stream-memory wait ever heads a queue its producer sits behind */
-  RF_OPT_COUNT = 14
+  RF_OPT_K4_DYNAMIC = 14,  /* 1: the K4 hybrid's two kernels pull 512 × 512 units of one raster from a shared device
+                              counter (no static split); 0: the static split of RF_OPT_K4_SPLIT_R100     default 1 */
+  RF_OPT_COUNT = 15
 } rf_opt;
 rf_status rf_ctx_set_option(rf_ctx* ctx, rf_opt opt, int64_t value);
 rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);

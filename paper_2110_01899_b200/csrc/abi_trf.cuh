@@ -13,7 +13,7 @@ TerPlan ter_plan(int64_t n, int64_t m_local) {
   t.ldS = odd_line_ld(std::max<int64_t>(m_local, 1), 1);
   size_t off = 0;
   t.off_s = off; off = align256(off + (size_t)n * t.ldS);
-  t.off_prog = off; off = align256(off + 1024);
+  t.off_prog = off; off = align256(off + 2048);   // lockstep words, start flag, unit queue
   t.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);
   t.total = off;
   return t;

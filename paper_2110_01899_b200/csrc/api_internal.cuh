@@ -272,7 +272,7 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
 }
 
 // ---------------------------------------------------------------- context and options (include/rf.h)
-constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3};
+constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1};
 thread_local rf_ctx* g_ctx = nullptr;     // the context of the call in progress on this thread
 int64_t opt(rf_opt o) { return g_ctx ? g_ctx->opts[o] : kOptDefault[o]; }
 
@@ -481,7 +481,7 @@ GramPlan gram_plan(int64_t p, int64_t n, int64_t m_local, rf_prec prec) {
     g.off_whi = off; off = align256(off + (size_t)m_local * g.ldp * 4);
     g.off_wlo = off; off = align256(off + (size_t)m_local * g.ldp * 4);
   }
-  g.off_prog = off; off = align256(off + 1024);      // K4 lockstep progress words (≤ 256 clusters)
+  g.off_prog = off; off = align256(off + 2048);      // K4 lockstep progress words, start flag, unit queue
   g.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);   // centering row sums + s (NEXT-2)
   g.total = off;
   return g;
@@ -629,13 +629,24 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
     ++S1;
   }
   if (2 * S1 >= T) return RF_OK;
-  RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 1024, st));
+  RF_CUDA_CHECK(cudaMemsetAsync(prog, 0, 2048, st));
   // multicast kernel: super rows of 512; CL 4 walks 512-wide column tiles, CL 8 1024-wide super columns
   rfk::Sched sm = kMcCl == 8 ? rfk::Sched::make(1, 512, 0, S1, (int)((n + 1023) / 1024), kb, 0, raster_gm(4, 4))
                              : rfk::Sched::make(1, 256, 0, S1, T2, kb, 0, raster_gm(4, 4));
   // tail raster: with 8 pair clusters in flight, groups of 4 row tiles × 2 column tiles re-read the fewest Σᵀ panels
   // (4·32 + 2·64 MB per 8 tiles vs 8·32 + 64 for groups of 8); measured ≈ 0.8 % on the whole K4 (scripts/gpu_tailgm.sh)
   rfk::Sched sp = rfk::Sched::make(1, 512, 2 * S1, T, T2, kb, 0, 4);
+  if (kMcCl == 4 && opt(RF_OPT_K4_DYNAMIC)) {
+    // Dynamic units (tc_gemm.cuh TileSeq): no static split — both kernels pull 512 × 512 units of ONE raster over the
+    // whole triangle from a shared counter (prog[256]); the multicast cluster computes a unit with its two pairs,
+    // a pair cluster as two 256 × 512 tiles.  The pair kernel's SMs follow the raster front (L2 reuse) and both
+    // kernels end together whatever their per-SM rates on this box.
+    sm = rfk::Sched::make(1, 256, 0, T2, T2, kb, 0, raster_gm(4, 4));
+    sp = sm;
+    sm.queue = sp.queue = prog + 256;
+    sp.nsub = 2;
+    sm.sub_rows = sp.sub_rows = T;
+  }
   if (lockw > 0) {
     sm.prog = prog;
     sp.prog = prog + 128;

@@ -70,6 +70,46 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Cluster-scope variants for the dynamic tile ring (tc_gemm.cuh TileSeq): a try_wait that acquires at cluster scope,
+// a release arrive on a (possibly remote) barrier, and a 32-bit store into a (possibly remote) CTA's shared memory.
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+#if defined(RF_DEBUG)
+  uint32_t spins = 0;
+  while (!mbar_try_wait_cluster(addr, parity)) {
+    if (++spins == (1u << 26)) {
+      printf("[rf debug] ring wait timeout: block %d thread %d smem 0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, addr, parity);
+      __trap();
+    }
+  }
+#else
+  while (!mbar_try_wait_cluster(addr, parity)) {
+  }
+#endif
+}
+__device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 // ---------------------------------------------------------------- global progress words (soft lockstep)
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

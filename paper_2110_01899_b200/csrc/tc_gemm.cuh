@@ -79,7 +79,7 @@ struct TcCfg {
                                    ? SMEM_MAX - STAGES * STAGE_BYTES - STG_BYTES - COL_BYTES - BAR_BYTES
                                    : 1024;
   static constexpr size_t SMEM_BYTES = (size_t)SLACK + (size_t)STAGES * STAGE_BYTES + STG_BYTES + COL_BYTES + BAR_BYTES;
-  static_assert(8 * (2 * STAGES + 6) + 4 <= BAR_BYTES, "barrier area");
+  static_assert(8 * (2 * STAGES + 6 + 2 * 4) + 4 + 4 * 4 <= BAR_BYTES, "barrier area");
   static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt == 3 ? 0u : (uint32_t)kFmt, 256, 256);
   static_assert(STAGES >= 2, "pipeline too shallow");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
@@ -130,6 +130,11 @@ struct Sched {
   // K5) and epilogue TMA stores (0 = normal, 1 = evict_first: a streamed output must not evict them).
   int load_pol, store_pol;
   uint32_t* started;    // non-null: the first CTA writes 1 here when the kernel starts (hybrid K4 launch order)
+  // Dynamic units (TileSeq): queue != nullptr → the cluster pulls work items ("units" = tiles of this schedule) from
+  // the counter *queue, shared with the other kernel of a hybrid launch; a 2-CTA-cluster kernel processes a unit as
+  // nsub row tiles (2I, 2I + 1; rows ≥ sub_rows skipped), a 4-CTA-cluster kernel as one row tile per pair (2I + pi).
+  uint32_t* queue;
+  int nsub, sub_rows;
 
   struct Group {
     int I0, I1, J0, Jf;
@@ -190,6 +195,9 @@ struct Sched {
     s.load_pol = 0;
     s.store_pol = 0;
     s.started = nullptr;
+    s.queue = nullptr;
+    s.nsub = 1;
+    s.sub_rows = 0;
     long long tot = 0;
     for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
     s.num_tiles = (int)tot;
@@ -235,6 +243,100 @@ struct TileCursor {
     const int rows = I1 - I0;
     tj = Jf + (int)(u / rows);
     ti = I0 + (int)(u % rows);
+  }
+};
+
+// Tile sequence of one warp role of a cluster (every role walks the same sequence).  Static: tiles t = cid, cid + ncl, …
+// of the schedule.  Dynamic (sched.queue): the cluster's fetcher — the producer warp of cluster rank 0 — takes the next
+// unit with an atomicAdd on the counter every cluster of the launch shares (both kernels of the K4 hybrid), writes it
+// into a kRing-deep ring in every CTA of the cluster (st.shared::cluster) and arrives (release, cluster scope) on
+// that CTA's ring_full; every other role waits there (acquire), reads the unit and arrives on the fetcher's
+// ring_empty, which the fetcher waits on before it reuses the slot.  A unit past the end is published as ~0u (stop).
+constexpr int kRing = 4;
+struct TileSeq {
+  const Sched* s;
+  TileCursor cur;
+  long long t;
+  int ncl, cl, pi;
+  bool dyn, fetcher;
+  uint32_t lane, ring_s, rfull_s, rempty_s, rempty_c;
+  int k, sub, nsub, ui, uj;
+  long long u;
+  __device__ __forceinline__ void init(const Sched* sp, int cid, int ncl_, int cl_, int pi_, bool fetcher_,
+                                       uint32_t lane_, uint32_t ring_s_, uint32_t rfull_s_, uint32_t rempty_s_,
+                                       uint32_t rempty_c_) {
+    s = sp;
+    cur.init(sp);
+    t = cid;
+    ncl = ncl_;
+    cl = cl_;
+    pi = pi_;
+    dyn = sp->queue != nullptr;
+    fetcher = fetcher_;
+    lane = lane_;
+    ring_s = ring_s_;
+    rfull_s = rfull_s_;
+    rempty_s = rempty_s_;
+    rempty_c = rempty_c_;
+    k = 0;
+    nsub = cl_ == 2 ? sp->nsub : 1;
+    sub = nsub;
+    ui = uj = 0;
+    u = 0;
+  }
+  __device__ __forceinline__ long long fetch() {
+    const int slot = k % kRing;
+    const uint32_t par = (uint32_t)(k / kRing) & 1u;
+    ++k;
+    uint32_t v = 0;
+    if (fetcher) {
+      if (lane == 0) {
+        ptx::mbar_wait_cluster(rempty_s + 8 * slot, par ^ 1u);
+        v = atomicAdd(s->queue, 1u);
+        if (v >= (uint32_t)s->num_tiles) v = 0xFFFFFFFFu;
+        for (int r = 0; r < cl; ++r) {
+          ptx::st_shared_cluster_u32(ptx::mapa(ring_s + 4 * slot, (uint32_t)r), v);
+          ptx::mbar_arrive_release_cluster(ptx::mapa(rfull_s + 8 * slot, (uint32_t)r));
+        }
+      }
+      v = __shfl_sync(0xFFFFFFFFu, v, 0);
+    } else {
+      ptx::mbar_wait_cluster(rfull_s + 8 * slot, par);
+      v = ptx::ld_shared_u32(ring_s + 4 * slot);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_release_cluster(rempty_c + 8 * slot);
+    }
+    return v == 0xFFFFFFFFu ? -1 : (long long)v;
+  }
+  // next tile of this role: (schedule index / unit, row tile, column tile) with the cluster's CTA placement applied
+  __device__ __forceinline__ bool next(long long& tt, int& ti, int& tj) {
+    if (!dyn) {
+      if (t >= s->num_tiles) return false;
+      cur.get(t, ti, tj);
+      tt = t;
+      t += ncl;
+      if (cl == 4) ti = 2 * ti + pi;       // 4-CTA clusters walk 512-row super tiles
+      if (cl == 8) {                       // … 8-CTA clusters also 1024-column super tiles
+        ti = 2 * ti + (pi & 1);
+        tj = 2 * tj + (pi >> 1);
+      }
+      return true;
+    }
+    for (;;) {
+      if (sub >= nsub) {
+        u = fetch();
+        if (u < 0) return false;
+        cur.get(u, ui, uj);
+        sub = 0;
+      }
+      const int row = 2 * ui + (cl == 4 ? pi : sub);
+      ++sub;
+      if (cl == 2 && row >= s->sub_rows) continue;   // the odd last super row has one row tile
+      tt = u;
+      ti = row;
+      tj = uj;
+      return true;
+    }
   }
 };
 
@@ -830,7 +932,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* colfull = tempty + 2;
   uint64_t* colempty = colfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colempty + 2);
+  uint64_t* rfull = colempty + 2;       // dynamic-unit ring (TileSeq)
+  uint64_t* rempty = rfull + kRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + kRing);
+  uint32_t* ring = tmem_slot + 1;
   constexpr bool kCol = ColVecOf<Epi>::value;
   static_assert(!kCol || (Cfg::COL_BYTES > 0 && Cfg::CL == 2), "column vectors: 256-wide pair tiles, clusters of 2");
 
@@ -862,6 +967,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       ptx::mbar_init(&colfull[a], 1);
       ptx::mbar_init(&colempty[a], Cfg::EPI_WARPS);
     }
+    // ring consumers per cluster: the other CTAs' producers, one MMA warp per pair, every epilogue warp
+    for (int a = 0; a < kRing; ++a) {
+      ptx::mbar_init(&rfull[a], 1);
+      ptx::mbar_init(&rempty[a], (Cfg::CL - 1) + Cfg::CL / 2 + Cfg::CL * Cfg::EPI_WARPS);
+    }
     ptx::fence_mbarrier_init();
   }
   if (sched.started && blockIdx.x == 0 && threadIdx.x == 0) ptx::st_relaxed_gpu(sched.started, 1u);
@@ -879,6 +989,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 #endif
   const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
+  const uint32_t ring_s = ptx::smem_u32(ring), rfull_s = ptx::smem_u32(&rfull[0]), rempty_s = ptx::smem_u32(&rempty[0]);
+  const uint32_t rempty_c = ptx::mapa(rempty_s, 0);   // the fetcher's (cluster rank 0) ring_empty
+  auto make_seq = [&](bool fetcher) {
+    TileSeq q;
+    q.init(&sched, cid, ncl, Cfg::CL, (int)pi, fetcher, lane, ring_s, rfull_s, rempty_s, rempty_c);
+    return q;
+  };
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs; completion bytes land on the leader's full barrier) =====
@@ -898,16 +1015,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     uint32_t step = 0;
-    TileCursor cur;
-    cur.init(&sched);
-    for (int t = cid; t < sched.num_tiles; t += ncl) {
-      int ti, tj;
-      cur.get(t, ti, tj);
-      if (Cfg::CL == 4) ti = 2 * ti + (int)pi;       // the scheduler walks 512-row super tiles
-      if (Cfg::CL == 8) {                            // … and 1024-column super tiles
-        ti = 2 * ti + (int)di;
-        tj = 2 * tj + (int)dj;
-      }
+    TileSeq seq = make_seq(crank == 0);
+    long long t;
+    int ti, tj;
+    while (seq.next(t, ti, tj)) {
       const int ra = ti * Cfg::BM + (int)rank * 128;
       const int rb = tj * Cfg::BN + (int)rank * 128;
       for (int c = 0; c < nchunks; ++c) {
@@ -989,7 +1100,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         const uint32_t pa = di + 2 * (1 - dj), pb = (1 - di) + 2 * dj;
         empty_mask = (uint16_t)((0x3u << (2 * pi)) | (0x3u << (2 * pa)) | (0x3u << (2 * pb)));
       }
-      for (int t = cid; t < sched.num_tiles; t += ncl) {
+      TileSeq seq = make_seq(false);
+      long long t;
+      int ti, tj;
+      while (seq.next(t, ti, tj)) {
         for (int c = 0; c < nchunks; ++c, ++it) {
           // K-chunked accumulation: every chunk goes to slot 0; the epilogue keeps the running fp32 sum in slot 1
           const bool dbl = Cfg::ACC_SLOTS == 2 && nchunks == 1;
@@ -1047,7 +1161,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       TileCursor cur;
       cur.init(&sched);
       int tcount = 0;
-      for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {
+      for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {   // static schedules only (kColVec, host-checked)
         int ti, tj;
         cur.get(t, ti, tj);
         if (lane == 0) {
@@ -1077,17 +1191,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), leader);
     constexpr int HALF = Cfg::ACC_COLS / 2;
     int it = 0;
-    TileCursor cur;
-    cur.init(&sched);
     int tcount = 0;
-    for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {
-      int ti, tj;
-      cur.get(t, ti, tj);
-      if (Cfg::CL == 4) ti = 2 * ti + (int)pi;
-      if (Cfg::CL == 8) {
-        ti = 2 * ti + (int)(pi & 1u);
-        tj = 2 * tj + (int)(pi >> 1);
-      }
+    TileSeq seq = make_seq(false);
+    long long t;
+    int ti, tj;
+    for (; seq.next(t, ti, tj); ++tcount) {
       if constexpr (kCol) {   // the tile's column vector (bulk-copied by this CTA's producer when the tile started)
         ptx::mbar_wait(&colfull[tcount & 1], (tcount >> 1) & 1);
         cx.col_s = ptx::smem_u32(sCol + (tcount & 1) * Cfg::BN);

@@ -365,17 +365,19 @@ def test_k3_multicast_hybrid_bit_exact(act, prec):
     check(f"G K3-multicast {act} {prec}", sub[I, J], ref[I, J], gram_bound(prec, act, Xs, back(Wd), ref, I, J))
 
 
-@pytest.mark.parametrize("cl8,out", [("0", "upper"), ("1", "upper"), ("0", "full"), ("0", "packed_tri")])
-def test_k4_hybrid_bit_exact(cl8, out):
-    """K4's multicast + pair hybrid (n ≥ 64 row tiles) — 4-CTA clusters sharing B, or (RF_K4_CL8=1) 8-CTA clusters
-    of 2 × 2 pairs sharing A and B — equals the pair-cluster kernel bit for bit (same accumulation order), in the
-    dense, mirrored and packed-triangle layouts (the last is what the e2e leg reads back)."""
+@pytest.mark.parametrize("cl8,dyn,out", [("0", 1, "upper"), ("0", 0, "upper"), ("1", 1, "upper"), ("0", 1, "full"),
+                                         ("0", 1, "packed_tri"), ("0", 0, "packed_tri")])
+def test_k4_hybrid_bit_exact(cl8, dyn, out):
+    """K4's multicast + pair hybrid (n ≥ 64 row tiles) — 4-CTA clusters sharing B, or (k4_cl8) 8-CTA clusters of
+    2 × 2 pairs sharing A and B; with the dynamic unit queue (default) or the static split — equals the pair-cluster
+    kernel bit for bit (same accumulation order), in the dense, mirrored and packed-triangle layouts."""
     n, p, m = 16384 + 77, 64, 1024
     rng = np.random.default_rng(5)
     Xd = dev(rng.standard_normal((n, p)) / math.sqrt(p), "bf16")
     Wd = dev(rng.standard_normal((m, p)), "bf16")
     ctx = rf.Context(0)
     ctx.set_option("k4_cl8", int(cl8))
+    ctx.set_option("k4_dynamic", dyn)      # 1: both kernels pull units from one device counter; 0: static split
     G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out=out, ctx=ctx)
     ctx.set_option("k4_hybrid", 0)
     G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper" if out == "packed_tri" else out, ctx=ctx)
