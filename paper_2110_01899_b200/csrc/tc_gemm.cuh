@@ -308,9 +308,11 @@ struct TileSeq {
     }
     return v == 0xFFFFFFFFu ? -1 : (long long)v;
   }
-  // next tile of this role: (schedule index / unit, row tile, column tile) with the cluster's CTA placement applied
+  // next tile of this role: (schedule index / unit, row tile, column tile) with the cluster's CTA placement applied.
+  // kDyn = false (every kernel but the K4 hybrid's): the static walk only, so the ring state costs no registers.
+  template <bool kDyn>
   __device__ __forceinline__ bool next(long long& tt, int& ti, int& tj) {
-    if (!dyn) {
+    if (!kDyn || !dyn) {
       if (t >= s->num_tiles) return false;
       cur.get(t, ti, tj);
       tt = t;
@@ -989,6 +991,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 #endif
   const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
+  // dynamic units only for the K4 hybrid's configurations (512-wide pair tiles); the host never sets sched.queue else
+  constexpr bool kDyn = Cfg::BN == 512 && Cfg::CL <= 4 && !kCol;
   const uint32_t ring_s = ptx::smem_u32(ring), rfull_s = ptx::smem_u32(&rfull[0]), rempty_s = ptx::smem_u32(&rempty[0]);
   const uint32_t rempty_c = ptx::mapa(rempty_s, 0);   // the fetcher's (cluster rank 0) ring_empty
   auto make_seq = [&](bool fetcher) {
@@ -1018,7 +1022,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     TileSeq seq = make_seq(crank == 0);
     long long t;
     int ti, tj;
-    while (seq.next(t, ti, tj)) {
+    while (seq.template next<kDyn>(t, ti, tj)) {
       const int ra = ti * Cfg::BM + (int)rank * 128;
       const int rb = tj * Cfg::BN + (int)rank * 128;
       for (int c = 0; c < nchunks; ++c) {
@@ -1103,7 +1107,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       TileSeq seq = make_seq(false);
       long long t;
       int ti, tj;
-      while (seq.next(t, ti, tj)) {
+      while (seq.template next<kDyn>(t, ti, tj)) {
         for (int c = 0; c < nchunks; ++c, ++it) {
           // K-chunked accumulation: every chunk goes to slot 0; the epilogue keeps the running fp32 sum in slot 1
           const bool dbl = Cfg::ACC_SLOTS == 2 && nchunks == 1;
@@ -1195,7 +1199,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     TileSeq seq = make_seq(false);
     long long t;
     int ti, tj;
-    for (; seq.next(t, ti, tj); ++tcount) {
+    for (; seq.template next<kDyn>(t, ti, tj); ++tcount) {
       if constexpr (kCol) {   // the tile's column vector (bulk-copied by this CTA's producer when the tile started)
         ptx::mbar_wait(&colfull[tcount & 1], (tcount >> 1) & 1);
         cx.col_s = ptx::smem_u32(sCol + (tcount & 1) * Cfg::BN);
