@@ -155,7 +155,9 @@ typedef enum {
                               on one stream, so no stream-memory wait ever heads a queue its producer sits behind */
   RF_OPT_K4_DYNAMIC = 14,  /* 1: the K4 hybrid's two kernels pull 512 × 512 units of one raster from a shared device
                               counter (no static split); 0: the static split of RF_OPT_K4_SPLIT_R100     default 1 */
-  RF_OPT_COUNT = 15
+  RF_OPT_K5_ARES = 15,     /* K5 with A-panel residency (bf16, 256 < p ≤ 512): 0 off, 1 with 8, 2 with 16 (2-KB
+                              staging), 3 with 12 epilogue warps                                      default 1 */
+  RF_OPT_COUNT = 16
 } rf_opt;
 rf_status rf_ctx_set_option(rf_ctx* ctx, rf_opt opt, int64_t value);
 rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);

@@ -257,22 +257,23 @@ rf_status make_tmap(CUtensorMap* m, const void* ptr, bool bf16, int64_t rows, in
   return make_tmap_es(m, ptr, bf16 ? 2 : 4, rows, kext, ld, box_rows);
 }
 
-// fp32 n_rows × n_cols output map for the epilogue's TMA stores: box 32 × 32, 128-B swizzle.
+// fp32 n_rows × n_cols output map for the epilogue's TMA stores: box 32 × 32, 128-B swizzle (half: box 16 × 32,
+// 64-B swizzle — the 2-KB staging buffers of EpiCtx<…, kHalf>).
 // Returns false (no error) when the rows are not 16-B aligned; the epilogue then stores directly.
-bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, bool half = false) {
   PFN_encode_tiled enc = encode_fn();
   if (!enc || (reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 4) % 16)) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {half ? 16u : 32u, 32};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, half ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---------------------------------------------------------------- context and options (include/rf.h)
-constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1};
+constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1, 1};
 thread_local rf_ctx* g_ctx = nullptr;     // the context of the call in progress on this thread
 int64_t opt(rf_opt o) { return g_ctx ? g_ctx->opts[o] : kOptDefault[o]; }
 
@@ -865,6 +866,19 @@ rf_status k5_go(const CUtensorMap& tA, const CUtensorMap& tAl, const CUtensorMap
   return launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, sms, st);
 }
 
+// K5 with A-panel residency (TcCfg kAres): segment schedule, column blocks of kSegLen tiles (tc_gemm.cuh Sched).
+constexpr int kSegLen = 16;
+template <class C, class E>
+rf_status k5_go_ares(const CUtensorMap& tA, const CUtensorMap& tO, const E& e, int64_t p, int rt0, int rt1, int tn,
+                     int sms, cudaStream_t st) {
+  rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, 1);
+  sc.seg_len = kSegLen;
+  sc.num_tiles = (int)sc.seg_prefix((tn + kSegLen - 1) / kSegLen);
+  sc.load_pol = 1;
+  sc.store_pol = 1;
+  return launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, sms, st);
+}
+
 // Φ4+Φ5: tensor-core XᵀX with the EQ1 epilogue over the row range's triangle pair tiles (256 × 256)
 template <bool kOdd>
 rf_status launch_k5(const K5Args& a) {
@@ -895,7 +909,23 @@ rf_status launch_k5(const K5Args& a) {
     // 96 registers) help: configs[4] 11.3 → 9.54 ms (12 warps: 9.94).  Long K: the MMA sets it and the 8-warp
     // kernel stays ahead (configs[3] shape, p = 1024: 3.63 vs 3.78 ms).  DESIGN.md §7.
     const bool wide = opt(RF_OPT_K5_WIDE) < 0 ? p <= 512 : opt(RF_OPT_K5_WIDE) != 0;
-    if (bf && wide) {
+    // A-panel residency: K = p of 5 … 8 K-blocks (the producer may run at most STAGES = 4 K-blocks ahead of the MMA,
+    // which keeps the aempty parity wait exact, tc_gemm.cuh)
+    const int kb5 = (int)((p + 63) / 64);
+    const int ares = (int)opt(RF_OPT_K5_ARES);
+    if (bf && ares > 0 && kb5 > 4 && kb5 <= 8) {
+      if (ares == 2) {   // 2-KB staging buffers: the store map with 16 × 32 boxes and 64-B swizzle
+        CUtensorMap tOh;
+        const bool okh = a.tri_T > 0 ? make_tmap_out(&tOh, Phi, tri_tiles(n) * 256, 256, 256, true)
+                                     : make_tmap_out(&tOh, Phi, n, n, ldphi, true);
+        if (!okh) tOh = tA;
+        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 16, 1>>(tA, tOh, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      } else if (ares == 3) {
+        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 12, 1>>(tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+      } else if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 8, 1>>(tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) {
+        return s;
+      }
+    } else if (bf && wide) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, 1, 2, 16>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
     } else if (bf) {
       if ((s = k5_go<rfk::TcCfg<1, 1, 256, K5_STG>>(tA, tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;

@@ -45,10 +45,14 @@ namespace rfk {
 // rank-in-pair and TMA-multicasts it to the same rank of both pairs, so a B sub-tile leaves L2 once per cluster
 // instead of once per pair (a third less L2 → SM traffic per flop for BN = 512, a quarter for BN = 256).
 // Requires kSplit == 1.
+// kAres: A-panel residency (K5 with K ≤ 8 K-blocks): each CTA keeps its 128 A rows over the whole K in shared memory
+// for a run of column tiles of the same row tile (segment schedule, Sched::seg_len), so only B streams per tile.
 template <int kFmt /*1 = bf16 (kind::f16), 2 = tf32, 3 = fp8 e4m3 (kind::f8f6f4)*/, int kSplit /*1 or 3*/,
-          int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8>
+          int kBN /*256 or 512*/, int kStg = -1, int kCl = 2, int kEpiW = 8, int kAres = 0>
 struct TcCfg {
   static constexpr int CL = kCl;
+  static constexpr bool ARES = kAres != 0;
+  static_assert(!kAres || (kSplit == 1 && kCl == 2 && kBN == 256), "A residency: one operand split, pairs, BN 256");
   static_assert(kCl == 2 || (kCl == 4 && kSplit == 1) || (kCl == 8 && kSplit == 1 && kBN == 512),
                 "4-CTA clusters: one operand split; 8-CTA clusters: BN = 512");
   static constexpr int BM = 256, BN = kBN;      // pair tile
@@ -59,7 +63,9 @@ struct TcCfg {
   static constexpr int NOPS = kSplit == 3 ? 2 : 1;
   static constexpr int A_BYTES = 128 * 128;     // per CTA: 128 rows × 128 B
   static constexpr int B_BYTES = 128 * 128;     // per CTA per N sub-tile
-  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + NSUB * B_BYTES);
+  static constexpr int ARES_KB = 8;              // resident K-blocks (K ≤ 512 bf16)
+  static constexpr int ARES_BYTES = kAres ? ARES_KB * A_BYTES : 0;
+  static constexpr int STAGE_BYTES = NOPS * ((kAres ? 0 : A_BYTES) + NSUB * B_BYTES);
   static constexpr int ACC_COLS = kBN;
   static constexpr int ACC_SLOTS = 512 / kBN;
   // 8 epilogue warps (two per TMEM lane quarter, each owning half of the accumulator columns), or 12 / 16 (three /
@@ -68,18 +74,21 @@ struct TcCfg {
   static_assert(kEpiW == 8 || kEpiW == 12 || kEpiW == 16, "8, 12 or 16 epilogue warps");
   static constexpr int THREADS = 128 + 32 * kEpiW;
   static constexpr int STG_BUFS = kStg >= 0 ? kStg : ((kSplit == 3 || kBN == 512) ? 1 : 2);   // per epi warp
-  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * 4096;
+  // 16 epilogue warps with A residency: 2-KB staging buffers (32 × 16 boxes, 64-B swizzle) keep four B stages
+  static constexpr bool HALF_STG = kAres && kEpiW == 16;
+  static constexpr int STG_BUF_BYTES = HALF_STG ? 2048 : 4096;
+  static constexpr int STG_BYTES = EPI_WARPS * STG_BUFS * STG_BUF_BYTES;
   // per-column vector of the tile (epilogues with kColVec, e.g. ‖x_j‖²/τ of K5), double-buffered with the accumulator
   static constexpr int COL_BYTES = kBN == 256 ? 2 * 256 * 4 : 0;
-  static constexpr int BAR_BYTES = 256;             // mbarriers (2·STAGES + 6) + the TMEM address word
+  static constexpr int BAR_BYTES = 512;             // mbarriers, the TMEM address word, the unit ring
   static constexpr int SMEM_MAX = 227 * 1024;       // opt-in dynamic shared memory per CTA
-  static constexpr int STAGES = (SMEM_MAX - STG_BYTES - COL_BYTES - BAR_BYTES) / STAGE_BYTES;
+  static constexpr int FIXED = ARES_BYTES + STG_BYTES + COL_BYTES + BAR_BYTES;
+  static constexpr int STAGES = (SMEM_MAX - FIXED) / STAGE_BYTES;
   // room left to align the dynamic window to 1024 B (the base is 1024-aligned in practice: the kernel checks)
-  static constexpr int SLACK = SMEM_MAX - STAGES * STAGE_BYTES - STG_BYTES - COL_BYTES - BAR_BYTES < 1024
-                                   ? SMEM_MAX - STAGES * STAGE_BYTES - STG_BYTES - COL_BYTES - BAR_BYTES
-                                   : 1024;
-  static constexpr size_t SMEM_BYTES = (size_t)SLACK + (size_t)STAGES * STAGE_BYTES + STG_BYTES + COL_BYTES + BAR_BYTES;
-  static_assert(8 * (2 * STAGES + 6 + 2 * 4) + 4 + 4 * 4 <= BAR_BYTES, "barrier area");
+  static constexpr int SLACK = SMEM_MAX - STAGES * STAGE_BYTES - FIXED < 1024 ? SMEM_MAX - STAGES * STAGE_BYTES - FIXED
+                                                                              : 1024;
+  static constexpr size_t SMEM_BYTES = (size_t)SLACK + (size_t)STAGES * STAGE_BYTES + FIXED;
+  static_assert(8 * (2 * STAGES + 6 + 2 * 4 + 2) + 4 + 4 * 4 <= BAR_BYTES, "barrier area");
   static constexpr uint32_t IDESC = ptx::idesc_f32acc(kFmt == 3 ? 0u : (uint32_t)kFmt, 256, 256);
   static_assert(STAGES >= 2, "pipeline too shallow");
   static_assert(SMEM_BYTES <= 227 * 1024, "smem budget");
@@ -135,6 +144,40 @@ struct Sched {
   // nsub row tiles (2I, 2I + 1; rows ≥ sub_rows skipped), a 4-CTA-cluster kernel as one row tile per pair (2I + pi).
   uint32_t* queue;
   int nsub, sub_rows;
+  // Segment schedule (A residency, seg_len > 0): work item = segment (row tile I, column tiles [J0, J1)), column-block
+  // major: for column block b (tiles [b·L, (b+1)·L) ∩ [0, T)) every row tile I ∈ [row_tile0, min(row_tile1, (b+1)L, T))
+  // in order, J0 = max(b·L, I).  Concurrent segments share the block's B panels; a cluster reloads A once per segment.
+  int seg_len;
+  __host__ __device__ __forceinline__ long long seg_rows(int b) const {   // segments of column block b
+    const int hi = min(min(row_tile1, (b + 1) * seg_len), tiles_n);
+    return hi > row_tile0 ? hi - row_tile0 : 0;
+  }
+  __host__ __device__ __forceinline__ long long seg_prefix(int b) const {   // segments of blocks [0, b)
+    // blocks whose row bound is (b'+1)L (before the bound saturates at U = min(row_tile1, T)) contribute an
+    // arithmetic series, the rest U − row_tile0 each
+    const long long U = min(row_tile1, tiles_n), L = seg_len, r0 = row_tile0;
+    const long long bsat = U / L;               // blocks b' < bsat have (b'+1)L ≤ U
+    long long tot = 0;
+    const long long b1 = b < bsat ? b : bsat;
+    long long blo = r0 / L;                     // first block with (b'+1)L > r0
+    if (blo < b1) {                             // Σ_{b'=blo}^{b1−1} ((b'+1)L − r0)
+      const long long cnt = b1 - blo;
+      tot += L * ((blo + 1 + b1) * cnt / 2) - r0 * cnt;
+    }
+    if (b > bsat && U > r0) tot += (long long)(b - bsat) * (U - r0);
+    return tot;
+  }
+  __host__ __device__ __forceinline__ void seg_get(long long sidx, int& I, int& J0, int& J1) const {
+    const int nb = (tiles_n + seg_len - 1) / seg_len;
+    int lo = 0, hi = nb;                        // largest b with seg_prefix(b) ≤ sidx
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (seg_prefix(mid) <= sidx) lo = mid; else hi = mid;
+    }
+    I = row_tile0 + (int)(sidx - seg_prefix(lo));
+    J0 = max(lo * seg_len, I);
+    J1 = min((lo + 1) * seg_len, tiles_n);
+  }
 
   struct Group {
     int I0, I1, J0, Jf;
@@ -198,6 +241,7 @@ struct Sched {
     s.queue = nullptr;
     s.nsub = 1;
     s.sub_rows = 0;
+    s.seg_len = 0;
     long long tot = 0;
     for (int I0 = row_tile0; I0 < row_tile1; I0 += s.gm) tot += s.group(I0).cnt;
     s.num_tiles = (int)tot;
@@ -262,6 +306,8 @@ struct TileSeq {
   uint32_t lane, ring_s, rfull_s, rempty_s, rempty_c;
   int k, sub, nsub, ui, uj;
   long long u;
+  int sI, sJ, sJ1;       // segment mode: current segment and next column tile
+  bool seg_first;        // the tile just returned starts a segment (a new A panel)
   __device__ __forceinline__ void init(const Sched* sp, int cid, int ncl_, int cl_, int pi_, bool fetcher_,
                                        uint32_t lane_, uint32_t ring_s_, uint32_t rfull_s_, uint32_t rempty_s_,
                                        uint32_t rempty_c_) {
@@ -283,6 +329,8 @@ struct TileSeq {
     sub = nsub;
     ui = uj = 0;
     u = 0;
+    sI = sJ = sJ1 = 0;
+    seg_first = false;
   }
   __device__ __forceinline__ long long fetch() {
     const int slot = k % kRing;
@@ -310,8 +358,21 @@ struct TileSeq {
   }
   // next tile of this role: (schedule index / unit, row tile, column tile) with the cluster's CTA placement applied.
   // kDyn = false (every kernel but the K4 hybrid's): the static walk only, so the ring state costs no registers.
-  template <bool kDyn>
+  template <bool kDyn, bool kSeg = false>
   __device__ __forceinline__ bool next(long long& tt, int& ti, int& tj) {
+    if (kSeg) {               // segment schedule (A residency configurations only)
+      seg_first = false;
+      if (sJ >= sJ1) {
+        if (t >= s->num_tiles) return false;
+        s->seg_get(t, sI, sJ, sJ1);
+        t += ncl;
+        seg_first = true;
+      }
+      tt = t - ncl;
+      ti = sI;
+      tj = sJ++;
+      return true;
+    }
     if (!kDyn || !dyn) {
       if (t >= s->num_tiles) return false;
       cur.get(t, ti, tj);
@@ -345,7 +406,7 @@ struct TileSeq {
 // ------------------------------------------------------------------------------------------
 // Epilogue store helpers.  A warp owns 32 rows (lanes) × 32 columns per call.
 // ------------------------------------------------------------------------------------------
-template <int kBufs>
+template <int kBufs, bool kHalf = false>
 struct EpiCtx {
   const CUtensorMap* tm;   // fp32 output map: box 32 × 32, 128-B swizzle, bounds = the n×n matrix
   uint8_t* sbuf;           // this warp's staging buffers (kBufs × 4 KB, 1024-B aligned)
@@ -373,8 +434,35 @@ struct EpiCtx {
 #pragma unroll
     for (int c = 0; c < 8; ++c) ptx::sts128(row + ((c ^ (lane & 7)) << 4), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
   }
+  // kHalf: one 2-KB buffer per warp, the block goes out as two 32-row × 16-column boxes (64-B swizzle: 16-B chunk c of
+  // row r at c ^ ((r >> 1) & 3), conflict-free for the 8-lane phases of STS.128); the second half waits until the
+  // first has been read out of shared memory.
+  __device__ __forceinline__ void stage_half(uint32_t b, const float (&v)[32], int hf) {
+    const uint32_t row = b + lane * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int q = 4 * hf + c;
+      ptx::sts128(row + ((c ^ ((lane >> 1) & 3)) << 4), v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+  }
   __device__ __forceinline__ void store_block(int64_t row_lo, int64_t col0, const float (&v)[32]) {
     static_assert(kBufs >= 1, "store_block needs staging buffers");
+    if constexpr (kHalf) {
+      static_assert(kBufs == 1, "half-width staging: one buffer per warp");
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        if (lane == 0) ptx::bulk_wait_read<0>();
+        __syncwarp();
+        stage_half(sbuf_s, v, hf);
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          issue(sbuf, (int32_t)col0 + 16 * hf, (int32_t)row_lo);
+          ptx::bulk_commit();
+        }
+      }
+      return;
+    }
     if (kBufs == 2) {
       if (nst == 0) {
         if (lane == 0) ptx::bulk_wait_read<0>();       // the previous batch has been read out of smem
@@ -924,8 +1012,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const uint32_t pad = (1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u;
   if (pad > (uint32_t)Cfg::SLACK) __trap();   // never seen: the dynamic window starts 1024-aligned
   uint8_t* smem = smem_raw + pad;
-  uint8_t* sA = smem;                                                    // [STAGES][NOPS][A_BYTES]
-  uint8_t* sB = sA + (size_t)STAGES * NOPS * Cfg::A_BYTES;               // [STAGES][NOPS][NSUB][B_BYTES]
+  uint8_t* sA = smem;                       // [STAGES][NOPS][A_BYTES], or (A residency) [ARES_KB][A_BYTES]
+  uint8_t* sB = sA + (Cfg::ARES ? (size_t)Cfg::ARES_BYTES : (size_t)STAGES * NOPS * Cfg::A_BYTES);   // [STAGES][NOPS][NSUB][B_BYTES]
   uint8_t* sStg = sB + (size_t)STAGES * NOPS * NSUB * Cfg::B_BYTES;      // [EPI_WARPS][STG_BUFS][4096]
   float* sCol = reinterpret_cast<float*>(sStg + Cfg::STG_BYTES);          // [2][BN] column vectors (kColVec)
   uint64_t* full = reinterpret_cast<uint64_t*>(sStg + Cfg::STG_BYTES + Cfg::COL_BYTES);
@@ -936,7 +1024,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint64_t* colempty = colfull + 2;
   uint64_t* rfull = colempty + 2;       // dynamic-unit ring (TileSeq)
   uint64_t* rempty = rfull + kRing;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + kRing);
+  uint64_t* afull = rempty + kRing;     // A residency: the resident A panel has landed / its last MMAs completed
+  uint64_t* aempty = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
   uint32_t* ring = tmem_slot + 1;
   constexpr bool kCol = ColVecOf<Epi>::value;
   static_assert(!kCol || (Cfg::COL_BYTES > 0 && Cfg::CL == 2), "column vectors: 256-wide pair tiles, clusters of 2");
@@ -974,6 +1064,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       ptx::mbar_init(&rfull[a], 1);
       ptx::mbar_init(&rempty[a], (Cfg::CL - 1) + Cfg::CL / 2 + Cfg::CL * Cfg::EPI_WARPS);
     }
+    ptx::mbar_init(afull, 1);
+    ptx::mbar_init(aempty, 1);
     ptx::fence_mbarrier_init();
   }
   if (sched.started && blockIdx.x == 0 && threadIdx.x == 0) ptx::st_relaxed_gpu(sched.started, 1u);
@@ -1022,9 +1114,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     TileSeq seq = make_seq(crank == 0);
     long long t;
     int ti, tj;
-    while (seq.template next<kDyn>(t, ti, tj)) {
+    uint32_t tiles_done = 0;
+    const uint32_t afull_c = ptx::mapa(ptx::smem_u32(afull), leader);
+    while (seq.template next<kDyn, Cfg::ARES>(t, ti, tj)) {
       const int ra = ti * Cfg::BM + (int)rank * 128;
       const int rb = tj * Cfg::BN + (int)rank * 128;
+      if constexpr (Cfg::ARES) {
+        // a new segment: reload this CTA's 128-row A panel over the whole K once the MMAs of the previous tile (the
+        // last reader of the old panel) have completed; completion bytes of both CTAs on the leader's afull
+        if (seq.seg_first && lane == 0) {
+          if (tiles_done > 0) ptx::mbar_wait(aempty, (tiles_done - 1) & 1u);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(afull, 2u * (uint32_t)num_kb * Cfg::A_BYTES);
+          for (int kb = 0; kb < num_kb; ++kb)
+            ptx::tma_load_2d_cg2(sA + (size_t)kb * Cfg::A_BYTES, &tmA, afull_c, kb * Cfg::BK, ra, pol);
+        }
+        __syncwarp();
+        ++tiles_done;
+      }
       for (int c = 0; c < nchunks; ++c) {
         const int kb1 = min(num_kb, (c + 1) * kchunk);
         for (int kb = c * kchunk; kb < kb1; ++kb, ++step) {
@@ -1060,7 +1166,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                                       mcA8, pol);
               ptx::tma_load_2d_cg2_mc(b + di * Cfg::B_BYTES, &tmB, full_rel0 + stage * 8, k, rb + 256 * (int)di, mcB8,
                                       pol);
-            } else if (!kSkipA) {
+            } else if (!kSkipA && !Cfg::ARES) {
               ptx::tma_load_2d_cg2(a, &tmA, fb, k, ra, pol);
             }
             if (Cfg::CL == 8) {
@@ -1107,7 +1213,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       TileSeq seq = make_seq(false);
       long long t;
       int ti, tj;
-      while (seq.template next<kDyn>(t, ti, tj)) {
+      uint32_t segs = 0;
+      while (seq.template next<kDyn, Cfg::ARES>(t, ti, tj)) {
+        if constexpr (Cfg::ARES) {
+          if (seq.seg_first) {   // the segment's A panel has landed in both CTAs
+            ptx::mbar_wait(afull, segs & 1u);
+            ++segs;
+          }
+        }
         for (int c = 0; c < nchunks; ++c, ++it) {
           // K-chunked accumulation: every chunk goes to slot 0; the epilogue keeps the running fp32 sum in slot 1
           const bool dbl = Cfg::ACC_SLOTS == 2 && nchunks == 1;
@@ -1120,7 +1233,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            const uint32_t a_s = ptx::smem_u32(sA + (size_t)(stage * NOPS) * Cfg::A_BYTES);
+            const uint32_t a_s = ptx::smem_u32(sA + (Cfg::ARES ? (size_t)kb * Cfg::A_BYTES
+                                                              : (size_t)(stage * NOPS) * Cfg::A_BYTES));
             const uint32_t b_s = ptx::smem_u32(sB + (size_t)(stage * NOPS * NSUB) * Cfg::B_BYTES);
             const uint64_t ad = ptx::sdesc_k128(a_s);
             if (ptx::elect_one()) {
@@ -1155,6 +1269,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (ptx::elect_one()) ptx::mma_commit_cg2_mc(&tfull[slot], (uint16_t)(0x3u << (2 * pi)));
           __syncwarp();
         }
+        // A residency: this tile's MMAs — the last readers so far of the resident A panel — complete → aempty
+        if (Cfg::ARES && ptx::elect_one()) ptx::mma_commit_cg2_mc(aempty, (uint16_t)0x3u);
+        __syncwarp();
       }
     }
   } else if (warp == 3) {
@@ -1162,12 +1279,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // ===== Column-vector loader: tile k's slice of the per-column vector into sCol[k & 1] once the epilogue has
       // released the buffer (tile k − 2), a 1-D bulk copy completing on colfull.  A warp of its own, so the operand
       // producer never waits on the epilogue.
-      TileCursor cur;
-      cur.init(&sched);
-      int tcount = 0;
-      for (int t = cid; t < sched.num_tiles; t += ncl, ++tcount) {   // static schedules only (kColVec, host-checked)
-        int ti, tj;
-        cur.get(t, ti, tj);
+      TileSeq seq = make_seq(false);   // static or segment schedules only (kColVec never runs the unit queue)
+      long long t;
+      int ti, tj;
+      for (int tcount = 0; seq.template next<false, Cfg::ARES>(t, ti, tj); ++tcount) {
         if (lane == 0) {
           const int cs = tcount & 1;
           ptx::mbar_wait(&colempty[cs], ((tcount >> 1) & 1) ^ 1);
@@ -1181,9 +1296,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     // ===== Epilogue: TMEM → registers → fused op → global (8 warps) =====
     const uint32_t q = warp & 3;               // TMEM lane quarter this warp may access
     const uint32_t h = (warp - 4) >> 2;        // column share of the accumulator (0 .. EPI_WARPS/4 − 1)
-    EpiCtx<Cfg::STG_BUFS> cx;
+    EpiCtx<Cfg::STG_BUFS, Cfg::HALF_STG> cx;
     cx.tm = &tmOut;
-    cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * 4096;
+    cx.sbuf = sStg + (size_t)(warp - 4) * Cfg::STG_BUFS * Cfg::STG_BUF_BYTES;
     cx.sbuf_s = ptx::smem_u32(cx.sbuf);
     cx.col_s = 0;
     cx.cur = 0;
@@ -1199,7 +1314,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     TileSeq seq = make_seq(false);
     long long t;
     int ti, tj;
-    for (; seq.template next<kDyn>(t, ti, tj); ++tcount) {
+    for (; seq.template next<kDyn, Cfg::ARES>(t, ti, tj); ++tcount) {
       if constexpr (kCol) {   // the tile's column vector (bulk-copied by this CTA's producer when the tile started)
         ptx::mbar_wait(&colfull[tcount & 1], (tcount >> 1) & 1);
         cx.col_s = ptx::smem_u32(sCol + (tcount & 1) * Cfg::BN);

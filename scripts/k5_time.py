@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--wide", type=int, default=-1)
     ap.add_argument("--out", default="upper")
     ap.add_argument("--act", default="tanh")
+    ap.add_argument("--ares", type=int, default=0, help="context option k5_ares (A-panel residency)")
     a = ap.parse_args()
     import torch
     import paper_2110_01899_b200 as rf
@@ -31,6 +32,8 @@ def main():
     ctx = rf.Context(0) if hasattr(rf, "Context") else None
     if ctx is not None:
         ctx.set_option("k5_wide", a.wide)
+        if a.ares:
+            ctx.set_option("k5_ares", a.ares)
     Phi = (torch.empty(rf.rf_packed_tri_elems(a.n), device=dev) if a.out == "packed_tri"
            else torch.empty(a.n, a.n, device=dev))
     ws = torch.empty(rf.rf_phi_workspace_size(a.p, a.n, "bf16"), dtype=torch.uint8, device=dev)
@@ -50,7 +53,7 @@ def main():
     med = ks[len(ks) // 2]
     tri = a.n * (a.n + 1) / 2.0
     by = 4.0 * tri + 2.0 * a.n * a.p
-    print(json.dumps({"lib": os.environ.get("RF_B200_LIB", "in-tree"), "n": a.n, "p": a.p, "wide": a.wide,
+    print(json.dumps({"lib": os.environ.get("RF_B200_LIB", "in-tree"), "n": a.n, "p": a.p, "wide": a.wide, "ares": a.ares,
                       "out": a.out, "k5_ms_median": med, "k5_ms_min": ks[0], "k5_ms_all": ks,
                       "hbm_gbs": by / (med * 1e-3) / 1e9, "tflops": a.p * a.n * (a.n + 1.0) / (med * 1e-3) / 1e12}))
 

@@ -394,3 +394,60 @@ def test_k4_hybrid_bit_exact(cl8, dyn, out):
         assert torch.equal(got, ref)
     else:
         assert torch.equal(G1, G0)
+
+
+def test_non_current_stream_orders_allocations_and_results():
+    """the wrappers allocate outputs and workspace on the stream the kernels are enqueued on, so a
+    call on a non-current stream neither races the allocator's zero-fill nor lets the workspace be reused while the
+    kernels still run: G from a side stream equals G from the current stream bit for bit, repeatedly, with the
+    side stream never synchronized against the current one by the caller."""
+    rng = np.random.default_rng(9)
+    n, p, m = 2100, 128, 1024
+    Xd = dev(rng.standard_normal((n, p)) / math.sqrt(p), "bf16")
+    Wd = dev(rng.standard_normal((m, p)), "bf16")
+    ref = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper")
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    outs = []
+    for _ in range(4):
+        G = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper", stream=side)   # allocated on `side`
+        Phi = rf.rf_phi_closed_form(Xd, act="tanh", prec="bf16", stream=side)
+        outs.append((G, Phi))
+        torch.empty(1 << 26, dtype=torch.uint8, device="cuda")   # allocator churn on the current stream
+    side.synchronize()
+    Pref = rf.rf_phi_closed_form(Xd, act="tanh", prec="bf16")
+    torch.cuda.synchronize()
+    for G, Phi in outs:
+        assert torch.equal(G, ref)
+        assert torch.equal(Phi, Pref)
+
+
+@pytest.mark.parametrize("ares", [1, 2])
+@pytest.mark.parametrize("out,rows", [("upper", None), ("full", None), ("packed_tri", None), ("upper", (512, 1536))])
+def test_phi_a_resident_bit_exact(ares, out, rows):
+    """K5 with A-panel residency (RF_OPT_K5_ARES: each CTA keeps its A rows over the whole K = p in shared memory for
+    a segment of up to 16 column tiles; column-block-major segment schedule) computes every entry with the same
+    arithmetic as the default K5: bit-identical, in every layout and on a row block."""
+    n, p = 2100, 448                     # 7 K-blocks, ragged rows
+    X = synthetic.make_X(4, n=n, p=p)
+    Xd = dev(X, "bf16")
+    ctx = rf.Context(0)
+    res = []
+    for a in (ares, 0):
+        ctx.set_option("k5_ares", a)
+        kw = {} if rows is None else {"row_begin": rows[0], "row_end": rows[1]}
+        if out == "packed_tri":
+            P = torch.full((rf.rf_packed_tri_elems(n),), float("nan"), device="cuda")
+        else:
+            P = torch.full((n, n), SENTINEL, device="cuda")
+        rf.rf_phi_closed_form(Xd, act="tanh", prec="bf16", out=out, Phi=P, ctx=ctx, **kw)
+        torch.cuda.synchronize()
+        res.append(P.cpu().numpy())
+    if out == "packed_tri":
+        from paper_2110_01899_b200 import layout
+        res = [layout.unpack_tri(r, n) for r in res]
+        I, J = upper_idx(n)
+        assert np.array_equal(res[0][I, J], res[1][I, J])
+    else:
+        assert np.array_equal(res[0], res[1])
