@@ -798,8 +798,7 @@ rf_status gram_tc(const GramTcArgs& g, int kchunk4) {
   }
   if (g.pack) {   // G5: every upper 256-tile of the partial into its exchange slot (canonical ownership, no schedule index)
     // the NCCL chunk counters expect 2 CTAs × EPI_WARPS arrivals per pair tile (abi_ctx.cuh kPackArrivals)
-    static_assert(C4::EPI_WARPS == 8 && rfk::TcCfg<kFmt, kSplit, kBN4, -1, 4>::EPI_WARPS == 8,
-                  "kPackArrivals = 2 × 8 epilogue warps");
+    static_assert(C4::EPI_WARPS == 8, "kPackArrivals = 2 × 8 epilogue warps (the hybrid's kernels have 8 as well)");
     rfk::EpiSyrkPacked e4{(float)(1.0 / (double)g.m_total), *g.pack};
     if constexpr (kBN4 == 512 && kSplit == 1) {
       if (lockw > 0) {
