@@ -666,6 +666,18 @@ def main():
                  "K5_ms": k5ms, "K5_hbm_gbs": by4 / (k5ms * 1e-3) / 1e9 if k5ms else None,
                  "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / pk["hbm_gbs"] if k5ms else None,
                  "K5_tflops": p4 * n4 * (n4 + 1.0) / (k5ms * 1e-3) / 1e12 if k5ms else None}
+            if k5ms:
+                # K5's two roofline floors (DESIGN.md §7 "K5's roofline"): the 2p-flop upper-triangle contraction on
+                # the tensor pipe at the sustained rate of its dtype, and its compulsory bytes at the measured HBM
+                # copy rate; at p = 512 the intensity 2p / 4 B = 256 flop/B is above the ridge, so the tensor floor
+                # binds.  frac_roofline = max(floors) / K5 time.
+                ptc = pk["bf16_tflops_sustained"] * (1.0 if mode == "bf16" else 0.5) / (3.0 if mode == "3xtf32" else 1.0)
+                t_tc = p4 * n4 * (n4 + 1.0) / (ptc * 1e12) * 1e3
+                t_hbm = by4 / (pk["hbm_gbs"] * 1e9) * 1e3
+                d.update({"K5_floor_tensor_ms": t_tc, "K5_floor_hbm_ms": t_hbm,
+                          "K5_bound": "tensor" if t_tc >= t_hbm else "hbm",
+                          "K5_frac_tensor_sustained": t_tc / k5ms,
+                          "K5_frac_roofline": max(t_tc, t_hbm) / k5ms})
             del ws4
             return d
 
