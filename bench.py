@@ -254,7 +254,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         try:
             for line in open(self.path):
@@ -267,6 +267,10 @@ class ClockSampler:
                     continue
                 sm.append(s)
                 mx.append(m)
+                try:
+                    pw.append(float(f[3]))
+                except ValueError:
+                    pass
                 for nm, v in zip(names, f[5:9]):
                     if v.lower().startswith("active"):
                         reasons.add(nm)
@@ -275,8 +279,10 @@ class ClockSampler:
         if not sm:
             return None
         sm.sort()
+        pw.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_min_mhz": sm[0], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": pw[len(pw) // 2] if pw else None,
+                "power_w_max": pw[-1] if pw else None}
 
 
 def main():

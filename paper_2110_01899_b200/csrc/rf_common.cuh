@@ -168,7 +168,7 @@ __device__ __forceinline__ void eq1_pair(float g0, float g1, float nj0, float nj
   const uint64_t r = sub2(pk2(nj0, nj1), mul2(nu, nu));
   float r0, r1;
   up2(r, r0, r1);
-  const uint64_t s = pk2(sqrt_fast(fmaxf(r0, 0.f)), sqrt_fast(fmaxf(r1, 0.f)));
+  const uint64_t s = pk2(sqrt_fast(fabsf(r0)), sqrt_fast(fabsf(r1)));
   const uint64_t C1 = fma2(s, f1_2, f0_2);
   uint64_t o;
   if (kOdd) {
@@ -190,7 +190,7 @@ __device__ __forceinline__ void eq1_pair_odd(float g0, float g1, float nj0, floa
   const uint64_t r = sub2(pk2(nj0, nj1), mul2(nu, nu));
   float r0, r1;
   up2(r, r0, r1);
-  const uint64_t s = pk2(sqrt_fast(fmaxf(r0, 0.f)), sqrt_fast(fmaxf(r1, 0.f)));
+  const uint64_t s = pk2(sqrt_fast(fabsf(r0)), sqrt_fast(fabsf(r1)));
   up2(mul2(g, fma2(s, q2, p2)), out0, out1);
 }
 
@@ -198,9 +198,11 @@ template <typename T>
 __device__ __forceinline__ T eq1_entry(T g, T a0, T a1, T a2h, T c, T njt, bool diag, T nu_diag, T e0, T e1, T e2,
                                        T f0, T f1) {
   T nu = g * c;
-  T r = fma(-nu, nu, njt);
-  r = r > T(0) ? r : T(0);
-  T s = sqrt_fast(r);
+  // r = ‖x_j‖²/τ − ν² ≥ 0 by Cauchy–Schwarz; a rounding-negative r (near-parallel rows) is taken by magnitude:
+  // |r| and max(r, 0) are equally close to the exact value (≤ the rounding of r), and |·| folds into MUFU.SQRT's
+  // operand (two FMNMX fewer per entry pair in K5)
+  const T r = fma(-nu, nu, njt);
+  T s = sqrt_fast(r < T(0) ? -r : r);
   if (diag) {
     nu = nu_diag;
     s = T(0);

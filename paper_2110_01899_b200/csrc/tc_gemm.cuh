@@ -31,6 +31,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ptx_sm100.cuh"
 #include "rf_common.cuh"
 
@@ -105,6 +107,17 @@ struct ColVecOf {
 template <class E>
 struct ColVecOf<E, decltype(void(E::kColVec))> {
   static constexpr bool value = E::kColVec != 0;
+};
+// Epilogues with an interior fast path declare kFast = 1 and provide fast_tile(ti, tj) (every chunk of the tile is
+// needed, off the diagonal band and stored whole by TMA) and fast<kSlot>(…): the kernel's 8-warp loop then runs the
+// tile with no per-chunk predicates and a static staging-batch slot (chunk cc goes to buffer cc & 1).
+template <class E, class = void>
+struct FastOf {
+  static constexpr bool value = false;
+};
+template <class E>
+struct FastOf<E, decltype(void(E::kFast))> {
+  static constexpr bool value = E::kFast != 0;
 };
 
 // Pair-tile scheduler.  Rows of 256, columns of BN.  Rectangular: row tiles [row_tile0, row_tile1) × all
@@ -428,6 +441,45 @@ struct EpiCtx {
       ptx::tma_store_2d_hint(tm, b, c0, r0, pol);
     else
       ptx::tma_store_2d(tm, b, c0, r0);
+  }
+  // stg_x = sbuf_s + 128·lane with the lane's 128-B-swizzle XOR folded in: chunk c of the lane's row sits at
+  // stg_x ^ (c << 4) (bits 4..6 of sbuf_s + 128·lane are zero: 1024-B aligned buffers), buffer b at + 4096·b.
+  uint32_t stg_x;
+  __device__ __forceinline__ void set_stg_x() { stg_x = (sbuf_s + lane * 128) | ((lane & 7) << 4); }
+  template <int kOff>
+  __device__ __forceinline__ void stage_x(const float (&v)[32]) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) ptx::sts128((stg_x ^ (c << 4)) + kOff, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+  // Interior tiles: with two buffers the warp's chunks pair up as (even, odd) = (buffer 0, buffer 1) of one batch
+  // (the odd chunk's block is 32 columns right of the even one's, so the batch needs no saved coordinates).
+  template <int kSlot>
+  __device__ __forceinline__ void store_static(int32_t r0, int32_t c0, const float (&v)[32]) {
+    static_assert(kBufs == 1 || kBufs == 2, "one or two 4-KB staging buffers");
+    if constexpr (kBufs == 1) {   // one buffer: wait until the previous block has been read out, stage, store
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+      stage_x<0>(v);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        issue(sbuf, c0, r0);
+        ptx::bulk_commit();
+      }
+    } else if constexpr (kSlot == 0) {
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+      stage_x<0>(v);
+    } else {
+      stage_x<4096>(v);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        issue(sbuf, c0 - 32, r0);
+        issue(sbuf + 4096, c0, r0);
+        ptx::bulk_commit();
+      }
+    }
   }
   __device__ __forceinline__ void stage(uint32_t b, const float (&v)[32]) {
     const uint32_t row = b + lane * 128;
@@ -792,6 +844,7 @@ struct EpiSyrkPacked {
 template <bool kOdd>
 struct EpiEq1 {
   static constexpr int kColVec = 1;   // ‖x_j‖²/τ staged per tile in shared memory by the producer (ColVecOf)
+  static constexpr int kFast = 1;     // interior tiles: fast<kSlot> (FastOf)
   float* Phi;
   int64_t ld, n;
   const RowCoef* rc;     // per row
@@ -811,6 +864,44 @@ struct EpiEq1 {
   __device__ __forceinline__ Pre prefetch(int64_t row_lo, int64_t, uint32_t lane) const {
     const int64_t row = row_lo + lane;
     return Pre{rc[row < n ? row : n - 1]};
+  }
+  // A 256×256 tile strictly right of the diagonal tile and inside the n×n matrix, stored by TMA into the plain
+  // upper triangle: every 32×32 chunk is needed and off the diagonal.
+  __device__ __forceinline__ bool fast_tile(int ti, int tj) const {
+#if defined(K5_EXP)
+    return false;   // timing experiments run the general path
+#endif
+    return tri_T == 0 && !full && use_tma && tj > ti && (int64_t)(tj + 1) * 256 <= n;
+  }
+  template <int kSlot, class Ctx>
+  __device__ __forceinline__ void fast(Ctx& cx, int32_t row_lo, int32_t col0, const uint32_t (&r)[32],
+                                       const Pre& pf) const {
+    RF_DCHECK(col0 >= row_lo + 32 && (int64_t)col0 + 32 <= n, "fast chunk row_lo %d col0 %d n %lld", row_lo, col0,
+              (long long)n);
+    const RowCoef& c = pf.c;
+    float nj[32];
+    const uint32_t ca = cx.col_s + (uint32_t)(col0 & 255) * 4;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 t = ptx::lds128(ca + 16 * q);
+      nj[4 * q] = t.x; nj[4 * q + 1] = t.y; nj[4 * q + 2] = t.z; nj[4 * q + 3] = t.w;
+    }
+    float v[32];
+    if (kOdd) {
+      const float P = c.c * c.a1 * f0, Q = c.c * c.a1 * f1;
+      const uint64_t c2 = pk2(c.c, c.c), p2 = pk2(P, P), q2 = pk2(Q, Q);
+#pragma unroll
+      for (int e = 0; e < 32; e += 2)
+        eq1_pair_odd(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, p2, q2, v[e], v[e + 1]);
+    } else {
+      const uint64_t c2 = pk2(c.c, c.c), a0_2 = pk2(c.a0, c.a0), a1_2 = pk2(c.a1, c.a1), a2h_2 = pk2(c.a2h, c.a2h);
+      const uint64_t e0_2 = pk2(e0, e0), e1_2 = pk2(e1, e1), e2_2 = pk2(e2, e2), f0_2 = pk2(f0, f0), f1_2 = pk2(f1, f1);
+#pragma unroll
+      for (int e = 0; e < 32; e += 2)
+        eq1_pair<kOdd>(__uint_as_float(r[e]), __uint_as_float(r[e + 1]), nj[e], nj[e + 1], c2, a0_2, a1_2, a2h_2, e0_2,
+                       e1_2, e2_2, f0_2, f1_2, v[e], v[e + 1]);
+    }
+    cx.template store_static<kSlot>(row_lo, col0, v);
   }
   template <class Ctx>
   __device__ __forceinline__ void operator()(Ctx& cx, int64_t row_lo, int64_t col0, const uint32_t (&r)[32], int,
@@ -1305,6 +1396,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     cx.nst = 0;
     cx.pc0 = cx.pr0 = 0;
     cx.lane = lane;
+    cx.set_stg_x();
     cx.hint = sched.store_pol;
     cx.pol = ptx::policy_evict_first();
     const uint32_t tempty0 = ptx::mapa(ptx::smem_u32(&tempty[0]), leader);
@@ -1418,6 +1510,29 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (epi.chunk_needed(row_lo, col0)) epi(cx, row_lo, col0, cur, c, nchunks, (long long)t, pf);
         };
         ptx::tmem_ld_32x32b_x32(tbase, ra);
+        if constexpr (FastOf<Epi>::value && !Cfg::HALF_STG && (Cfg::STG_BUFS == 1 || Cfg::STG_BUFS == 2)) {
+          if (nchunks == 1 && epi.fast_tile(ti, tj)) {
+            // interior tile: the same pipeline with no per-chunk predicates; chunk cc → staging buffer cc & 1
+            const int32_t r32 = (int32_t)row_lo, c32 = (int32_t)colb;
+            auto fstep = [&](auto kslot, int cc, uint32_t(&cur)[32], uint32_t(&nxt)[32]) __attribute__((always_inline)) {
+              ptx::tmem_ld_wait();
+              if (cc + 1 < NCH) {
+                ptx::tmem_ld_32x32b_x32(tbase + (cc + 1) * 32, nxt);
+              } else {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + slot * 8);
+              }
+              epi.template fast<decltype(kslot)::value>(cx, r32, c32 + cc * 32, cur, pf);
+            };
+#pragma unroll 1
+            for (int cc = 0; cc < NCH; cc += 2) {
+              fstep(std::integral_constant<int, 0>{}, cc, ra, rb);
+              fstep(std::integral_constant<int, 1>{}, cc + 1, rb, ra);
+            }
+            continue;
+          }
+        }
 #pragma unroll 1
         for (int cc = 0; cc < NCH; cc += 2) {
           step(cc, ra, rb);

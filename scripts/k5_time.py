@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--out", default="upper")
     ap.add_argument("--act", default="tanh")
     ap.add_argument("--ares", type=int, default=0, help="context option k5_ares (A-panel residency)")
+    ap.add_argument("--clocks", action="store_true", help="sample SM clock / power / throttle reasons (nvidia-smi) "
+                    "over the timed launches (use --reps ≥ 200 so the 200-ms sampler sees them)")
     a = ap.parse_args()
     import torch
     import paper_2110_01899_b200 as rf
@@ -45,17 +47,23 @@ def main():
     torch.cuda.synchronize()
     rf.rf_profile_read()
     rf.rf_profile_enable(True)
+    sampler = None
+    if a.clocks:
+        import bench
+        sampler = bench.ClockSampler([0])
     for _ in range(a.reps):
         rf.rf_phi_closed_form(X, act=a.act, tau=tau, mom=mom, prec="bf16", out=a.out, Phi=Phi, ws=ws, **kw)
     torch.cuda.synchronize()
+    clk = sampler.stop() if sampler is not None else None
     ks = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
     ks.sort()
     med = ks[len(ks) // 2]
     tri = a.n * (a.n + 1) / 2.0
     by = 4.0 * tri + 2.0 * a.n * a.p
     print(json.dumps({"lib": os.environ.get("RF_B200_LIB", "in-tree"), "n": a.n, "p": a.p, "wide": a.wide, "ares": a.ares,
-                      "out": a.out, "k5_ms_median": med, "k5_ms_min": ks[0], "k5_ms_all": ks,
-                      "hbm_gbs": by / (med * 1e-3) / 1e9, "tflops": a.p * a.n * (a.n + 1.0) / (med * 1e-3) / 1e12}))
+                      "out": a.out, "k5_ms_median": med, "k5_ms_min": ks[0], "k5_ms_all": ks if len(ks) <= 10 else None,
+                      "hbm_gbs": by / (med * 1e-3) / 1e9, "tflops": a.p * a.n * (a.n + 1.0) / (med * 1e-3) / 1e12,
+                      "clocks": clk}))
 
 
 if __name__ == "__main__":
