@@ -150,7 +150,8 @@ typedef enum {
   RF_OPT_COMM_SMS = 11,    /* NCCL G5: SMs kept free of K4 for the overlapped reduce-scatter         default 8 */
   RF_OPT_VERBOSE = 12,     /* 1: print launch geometry to stderr                                     default 0 */
   RF_OPT_G5_PHASES = 13,   /* TEST HOOK, peers: which half of a collective rf_gram to enqueue — 1: K3 + K4 stores +
-                              arrival flags, 2: the arrival waits + owner-side sum + release flags, 3: both (default).
+                              arrival flags, 2: the arrival waits + owner-side sums + release flags (on the caller's
+                              stream), 3: the whole pipelined call (default).
                               Emulating R ranks on ONE GPU in one process: call phase 1 for every rank, then phase 2,
                               on one stream, so no stream-memory wait ever heads a queue its producer sits behind */
   RF_OPT_K4_DYNAMIC = 14,  /* 1: the K4 hybrid's two kernels pull 512 × 512 units of one raster from a shared device
@@ -184,7 +185,10 @@ rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);
  *     owner's staging buffer over NVLink as it finishes (the exchange overlaps the SYRK, no collective kernel), then
  *     device epoch flags (peer-mapped words written with system-scope release by a one-thread kernel, awaited with
  *     stream-memory waits) order the owner-side sum in rank order (deterministic) and the next call's stores —
- *     no host synchronization, no barrier.
+ *     no host synchronization, no barrier.  Chunk-pipelined: K4 counts each chunk's finished pair tiles; on the
+ *     context's comm stream chunk c's arrival flag goes to every owner as soon as its count is complete, and on the
+ *     context's reduce stream chunk c is summed as soon as every source's flag for it is up — beside K4, which is
+ *     still computing the later chunks (the caller's stream waits for both streams before the call's end).
  *   NCCL (the baseline): K4 writes a packed send buffer (in the workspace) chunk by chunk and bumps a per-chunk
  *     counter; on the context's communication stream each chunk's ncclReduceScatter waits (stream-memory wait) for
  *     its counter, so chunk c is reduced while K4 computes chunk c + 1.  K4 leaves RF_OPT_COMM_SMS SMs free.
@@ -424,6 +428,9 @@ int32_t rf_last_launch_count(void);
  * records taken (may exceed max_records; the excess is dropped) and clears the record list. */
 rf_status rf_profile_enable(int on);
 rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* count);
+/* rf_profile_timeline: as rf_profile_read, plus start_ms[k] = the launch's start relative to the first record's
+ * start (records on several streams — a collective's flag / sum kernels beside K4 — on one device time line). */
+rf_status rf_profile_timeline(int32_t max_records, char* names, float* start_ms, float* ms, int32_t* count);
 
 #ifdef __cplusplus
 }

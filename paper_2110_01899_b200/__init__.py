@@ -291,6 +291,20 @@ def rf_profile_read(max_records: int = 4096):
     return [(raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(k)]
 
 
+def rf_profile_timeline(max_records: int = 4096):
+    """[(kernel name, start ms relative to the first record, device ms)] of the launches recorded since the last
+    read (waits for them)."""
+    lib = load()
+    names = ctypes.create_string_buffer(32 * max_records)
+    t0 = (ctypes.c_float * max_records)()
+    ms = (ctypes.c_float * max_records)()
+    cnt = ctypes.c_int32()
+    _lib.check(lib.rf_profile_timeline(max_records, names, t0, ms, ctypes.byref(cnt)))
+    k = min(cnt.value, max_records)
+    raw = names.raw
+    return [(raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode(), float(t0[i]), float(ms[i])) for i in range(k)]
+
+
 # ------------------------------------------------------------------------------------------ compute calls
 def rf_estimate_tau(X, ws=None, stream=None, ctx=None) -> float:
     torch = _torch()

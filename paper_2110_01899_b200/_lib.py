@@ -32,7 +32,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
            "rf_ridge", "rf_round_bf16", "rf_ctx_create", "rf_ctx_destroy", "rf_ctx_set_option", "rf_ctx_get_option",
            "rf_tile_map", "rf_nccl_get_unique_id", "rf_ctx_init_nccl", "rf_ctx_attach_nccl", "rf_ctx_attach_peers",
            "rf_ctx_peer_handle", "rf_ctx_open_peers", "rf_ctx_peer_base", "rf_ctx_connect_peers", "rf_ctx_collective",
-           "rf_workspace_size", "rf_act_leaky_relu", "rf_act_quadratic")
+           "rf_workspace_size", "rf_act_leaky_relu", "rf_act_quadratic", "rf_profile_timeline")
 
 RF_PACK_TILE = 256
 RF_MAX_PEERS = 16
@@ -88,6 +88,8 @@ def load() -> ctypes.CDLL:
     lib.rf_debug_gemm_workspace_size.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.POINTER(sz)]
     lib.rf_debug_gemm_nt.argtypes = [vp, vp, i64, vp, i64, i64, i64, i64, ctypes.c_int, i32, vp, i64, vp, sz, vp]
     lib.rf_profile_read.argtypes = [i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
+    lib.rf_profile_timeline.argtypes = [i32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_float),
+                                        ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)]
     lib.rf_trf_thresholds.argtypes = [dbl, dbl, dbl, i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
     lib.rf_trf_thresholds_for.argtypes = [ctypes.c_int, dbl, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
     lib.rf_ter_features.argtypes = [vp, vp, i64, vp, i64, i64, i64, i64, dbl, dbl, dbl, vp, i64, vp]

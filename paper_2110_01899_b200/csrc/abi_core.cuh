@@ -28,6 +28,10 @@ rf_status rf_profile_enable(int on) {
 }
 
 rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* count) {
+  return rf_profile_timeline(max_records, names, nullptr, ms, count);
+}
+
+rf_status rf_profile_timeline(int32_t max_records, char* names, float* start_ms, float* ms, int32_t* count) {
   if (!count || (max_records > 0 && (!names || !ms))) return fail(RF_E_INVALID, "rf_profile_read: NULL output");
   std::vector<ProfRec> recs;
   {
@@ -44,6 +48,11 @@ rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* 
     if (k < max_records) {
       std::snprintf(names + 32 * k, 32, "%s", r.name);
       ms[k] = t;
+      if (start_ms) {
+        float t0 = 0.f;
+        if (e == cudaSuccess && cudaEventElapsedTime(&t0, recs[0].a, r.a) != cudaSuccess) t0 = 0.f;
+        start_ms[k] = t0;
+      }
     }
     ++k;
   }

@@ -110,14 +110,11 @@ rf_status nccl_fail(const char* what, int r) {
 }
 
 // ------------------------------------------------------------------------------- attach helpers
+rf_status create_g5_streams(rf_ctx* c, bool peers);
+
 rf_status attach_nccl_common(rf_ctx* c, int32_t rank, int32_t world) {
-  RF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
-  RF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
-  void* p = nullptr;
-  RF_CUDA_CHECK(cudaMalloc(&p, rfk::kMaxChunks * sizeof(uint32_t)));
-  RF_CUDA_CHECK(cudaMemset(p, 0, rfk::kMaxChunks * sizeof(uint32_t)));
-  c->sync = (uint32_t*)p;
+  rf_status s;
+  if ((s = create_g5_streams(c, false))) return s;
   c->rank = rank;
   c->world = world;
   c->mode = 1;
@@ -143,8 +140,42 @@ struct DeviceGuard {   // make `dev` current for a set-up call
   }
 };
 
+// The flags after the staging slots: arrived[chunk][source] (source's tiles of that chunk have landed here),
+// freed[source] (that owner has summed the previous call out of its staging buffer).  Values are call epochs.
+constexpr int kFlagWords = (rfk::kMaxChunks + 1) * RF_MAX_PEERS;
 uint32_t* flags_of(void* base, int world, int64_t recv_cap) {
-  return (uint32_t*)((char*)base + (size_t)world * recv_cap * 4);   // arrived[RF_MAX_PEERS], freed[RF_MAX_PEERS]
+  return (uint32_t*)((char*)base + (size_t)world * recv_cap * 4);
+}
+inline uint32_t* arrived_flag(uint32_t* flags, int chunk, int src) { return flags + chunk * RF_MAX_PEERS + src; }
+inline uint32_t* freed_flag(uint32_t* flags, int src) { return flags + rfk::kMaxChunks * RF_MAX_PEERS + src; }
+
+// Per-chunk counter targets of this call: each chunk's counter grows by kPackArrivals per K4 pair tile of the chunk;
+// the running sums (not epoch × tiles) stay right when n changes between calls on one context.
+void advance_sync_targets(rf_ctx* c, const G5Plan& pl, int64_t n, int bn) {
+  for (int k = 0; k < pl.C; ++k) c->sync_target[k] += (uint32_t)(kPackArrivals * chunk_pair_tiles(pl, k, n, bn));
+}
+
+rf_status create_g5_streams(rf_ctx* c, bool peers) {
+  RF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+  RF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  if (peers) {
+    // the per-chunk flags and sums run beside K4, whose CTAs take the SM's maximum shared-memory carveout: ask for
+    // the same carveout so the block scheduler can place them next to a K4 CTA (with the default preference the
+    // one-thread flag kernel waited for K4 to end, and every chunk's sum with it)
+    RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_pack_reduce, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+    RF_CUDA_CHECK(cudaFuncSetAttribute(rfk::k_signal, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+    RF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->red_stream, cudaStreamNonBlocking));
+    RF_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_sig, cudaEventDisableTiming));
+  }
+  void* p = nullptr;
+  RF_CUDA_CHECK(cudaMalloc(&p, rfk::kMaxChunks * sizeof(uint32_t)));
+  RF_CUDA_CHECK(cudaMemset(p, 0, rfk::kMaxChunks * sizeof(uint32_t)));
+  c->sync = (uint32_t*)p;
+  for (int k = 0; k < rfk::kMaxChunks; ++k) c->sync_target[k] = 0;
+  return RF_OK;
 }
 
 rf_status signal(const char* name, uint32_t* const* dst, int count, uint32_t value, cudaStream_t st) {
@@ -235,10 +266,10 @@ rf_status gram_collective(const void* X, int64_t ldx, const void* W, int64_t ldw
     if ((s = gram_tc_dispatch(ga, prec))) return s;
     launches = g_launches;
     RF_CUDA_CHECK(cudaStreamWaitEvent(c->comm_stream, c->ev_start, 0));
-    const int bn = prec == RF_PREC_3XTF32 ? 256 : 512;
+    advance_sync_targets(c, pl, n, prec == RF_PREC_3XTF32 ? 256 : 512);
+    (void)epoch;
     for (int k = 0; k < pl.C; ++k) {
-      const uint32_t target = (uint32_t)(kPackArrivals * chunk_pair_tiles(pl, k, n, bn)) * epoch;   // wrap-safe GEQ
-      if ((s = stream_wait_geq(c->comm_stream, c->sync + k, target))) return s;
+      if ((s = stream_wait_geq(c->comm_stream, c->sync + k, c->sync_target[k]))) return s;   // wrap-safe GEQ
       r = api.reduce_scatter(dv.send + pl.soff[k], recv + pl.roff[k], (size_t)pl.slots[k] * RF_PACK_TILE * RF_PACK_TILE,
                              kNcclFloat32, kNcclSum, c->comm, c->comm_stream);
       if (r != kNcclSuccess) return nccl_fail("ncclReduceScatter", r);
@@ -250,50 +281,78 @@ rf_status gram_collective(const void* X, int64_t ldx, const void* W, int64_t ldw
     return ok();
   }
 
-  // ---------------- PEERS: K4 stores into the owners' staging buffers; device epoch flags order the owner-side sum
+  // ---------------- PEERS: K4 stores into the owners' staging buffers; device epoch flags order the owner-side sum.
+  // Chunk-pipelined: K4 bumps the chunk counter after each pair tile's stores (system-scope fence first); on the
+  // comm stream, chunk c's arrival flag goes to every owner once its counter is complete; on the reduce stream, chunk
+  // c is summed once every source's flag for it is up.  Chunks complete in raster order, so the owner-side sum of
+  // chunk c runs beside K4's later chunks and only the last chunk's sum is left after K4.
   if (!c->connected) return fail(RF_E_INVALID, "rf_gram: peers attached but not connected (rf_ctx_open_peers)");
   if (pl.recv_elems > c->recv_cap)
     return fail(RF_E_INVALID, "rf_gram: n = %lld exceeds the n_max the peers were attached for", (long long)n);
   const int R = c->world, me = c->rank;
   uint32_t* mine = flags_of(c->stage, R, c->recv_cap);
   const int phases = (int)opt(RF_OPT_G5_PHASES);
+  const bool piped = phases == 3;   // both halves in one call: the sum runs on the reduce stream beside K4
   uint32_t* dst[RF_MAX_PEERS];
   if (phases & 1) {
     const uint32_t epoch = ++c->epoch;
     for (int o = 0; o < R; ++o)   // owner o has summed the previous call's tiles out of its staging buffer
-      if (o != me && (s = stream_wait_geq(st, mine + RF_MAX_PEERS + o, epoch - 1))) return s;
+      if (o != me && (s = stream_wait_geq(st, freed_flag(mine, o), epoch - 1))) return s;
+    RF_CUDA_CHECK(cudaEventRecord(c->ev_start, st));
     dv.p2p = 1;
-    dv.sync = nullptr;
+    dv.sync = c->sync;
     for (int o = 0; o < R; ++o) dv.peer[o] = c->peer[o];
     GramTcArgs ga{X, ldx, W, ldw, p, n, m_local, m_total, act, 0, nullptr, n, w, gp, usable_sms(dev.sms), st, &dv, 0};
     if ((s = gram_tc_dispatch(ga, prec))) return s;
     launches = g_launches;
-    for (int o = 0; o < R; ++o) dst[o] = c->peer_flags[o] + me;                       // arrived[me] at every owner
-    if ((s = signal("G5_signal_arrived", dst, R, epoch, st))) return s;
-    launches = g_launches;
+    advance_sync_targets(c, pl, n, 512);
+    RF_CUDA_CHECK(cudaStreamWaitEvent(c->comm_stream, c->ev_start, 0));
+    for (int k = 0; k < pl.C; ++k) {   // chunk k's stores have landed (fenced) → arrived[k][me] at every owner
+      if ((s = stream_wait_geq(c->comm_stream, c->sync + k, c->sync_target[k]))) return s;
+      for (int o = 0; o < R; ++o) dst[o] = arrived_flag(c->peer_flags[o], k, me);
+      g_launches = 0;
+      if ((s = signal("G5_signal_arrived", dst, R, epoch, c->comm_stream))) return s;
+      launches += g_launches;
+    }
+    RF_CUDA_CHECK(cudaEventRecord(c->ev_sig, c->comm_stream));
+    if (!piped) RF_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_sig, 0));
   }
   if (!(phases & 2)) {
     g_launches = launches;
     return ok();
   }
-  g_launches = 0;
   const uint32_t epoch = c->epoch;
-  for (int q = 0; q < R; ++q)   // every source's tiles have landed in my staging buffer
-    if ((s = stream_wait_geq(st, mine + q, epoch))) return s;
-  {
-    const int64_t recv4 = pl.recv_elems / 4;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((recv4 + 255) / 256, (int64_t)dev.sms * 8));
-    ProfScope ps("G5_pack_reduce", st);
-    rfk::k_pack_reduce<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(c->stage), recv4, R,
+  cudaStream_t rs = st;
+  if (piped) {   // after st's earlier work (readers of recv), not after K4
+    rs = c->red_stream;
+    RF_CUDA_CHECK(cudaStreamWaitEvent(rs, c->ev_start, 0));
+  }
+  const int64_t stride4 = pl.recv_elems / 4;
+  for (int k = 0; k < pl.C; ++k) {
+    for (int q = 0; q < R; ++q)   // every source's tiles of chunk k have landed in my staging buffer
+      if ((s = stream_wait_geq(rs, arrived_flag(mine, k, q), epoch))) return s;
+    const int64_t off4 = pl.roff[k] / 4, cnt4 = (pl.roff[k + 1] - pl.roff[k]) / 4;
+    if (cnt4 <= 0) continue;
+    constexpr int kT = rfk::kReduceThreads;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cnt4 + kT - 1) / kT, (int64_t)dev.sms * 8));
+    ProfScope ps("G5_pack_reduce", rs);
+    rfk::k_pack_reduce<<<grid, kT, 0, rs>>>(reinterpret_cast<const float4*>(c->stage), stride4, off4, cnt4, R,
                                               reinterpret_cast<float4*>(recv));
     RF_CUDA_CHECK(cudaGetLastError());
-    ++g_launches;
+    ++launches;
   }
   int k = 0;
   for (int q = 0; q < R; ++q)
-    if (q != me) dst[k++] = c->peer_flags[q] + RF_MAX_PEERS + me;                     // freed[me] at every source
-  if ((s = signal("G5_signal_freed", dst, k, epoch, st))) return s;
-  g_launches += launches;
+    if (q != me) dst[k++] = freed_flag(c->peer_flags[q], me);                        // freed[me] at every source
+  g_launches = 0;
+  if ((s = signal("G5_signal_freed", dst, k, epoch, rs))) return s;
+  launches += g_launches;
+  if (piped) {
+    RF_CUDA_CHECK(cudaEventRecord(c->ev_done, rs));
+    RF_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_done, 0));
+    RF_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_sig, 0));
+  }
+  g_launches = launches;
   return ok();
 }
 
@@ -323,6 +382,8 @@ void rf_ctx_destroy(rf_ctx* c) {
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->ev_sig) cudaEventDestroy(c->ev_sig);
+  if (c->red_stream) cudaStreamDestroy(c->red_stream);
   if (c->sync) cudaFree(c->sync);
   for (int r = 0; r < RF_MAX_PEERS; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->opened[r]);
@@ -448,11 +509,12 @@ rf_status rf_ctx_attach_peers(rf_ctx* c, int32_t rank, int32_t world, int64_t n_
   DeviceGuard dg(c->device);
   // room for the receive slots of any n ≤ n_max (padding differs by at most one slot per chunk and owner)
   c->recv_cap = pl.recv_elems + (int64_t)rfk::kMaxChunks * RF_PACK_TILE * RF_PACK_TILE;
-  c->stage_bytes = (size_t)world * c->recv_cap * 4 + 2 * RF_MAX_PEERS * sizeof(uint32_t);
+  c->stage_bytes = (size_t)world * c->recv_cap * 4 + kFlagWords * sizeof(uint32_t);
   void* p = nullptr;
   RF_CUDA_CHECK(cudaMalloc(&p, c->stage_bytes));   // its own allocation: the IPC handle names exactly this buffer
   RF_CUDA_CHECK(cudaMemset(p, 0, c->stage_bytes));
   c->stage = p;
+  if ((s = create_g5_streams(c, true))) return s;
   c->rank = rank;
   c->world = world;
   c->mode = 2;

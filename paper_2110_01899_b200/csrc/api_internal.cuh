@@ -36,10 +36,15 @@ struct rf_ctx {
   void* comm = nullptr;
   bool own_comm = false;
   cudaStream_t comm_stream = nullptr;
-  uint32_t* sync = nullptr;               // device: per-chunk counters (monotone across calls)
-  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
+  uint32_t* sync = nullptr;               // device: per-chunk counters of finished K4 (pair tile, epilogue warp)s,
+                                          // monotone across calls (NCCL and peers)
+  uint32_t sync_target[rfk::kMaxChunks] = {};   // host: the counter values the calls so far reach (wrap-safe GEQ)
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_sig = nullptr;
   bool comm_pending = false;              // ev_done recorded by an earlier call (its reduce-scatters read the send buffer)
-  // peers: [world × recv_cap floats][flags: arrived[RF_MAX_PEERS], freed[RF_MAX_PEERS]] in one cudaMalloc
+  // peers: comm_stream sends chunk c's arrival flags once the chunk counter says its stores are done; red_stream sums
+  // chunk c once every source's flag for it is up — both overlap the rest of K4
+  cudaStream_t red_stream = nullptr;
+  // peers: [world × recv_cap floats][flags: arrived[kMaxChunks][RF_MAX_PEERS], freed[RF_MAX_PEERS]] in one cudaMalloc
   void* stage = nullptr;
   size_t stage_bytes = 0;
   int64_t recv_cap = 0;

@@ -6,8 +6,10 @@
   stream-memory waits order the owner-side sums and the next call's stores.  On one GPU in one process the ranks'
   streams may share a hardware queue, so a wait could head a queue its producer sits behind: the emulation enqueues
   each call in its two halves (RF_OPT_G5_PHASES test hook: phase 1 of every rank, then phase 2 of every rank) on one
-  stream, where every wait's producer is already ahead of it.  No kernel ever waits on another.  Three calls in a row
-  (epochs 1..3) are bit-identical, and the summed owned tiles match the fp64 oracle G of the full W.
+  stream, where every wait's producer is already ahead of it; or (piped) each call has one rank t run the whole
+  pipelined call — per-chunk arrival flags and per-chunk owner-side sums on its context's comm / reduce streams beside
+  its K4 — after the others' first halves.  No kernel ever waits on another.  Three calls in a row (epochs 1..3) are
+  bit-identical, and the summed owned tiles match the fp64 oracle G of the full W.
 * world 1, peers and NCCL (the library's own communicator from rf_nccl_get_unique_id): the packed tiles equal the
   dense K4 bit for bit, in BF16, TF32 and (NCCL) 3×TF32, and the NCCL chunk counters K4 publishes reach their
   per-epoch targets.
@@ -38,7 +40,7 @@ def _gpu():
     yield
 
 
-def _emulated(n, p, m, world, prec, act, calls=3, seed=0):
+def _emulated(n, p, m, world, prec, act, calls=3, seed=0, piped=False):
     rng = np.random.default_rng(seed + n + world)
     Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(DT[prec])
     Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(DT[prec])
@@ -53,11 +55,30 @@ def _emulated(n, p, m, world, prec, act, calls=3, seed=0):
              for r in range(world)]
     torch.cuda.synchronize()
     outs = []
-    for _ in range(calls):
-        for phase in (1, 2):         # no host synchronization between the halves or between calls
+
+    def go(r, phase):
+        ctxs[r].set_option("g5_phases", phase)
+        rf.rf_gram(Xd, shards[r], act=act, prec=prec, out="packed_tiles", m_total=m, G=recvs[r], ctx=ctxs[r])
+
+    for call in range(calls):
+        if not piped:
+            for phase in (1, 2):     # no host synchronization between the halves or between calls
+                for r in range(world):
+                    go(r, phase)
+        else:
+            # rank t arrives last and runs the whole pipelined call (phases 3: its per-chunk arrival flags and
+            # owner-side sums on the context's comm / reduce streams beside its K4); the others run their halves
+            # around it, each half after the previous has finished (one GPU: no wait may head its producer's queue)
+            t = call % world
             for r in range(world):
-                ctxs[r].set_option("g5_phases", phase)
-                rf.rf_gram(Xd, shards[r], act=act, prec=prec, out="packed_tiles", m_total=m, G=recvs[r], ctx=ctxs[r])
+                if r != t:
+                    go(r, 1)
+                    torch.cuda.synchronize()
+            go(t, 3)
+            torch.cuda.synchronize()
+            for r in range(world):
+                if r != t:
+                    go(r, 2)
         torch.cuda.synchronize()
         outs.append([x.cpu().numpy().copy() for x in recvs])
     for c in ctxs:
@@ -65,14 +86,16 @@ def _emulated(n, p, m, world, prec, act, calls=3, seed=0):
     return Xd, Wd, outs
 
 
-@pytest.mark.parametrize("n,p,m,world,prec,act", [
-    (600, 64, 384, 2, "bf16", "tanh"),         # ragged n (not a multiple of 256 / 512)
-    (1024, 96, 512, 3, "bf16", "erf"),         # tile multiple, world not a power of two
-    (2100, 128, 640, 4, "tf32", "sigmoid_half"),
-    (17000, 64, 256, 2, "bf16", "sigmoid_half"),   # ≥ 64 row tiles: K4's multicast + pair hybrid with packed tiles
+@pytest.mark.parametrize("n,p,m,world,prec,act,piped", [
+    (600, 64, 384, 2, "bf16", "tanh", False),         # ragged n (not a multiple of 256 / 512)
+    (1024, 96, 512, 3, "bf16", "erf", False),         # tile multiple, world not a power of two
+    (2100, 128, 640, 4, "tf32", "sigmoid_half", False),
+    (17000, 64, 256, 2, "bf16", "sigmoid_half", False),   # ≥ 64 row tiles: K4's multicast + pair hybrid, packed tiles
+    (1024, 96, 512, 3, "bf16", "erf", True),          # the pipelined call (per-chunk flags and sums), each rank last
+    (17000, 64, 256, 3, "bf16", "sigmoid_half", True),    # … with the hybrid K4 and all 16 chunks
 ])
-def test_peer_exchange_emulated_ranks(n, p, m, world, prec, act):
-    Xd, Wd, outs = _emulated(n, p, m, world, prec, act)
+def test_peer_exchange_emulated_ranks(n, p, m, world, prec, act, piped):
+    Xd, Wd, outs = _emulated(n, p, m, world, prec, act, piped=piped)
     for k in range(1, len(outs)):
         for r in range(world):
             assert np.array_equal(outs[k][r], outs[0][r]), f"call {k + 1} differs from call 1 on rank {r}"
@@ -138,6 +161,47 @@ def test_nccl_world1_equals_dense(prec):
     ctx.init_nccl(rf.rf_nccl_get_unique_id(), 0, 1)
     assert ctx.collective() == (0, 1, 1)
     _dense_vs_packed(ctx, 1300, 96, 768, prec, "sigmoid_half", calls=3)
+    ctx.destroy()
+
+
+@pytest.mark.parametrize("mode", ["peers", "nccl"])
+def test_world1_n_changes_between_calls(mode):
+    """The per-chunk counter targets are running sums over the calls (not epoch × this call's tiles), so n may change
+    between collective calls on one context."""
+    ctx = rf.Context(0)
+    if mode == "peers":
+        ctx.attach_peers(0, 1, 1500)
+    else:
+        ctx.init_nccl(rf.rf_nccl_get_unique_id(), 0, 1)
+    for n in (1500, 700, 1300):
+        _dense_vs_packed(ctx, n, 96, 512, "bf16", "tanh", calls=2)
+    ctx.destroy()
+
+
+def test_peers_world1_on_side_stream():
+    """The pipelined call on a non-current stream: its comm / reduce streams order after the caller's stream, and the
+    caller's stream after them (recv complete on `stream`)."""
+    n, p, m = 1400, 64, 512
+    rng = np.random.default_rng(11)
+    Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(torch.bfloat16)
+    Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(torch.bfloat16)
+    ctx = rf.Context(0)
+    ctx.attach_peers(0, 1, n)
+    side = torch.cuda.Stream()
+    recv = torch.full((len(rf.rf_tile_map(n, 1, 0)) * collective.TILE_ELEMS,), float("nan"), device="cuda")
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            rf.rf_gram(Xd, Wd, act="erf", out="packed_tiles", G=recv, stream=side, ctx=ctx)
+        got_s = recv.clone()
+    torch.cuda.current_stream().wait_stream(side)
+    G = rf.rf_gram(Xd, Wd, act="erf", out="upper", ctx=ctx)
+    torch.cuda.synchronize()
+    got = np.full((n, n), np.nan, dtype=np.float32)
+    w = collective.scatter_owned(got_s.cpu().numpy(), rf.rf_tile_map(n, 1, 0), n, got)
+    I, J = np.triu_indices(n)
+    assert w[I, J].all()
+    assert np.array_equal(got[I, J], G.cpu().numpy()[I, J])
     ctx.destroy()
 
 
