@@ -819,16 +819,22 @@ struct EpiSyrkPacked {
     float* tile = pk.p2p ? pk.peer[owner] + (int64_t)pk.self * pk.recv_elems + pk.roff[c] +
                                slot * (int64_t)(RF_PACK_TILE * RF_PACK_TILE)
                          : pk.send + pk.soff[c] + (owner * pk.slots[c] + slot) * (int64_t)(RF_PACK_TILE * RF_PACK_TILE);
-    float* dst = tile + ((row_lo & 255) + cx.lane) * RF_PACK_TILE + (col0 & 255);
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]) * scale;
+    // Whole 32-B sectors: four 256-bit stores per lane (its row's 128 B), so over NVLink (the peer path) every store
+    // carries full sectors rather than 16-B halves, and the warp issues half the store instructions.  (Staging the
+    // block through shared memory for whole 128-B lines made the K4 epilogue slower beside the co-resident G5 sums:
+    // R = 8 emulation 31.2 vs 29.4 ms per call.)
+    float* dst = tile + ((row_lo & 255) + cx.lane) * RF_PACK_TILE + (col0 & 255);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    for (int q = 0; q < 4; ++q)
+      ptx::stg256(dst + 8 * q, v[8 * q], v[8 * q + 1], v[8 * q + 2], v[8 * q + 3], v[8 * q + 4], v[8 * q + 5],
+                  v[8 * q + 6], v[8 * q + 7]);
   }
-  // NCCL: after the warp's last store of a pair tile in row tile ti, publish it to the chunk counter (system-scope
-  // fence, one atomic per epilogue warp: the library waits for 2 · EPI_WARPS · (pair tiles of the chunk)).
+  // After the warp's last store of a pair tile in row tile ti, publish it to the chunk counter (system-scope fence,
+  // one atomic per epilogue warp: the library waits for 2 · EPI_WARPS · (pair tiles of the chunk) — NCCL: before the
+  // chunk's reduce-scatter; peers: before the chunk's arrival flags).
   __device__ __forceinline__ void tile_done(int ti, uint32_t lane) const {
     if (!pk.sync) return;
     __syncwarp();
