@@ -143,7 +143,7 @@ typedef enum {
   RF_OPT_K3_SPLIT_R100 = 4,/* K3 hybrid work split, as above                                        default 120 */
   RF_OPT_LOCK_W = 5,       /* K4 soft lockstep: allowed lead in K-blocks (0 = off)                  default 24 */
   RF_OPT_LOCK_KS = 6,      /* K4 soft lockstep: check period in K-blocks                            default 8 */
-  RF_OPT_K5_WIDE = 7,      /* K5 epilogue warps: −1 auto (16 for p ≤ 512, else 8), 0 → 8, 1 → 16     default −1 */
+  RF_OPT_K5_WIDE = 7,      /* K5 epilogue warps: −1 auto (8), 0 → 8, 1 → 16                          default −1 */
   RF_OPT_EQ1_GENERAL = 8,  /* 1: the general EQ1 epilogue also for odd σ (A0, A2 kept)               default 0 */
   RF_OPT_KCHUNK = 9,       /* 3×TF32 K4 accumulation chunk in K-blocks (0 = whole K)                default 4 */
   RF_OPT_MAX_SMS = 10,     /* ≤ 0: all SMs; else the tensor-core kernels use at most this many       default 0 */

@@ -915,7 +915,10 @@ rf_status launch_k5(const K5Args& a) {
     // epilogue warps (four per TMEM lane quarter; one 4-KB staging buffer each, which keeps five operand stages;
     // 96 registers) help: configs[4] 11.3 → 9.54 ms (12 warps: 9.94).  Long K: the MMA sets it and the 8-warp
     // kernel stays ahead (configs[3] shape, p = 1024: 3.63 vs 3.78 ms).  DESIGN.md §7.
-    const bool wide = opt(RF_OPT_K5_WIDE) < 0 ? p <= 512 : opt(RF_OPT_K5_WIDE) != 0;
+    // Since the 8-warp kernel got its interior fast path (round 2) it is ahead at every p measured (configs[4]
+    // without residency: bf16 11.1 vs 13.2 ms, TF32 16.7 vs 17.3 ms; profiles/r02/k5_fast/k5_wide_vs_8.log), so
+    // auto (−1) means 8 warps; 1 keeps the 16-warp kernel as an option.
+    const bool wide = opt(RF_OPT_K5_WIDE) > 0;
     // A-panel residency: K = p of 5 … 8 K-blocks (the producer may run at most STAGES = 4 K-blocks ahead of the MMA,
     // which keeps the aempty parity wait exact, tc_gemm.cuh)
     const int kb5 = (int)((p + 63) / 64);

@@ -21,7 +21,9 @@ def main():
     ap.add_argument("--wide", type=int, default=-1)
     ap.add_argument("--out", default="upper")
     ap.add_argument("--act", default="tanh")
-    ap.add_argument("--ares", type=int, default=0, help="context option k5_ares (A-panel residency)")
+    ap.add_argument("--ares", type=int, default=None, help="context option k5_ares (A-panel residency; default: the "
+                    "library's)")
+    ap.add_argument("--prec", default="bf16", choices=["bf16", "tf32"])
     ap.add_argument("--clocks", action="store_true", help="sample SM clock / power / throttle reasons (nvidia-smi) "
                     "over the timed launches (use --reps ≥ 200 so the 200-ms sampler sees them)")
     a = ap.parse_args()
@@ -30,20 +32,21 @@ def main():
     import synthetic
     dev = torch.device("cuda:0")
     cfg = synthetic.CONFIGS[4]
-    X = torch.from_numpy(synthetic.make_X(cfg, n=a.n, p=a.p)).to(torch.bfloat16).to(dev)
+    X = torch.from_numpy(synthetic.make_X(cfg, n=a.n, p=a.p)).to(torch.bfloat16 if a.prec == "bf16" else torch.float32)
+    X = X.to(dev)
     ctx = rf.Context(0) if hasattr(rf, "Context") else None
     if ctx is not None:
         ctx.set_option("k5_wide", a.wide)
-        if a.ares:
+        if a.ares is not None:
             ctx.set_option("k5_ares", a.ares)
     Phi = (torch.empty(rf.rf_packed_tri_elems(a.n), device=dev) if a.out == "packed_tri"
            else torch.empty(a.n, a.n, device=dev))
-    ws = torch.empty(rf.rf_phi_workspace_size(a.p, a.n, "bf16"), dtype=torch.uint8, device=dev)
+    ws = torch.empty(rf.rf_phi_workspace_size(a.p, a.n, a.prec), dtype=torch.uint8, device=dev)
     tau = rf.rf_estimate_tau(X)
     mom = rf.rf_moments(a.act, tau)
     kw = {"ctx": ctx} if ctx is not None else {}
     for _ in range(2):
-        rf.rf_phi_closed_form(X, act=a.act, tau=tau, mom=mom, prec="bf16", out=a.out, Phi=Phi, ws=ws, **kw)
+        rf.rf_phi_closed_form(X, act=a.act, tau=tau, mom=mom, prec=a.prec, out=a.out, Phi=Phi, ws=ws, **kw)
     torch.cuda.synchronize()
     rf.rf_profile_read()
     rf.rf_profile_enable(True)
@@ -52,7 +55,7 @@ def main():
         import bench
         sampler = bench.ClockSampler([0])
     for _ in range(a.reps):
-        rf.rf_phi_closed_form(X, act=a.act, tau=tau, mom=mom, prec="bf16", out=a.out, Phi=Phi, ws=ws, **kw)
+        rf.rf_phi_closed_form(X, act=a.act, tau=tau, mom=mom, prec=a.prec, out=a.out, Phi=Phi, ws=ws, **kw)
     torch.cuda.synchronize()
     clk = sampler.stop() if sampler is not None else None
     ks = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
@@ -60,7 +63,7 @@ def main():
     med = ks[len(ks) // 2]
     tri = a.n * (a.n + 1) / 2.0
     by = 4.0 * tri + 2.0 * a.n * a.p
-    print(json.dumps({"lib": os.environ.get("RF_B200_LIB", "in-tree"), "n": a.n, "p": a.p, "wide": a.wide, "ares": a.ares,
+    print(json.dumps({"lib": os.environ.get("RF_B200_LIB", "in-tree"), "n": a.n, "p": a.p, "wide": a.wide, "ares": a.ares, "prec": a.prec,
                       "out": a.out, "k5_ms_median": med, "k5_ms_min": ks[0], "k5_ms_all": ks if len(ks) <= 10 else None,
                       "hbm_gbs": by / (med * 1e-3) / 1e9, "tflops": a.p * a.n * (a.n + 1.0) / (med * 1e-3) / 1e12,
                       "clocks": clk}))
