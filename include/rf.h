@@ -158,7 +158,9 @@ typedef enum {
                               counter (no static split); 0: the static split of RF_OPT_K4_SPLIT_R100     default 1 */
   RF_OPT_K5_ARES = 15,     /* K5 with A-panel residency (bf16, 256 < p ≤ 512): 0 off, 1 with 8, 2 with 16 (2-KB
                               staging), 3 with 12 epilogue warps                                      default 1 */
-  RF_OPT_COUNT = 16
+  RF_OPT_K5_DYNAMIC = 16,  /* 1: the A-resident K5 pulls its segments from a device counter (balanced last wave);
+                              0: static round-robin                                                   default 1 */
+  RF_OPT_COUNT = 17
 } rf_opt;
 rf_status rf_ctx_set_option(rf_ctx* ctx, rf_opt opt, int64_t value);
 rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);

@@ -405,7 +405,7 @@ rf_status rf_ctx_set_option(rf_ctx* c, rf_opt o, int64_t v) {
     case RF_OPT_K5_WIDE: okv = v >= -1 && v <= 1; break;
     case RF_OPT_COMM_SMS: okv = v >= 0 && v <= 64; break;
     case RF_OPT_G5_PHASES: okv = v >= 1 && v <= 3; break;
-    case RF_OPT_K4_DYNAMIC: okv = v == 0 || v == 1; break;
+    case RF_OPT_K4_DYNAMIC: case RF_OPT_K5_DYNAMIC: okv = v == 0 || v == 1; break;
     case RF_OPT_K5_ARES: okv = v >= 0 && v <= 3; break;
     default: break;
   }

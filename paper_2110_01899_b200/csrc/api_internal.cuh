@@ -278,7 +278,7 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
 }
 
 // ---------------------------------------------------------------- context and options (include/rf.h)
-constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1, 1};
+constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1, 1, 1};
 thread_local rf_ctx* g_ctx = nullptr;     // the context of the call in progress on this thread
 int64_t opt(rf_opt o) { return g_ctx ? g_ctx->opts[o] : kOptDefault[o]; }
 
@@ -495,7 +495,7 @@ GramPlan gram_plan(int64_t p, int64_t n, int64_t m_local, rf_prec prec) {
 
 struct PhiPlan {
   int64_t ldp;
-  size_t off_nrm2, off_tau, off_rc, off_nrm2o, off_xhi, off_xlo, off_cen, total;
+  size_t off_nrm2, off_tau, off_rc, off_nrm2o, off_xhi, off_xlo, off_cen, off_queue, total;
 };
 PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
   PhiPlan g{};
@@ -510,6 +510,7 @@ PhiPlan phi_plan(int64_t p, int64_t n, rf_prec prec) {
     g.off_xlo = off; off = align256(off + (size_t)n * g.ldp * 4);
   }
   g.off_cen = off; off = align256(off + (size_t)(n + 2) * 8);
+  g.off_queue = off; off = align256(off + 4);   // K5's dynamic segment counter (A residency)
   g.total = off;
   return g;
 }
@@ -873,16 +874,23 @@ rf_status k5_go(const CUtensorMap& tA, const CUtensorMap& tAl, const CUtensorMap
   return launch_tc<C>("K5_xtx_eq1", tA, tA, tAl, tAl, tO, sc, e, sms, st);
 }
 
-// K5 with A-panel residency (TcCfg kAres): segment schedule, column blocks of kSegLen tiles (tc_gemm.cuh Sched).
+// K5 with A-panel residency (TcCfg kAres): segment schedule, column blocks of kSegLen tiles (tc_gemm.cuh Sched),
+// segments pulled from a device counter in schedule order (TileSeq's unit ring): a segment holds up to 16 tiles
+// (≈ 60 µs at configs[4]), so a static round-robin could leave a cluster one segment behind in the last wave —
+// ≈ 5 % of a rank's launch at R = 8.
 constexpr int kSegLen = 16;
 template <class C, class E>
 rf_status k5_go_ares(const CUtensorMap& tA, const CUtensorMap& tO, const E& e, int64_t p, int rt0, int rt1, int tn,
-                     int sms, cudaStream_t st) {
+                     uint32_t* queue, int sms, cudaStream_t st) {
   rfk::Sched sc = rfk::Sched::make(1, 256, rt0, rt1, tn, (int)((p + C::BK - 1) / C::BK), 0, 1);
   sc.seg_len = kSegLen;
   sc.num_tiles = (int)sc.seg_prefix((tn + kSegLen - 1) / kSegLen);
   sc.load_pol = 1;
   sc.store_pol = 1;
+  if (queue && opt(RF_OPT_K5_DYNAMIC)) {
+    RF_CUDA_CHECK(cudaMemsetAsync(queue, 0, 4, st));
+    sc.queue = queue;
+  }
   return launch_tc<C>("K5_xtx_eq1", tA, tA, tA, tA, tO, sc, e, sms, st);
 }
 
@@ -924,15 +932,16 @@ rf_status launch_k5(const K5Args& a) {
     const int kb5 = (int)((p + 63) / 64);
     const int ares = (int)opt(RF_OPT_K5_ARES);
     if (bf && ares > 0 && kb5 > 4 && kb5 <= 8) {
+      uint32_t* q5 = (uint32_t*)(w + a.pl.off_queue);
       if (ares == 2) {   // 2-KB staging buffers: the store map with 16 × 32 boxes and 64-B swizzle
         CUtensorMap tOh;
         const bool okh = a.tri_T > 0 ? make_tmap_out(&tOh, Phi, tri_tiles(n) * 256, 256, 256, true)
                                      : make_tmap_out(&tOh, Phi, n, n, ldphi, true);
         if (!okh) tOh = tA;
-        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 16, 1>>(tA, tOh, e, p, rt0, rt1, tn, dev.sms, st))) return s;
+        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 16, 1>>(tA, tOh, e, p, rt0, rt1, tn, q5, dev.sms, st))) return s;
       } else if (ares == 3) {
-        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 12, 1>>(tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) return s;
-      } else if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 8, 1>>(tA, tO, e, p, rt0, rt1, tn, dev.sms, st))) {
+        if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 12, 1>>(tA, tO, e, p, rt0, rt1, tn, q5, dev.sms, st))) return s;
+      } else if ((s = k5_go_ares<rfk::TcCfg<1, 1, 256, 1, 2, 8, 1>>(tA, tO, e, p, rt0, rt1, tn, q5, dev.sms, st))) {
         return s;
       }
     } else if (bf && wide) {

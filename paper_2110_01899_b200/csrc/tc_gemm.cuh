@@ -370,18 +370,25 @@ struct TileSeq {
     return v == 0xFFFFFFFFu ? -1 : (long long)v;
   }
   // next tile of this role: (schedule index / unit, row tile, column tile) with the cluster's CTA placement applied.
-  // kDyn = false (every kernel but the K4 hybrid's): the static walk only, so the ring state costs no registers.
+  // kDyn = false (every kernel but the K4 hybrid's and the A-resident K5): the static walk only, so the ring state
+  // costs no registers.
   template <bool kDyn, bool kSeg = false>
   __device__ __forceinline__ bool next(long long& tt, int& ti, int& tj) {
     if (kSeg) {               // segment schedule (A residency configurations only)
       seg_first = false;
       if (sJ >= sJ1) {
-        if (t >= s->num_tiles) return false;
-        s->seg_get(t, sI, sJ, sJ1);
-        t += ncl;
+        if (kDyn && dyn) {    // dynamic: the next segment from the shared counter (keeps the last wave balanced)
+          u = fetch();
+          if (u < 0) return false;
+        } else {
+          if (t >= s->num_tiles) return false;
+          u = t;
+          t += ncl;
+        }
+        s->seg_get(u, sI, sJ, sJ1);
         seg_first = true;
       }
-      tt = t - ncl;
+      tt = u;
       ti = sI;
       tj = sJ++;
       return true;
@@ -1156,10 +1163,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       ptx::mbar_init(&colfull[a], 1);
       ptx::mbar_init(&colempty[a], Cfg::EPI_WARPS);
     }
-    // ring consumers per cluster: the other CTAs' producers, one MMA warp per pair, every epilogue warp
+    // ring consumers per cluster: the other CTAs' producers, one MMA warp per pair, every epilogue warp (and, with
+    // a column vector, every CTA's column loader)
     for (int a = 0; a < kRing; ++a) {
       ptx::mbar_init(&rfull[a], 1);
-      ptx::mbar_init(&rempty[a], (Cfg::CL - 1) + Cfg::CL / 2 + Cfg::CL * Cfg::EPI_WARPS);
+      ptx::mbar_init(&rempty[a], (Cfg::CL - 1) + Cfg::CL / 2 + Cfg::CL * Cfg::EPI_WARPS + (kCol ? Cfg::CL : 0));
     }
     ptx::mbar_init(afull, 1);
     ptx::mbar_init(aempty, 1);
@@ -1180,8 +1188,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 #endif
   const int kchunk = sched.kchunk, nchunks = sched.nchunks, num_kb = sched.num_kb;
-  // dynamic units only for the K4 hybrid's configurations (512-wide pair tiles); the host never sets sched.queue else
-  constexpr bool kDyn = Cfg::BN == 512 && Cfg::CL <= 4 && !kCol;
+  // dynamic units only for the K4 hybrid's configurations (512-wide pair tiles) and the A-resident K5 (segments);
+  // the host never sets sched.queue else
+  constexpr bool kDyn = (Cfg::BN == 512 && Cfg::CL <= 4 && !kCol) || Cfg::ARES;
   const uint32_t ring_s = ptx::smem_u32(ring), rfull_s = ptx::smem_u32(&rfull[0]), rempty_s = ptx::smem_u32(&rempty[0]);
   const uint32_t rempty_c = ptx::mapa(rempty_s, 0);   // the fetcher's (cluster rank 0) ring_empty
   auto make_seq = [&](bool fetcher) {
@@ -1376,10 +1385,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // ===== Column-vector loader: tile k's slice of the per-column vector into sCol[k & 1] once the epilogue has
       // released the buffer (tile k − 2), a 1-D bulk copy completing on colfull.  A warp of its own, so the operand
       // producer never waits on the epilogue.
-      TileSeq seq = make_seq(false);   // static or segment schedules only (kColVec never runs the unit queue)
+      TileSeq seq = make_seq(false);   // static, segment or dynamic-segment schedules
       long long t;
       int ti, tj;
-      for (int tcount = 0; seq.template next<false, Cfg::ARES>(t, ti, tj); ++tcount) {
+      for (int tcount = 0; seq.template next<kDyn, Cfg::ARES>(t, ti, tj); ++tcount) {
         if (lane == 0) {
           const int cs = tcount & 1;
           ptx::mbar_wait(&colempty[cs], ((tcount >> 1) & 1) ^ 1);

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--ares", type=int, default=None, help="context option k5_ares (default: the library's)")
+    ap.add_argument("--dyn", type=int, default=None, help="context option k5_dynamic (default: the library's)")
     a = ap.parse_args()
     import torch
     import paper_2110_01899_b200 as rf
@@ -37,6 +38,8 @@ def main():
     ctx = rf.Context(0)
     if a.ares is not None:
         ctx.set_option("k5_ares", a.ares)
+    if a.dyn is not None:
+        ctx.set_option("k5_dynamic", a.dyn)
 
     def run(rb, re_):
         rf.rf_phi_closed_form(X, act=cfg.act, tau=tau, mom=mom, prec="bf16", out="upper", row_begin=rb, row_end=re_,
@@ -68,7 +71,7 @@ def main():
             row["speedup"] = base / row["step_ms"]
             row["efficiency"] = row["speedup"] / row["R"]
         print(json.dumps({k: v for k, v in row.items() if k != "rows"}), flush=True)
-    print(json.dumps({"config": 4, "n": n, "p": p, "k5_ares": a.ares, "rows": rows}))
+    print(json.dumps({"config": 4, "n": n, "p": p, "k5_ares": a.ares, "k5_dynamic": a.dyn, "rows": rows}))
 
 
 if __name__ == "__main__":

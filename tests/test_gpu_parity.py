@@ -423,16 +423,18 @@ def test_non_current_stream_orders_allocations_and_results():
         assert torch.equal(Phi, Pref)
 
 
-@pytest.mark.parametrize("ares", [1, 2])
+@pytest.mark.parametrize("ares,dyn", [(1, 1), (1, 0), (2, 1)])
 @pytest.mark.parametrize("out,rows", [("upper", None), ("full", None), ("packed_tri", None), ("upper", (512, 1536))])
-def test_phi_a_resident_bit_exact(ares, out, rows):
+def test_phi_a_resident_bit_exact(ares, dyn, out, rows):
     """K5 with A-panel residency (RF_OPT_K5_ARES: each CTA keeps its A rows over the whole K = p in shared memory for
-    a segment of up to 16 column tiles; column-block-major segment schedule) computes every entry with the same
-    arithmetic as the default K5: bit-identical, in every layout and on a row block."""
+    a segment of up to 16 column tiles; column-block-major segment schedule, segments pulled from a device counter
+    (RF_OPT_K5_DYNAMIC = 1) or dealt round-robin (0)) computes every entry with the same arithmetic as the K5 without
+    residency: bit-identical, in every layout and on a row block."""
     n, p = 2100, 448                     # 7 K-blocks, ragged rows
     X = synthetic.make_X(4, n=n, p=p)
     Xd = dev(X, "bf16")
     ctx = rf.Context(0)
+    ctx.set_option("k5_dynamic", dyn)
     res = []
     for a in (ares, 0):
         ctx.set_option("k5_ares", a)
