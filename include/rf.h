@@ -137,7 +137,10 @@ void rf_ctx_destroy(rf_ctx* ctx);
 typedef enum {
   RF_OPT_K3_HYBRID = 0,    /* 1: K3 as 4-CTA multicast clusters + pair clusters on the leftover SMs (n ≥ 32 row
                               tiles); 0: pair clusters only                                          default 1 */
-  RF_OPT_K4_HYBRID = 1,    /* the same for K4 (n ≥ 64 row tiles)                                    default 1 */
+  RF_OPT_K4_HYBRID = 1,    /* the same for K4 (n ≥ 64 row tiles)                                    default 1
+                              Both hybrids' 4-CTA multicast kernels can hang when the GPU is time-sliced between
+                              PROCESSES (compute preemption): set both to 0 when processes share a GPU.
+                              One process per GPU never preempts them. */
   RF_OPT_K4_CL8 = 2,       /* 1: the K4 hybrid with 8-CTA clusters (2 × 2 pairs sharing A and B)     default 0 */
   RF_OPT_K4_SPLIT_R100 = 3,/* K4 hybrid work split: per-SM rate ratio multicast/pair × 100          default 111 */
   RF_OPT_K3_SPLIT_R100 = 4,/* K3 hybrid work split, as above                                        default 120 */
@@ -160,7 +163,9 @@ typedef enum {
                               staging), 3 with 12 epilogue warps                                      default 1 */
   RF_OPT_K5_DYNAMIC = 16,  /* 1: the A-resident K5 pulls its segments from a device counter (balanced last wave);
                               0: static round-robin                                                   default 1 */
-  RF_OPT_COUNT = 17
+  RF_OPT_G5_PIPE = 17,     /* peers: 1 = each chunk's owner-side sum on the context's reduce stream beside K4;
+                              0 = all sums after K4 on the caller's stream                             default 1 */
+  RF_OPT_COUNT = 18
 } rf_opt;
 rf_status rf_ctx_set_option(rf_ctx* ctx, rf_opt opt, int64_t value);
 rf_status rf_ctx_get_option(const rf_ctx* ctx, rf_opt opt, int64_t* value);

@@ -37,7 +37,7 @@ SYMBOLS = ("rf_last_error", "rf_version", "rf_device_supported", "rf_moments", "
 RF_PACK_TILE = 256
 RF_MAX_PEERS = 16
 OPT = {"k3_hybrid": 0, "k4_hybrid": 1, "k4_cl8": 2, "k4_split_r100": 3, "k3_split_r100": 4, "lock_w": 5, "lock_ks": 6,
-       "k5_wide": 7, "eq1_general": 8, "kchunk": 9, "max_sms": 10, "comm_sms": 11, "verbose": 12, "g5_phases": 13, "k4_dynamic": 14, "k5_ares": 15, "k5_dynamic": 16}
+       "k5_wide": 7, "eq1_general": 8, "kchunk": 9, "max_sms": 10, "comm_sms": 11, "verbose": 12, "g5_phases": 13, "k4_dynamic": 14, "k5_ares": 15, "k5_dynamic": 16, "g5_pipe": 17}
 
 
 class rf_moments_t(ctypes.Structure):

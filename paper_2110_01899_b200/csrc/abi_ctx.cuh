@@ -292,7 +292,9 @@ rf_status gram_collective(const void* X, int64_t ldx, const void* W, int64_t ldw
   const int R = c->world, me = c->rank;
   uint32_t* mine = flags_of(c->stage, R, c->recv_cap);
   const int phases = (int)opt(RF_OPT_G5_PHASES);
-  const bool piped = phases == 3;   // both halves in one call: the sum runs on the reduce stream beside K4
+  // both halves in one call: the sums run on the reduce stream beside K4 (RF_OPT_G5_PIPE = 0: after K4, on the
+  // caller's stream — the round-2 first cut, kept for A/B runs)
+  const bool piped = phases == 3 && opt(RF_OPT_G5_PIPE) != 0;
   uint32_t* dst[RF_MAX_PEERS];
   if (phases & 1) {
     const uint32_t epoch = ++c->epoch;
@@ -405,7 +407,7 @@ rf_status rf_ctx_set_option(rf_ctx* c, rf_opt o, int64_t v) {
     case RF_OPT_K5_WIDE: okv = v >= -1 && v <= 1; break;
     case RF_OPT_COMM_SMS: okv = v >= 0 && v <= 64; break;
     case RF_OPT_G5_PHASES: okv = v >= 1 && v <= 3; break;
-    case RF_OPT_K4_DYNAMIC: case RF_OPT_K5_DYNAMIC: okv = v == 0 || v == 1; break;
+    case RF_OPT_K4_DYNAMIC: case RF_OPT_K5_DYNAMIC: case RF_OPT_G5_PIPE: okv = v == 0 || v == 1; break;
     case RF_OPT_K5_ARES: okv = v >= 0 && v <= 3; break;
     default: break;
   }

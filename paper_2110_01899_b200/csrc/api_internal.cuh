@@ -278,7 +278,7 @@ bool make_tmap_out(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, 
 }
 
 // ---------------------------------------------------------------- context and options (include/rf.h)
-constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1, 1, 1};
+constexpr int64_t kOptDefault[RF_OPT_COUNT] = {1, 1, 0, 111, 120, 24, 8, -1, 0, 4, 0, 8, 0, 3, 1, 1, 1, 1};
 thread_local rf_ctx* g_ctx = nullptr;     // the context of the call in progress on this thread
 int64_t opt(rf_opt o) { return g_ctx ? g_ctx->opts[o] : kOptDefault[o]; }
 

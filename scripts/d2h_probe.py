@@ -60,3 +60,22 @@ t0 = time.perf_counter()
 dst.copy_(src, non_blocking=True)
 torch.cuda.synchronize()
 print(f"8 GiB D2H alone: {time.perf_counter() - t0:.3f} s", flush=True)
+
+# D2H rate measured on the copy stream itself (events), in 256-MB pieces, alone and under the SYRK
+def d2h_events(with_gram):
+    ce = (256 << 20) // 4
+    torch.cuda.synchronize()
+    if with_gram:
+        rf.rf_gram(X, W, act=cfg.act, out="packed_tri", G=G, ws=ws)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        a.record(cs)
+        for off in range(0, src.numel(), ce):
+            dst[off:off + ce].copy_(src[off:off + ce], non_blocking=True)
+        b.record(cs)
+    torch.cuda.synchronize()
+    return nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+
+
+for rep in range(2):
+    print(f"D2H 256-MB pieces, alone: {d2h_events(False):.1f} GB/s; under K3+K4: {d2h_events(True):.1f} GB/s", flush=True)
