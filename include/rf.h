@@ -435,7 +435,7 @@ int32_t rf_last_launch_count(void);
  * records taken (may exceed max_records; the excess is dropped) and clears the record list. */
 rf_status rf_profile_enable(int on);
 rf_status rf_profile_read(int32_t max_records, char* names, float* ms, int32_t* count);
-/* rf_profile_timeline: as rf_profile_read, plus start_ms[k] = the launch's start relative to the first record's
+/* rf_profile_timeline: as rf_profile_read, plus start_ms[k] = the launch's start relative to the earliest recorded
  * start (records on several streams — a collective's flag / sum kernels beside K4 — on one device time line). */
 rf_status rf_profile_timeline(int32_t max_records, char* names, float* start_ms, float* ms, int32_t* count);
 

@@ -292,7 +292,7 @@ def rf_profile_read(max_records: int = 4096):
 
 
 def rf_profile_timeline(max_records: int = 4096):
-    """[(kernel name, start ms relative to the first record, device ms)] of the launches recorded since the last
+    """[(kernel name, start ms relative to the earliest record, device ms)] of the launches recorded since the last
     read (waits for them)."""
     lib = load()
     names = ctypes.create_string_buffer(32 * max_records)

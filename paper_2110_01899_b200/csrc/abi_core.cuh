@@ -48,13 +48,19 @@ rf_status rf_profile_timeline(int32_t max_records, char* names, float* start_ms,
     if (k < max_records) {
       std::snprintf(names + 32 * k, 32, "%s", r.name);
       ms[k] = t;
-      if (start_ms) {
+      if (start_ms) {   // relative to the first record pushed; shifted to the earliest start below
         float t0 = 0.f;
         if (e == cudaSuccess && cudaEventElapsedTime(&t0, recs[0].a, r.a) != cudaSuccess) t0 = 0.f;
         start_ms[k] = t0;
       }
     }
     ++k;
+  }
+  if (start_ms && k > 0) {   // records are pushed when a launch scope closes, not in start order
+    const int32_t kk = std::min(k, max_records);
+    float mn = 0.f;
+    for (int32_t i = 0; i < kk; ++i) mn = std::min(mn, start_ms[i]);
+    for (int32_t i = 0; i < kk; ++i) start_ms[i] -= mn;
   }
   {
     std::lock_guard<std::mutex> lk(g_pmu);

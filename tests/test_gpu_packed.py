@@ -224,3 +224,47 @@ def test_collective_errors():
     ctx.destroy()
     with pytest.raises(rf.RFError):
         rf.Context(0).set_option("k5_wide", 7)
+
+
+def test_peers_pipelined_timeline():
+    """The pipelined call's launch timeline (rf_profile_timeline): one arrival-flag kernel and one owner-side sum per
+    G5 chunk (C = min(16, ⌈T/8⌉) chunks of 8-row-tile groups), each chunk's sum starting after its flag, and the
+    whole call's result equal to the dense K4."""
+    n, p, m = 16400, 64, 256                   # 65 row tiles: the K4 multicast + pair hybrid, 9 chunks
+    T = (n + 255) // 256
+    C = min(16, (T + 7) // 8)
+    rng = np.random.default_rng(3)
+    Xd = torch.tensor(rng.standard_normal((n, p)) / math.sqrt(p), device="cuda").to(torch.bfloat16)
+    Wd = torch.tensor(rng.standard_normal((m, p)), device="cuda").to(torch.bfloat16)
+    ctx = rf.Context(0)
+    ctx.attach_peers(0, 1, n)
+    recv = rf.rf_gram(Xd, Wd, act="tanh", out="packed_tiles", ctx=ctx)
+    torch.cuda.synchronize()
+    rf.rf_profile_read()
+    rf.rf_profile_enable(True)
+    rf.rf_gram(Xd, Wd, act="tanh", out="packed_tiles", G=recv, ctx=ctx)
+    torch.cuda.synchronize()
+    rf.rf_profile_enable(False)
+    tl = rf.rf_profile_timeline()
+    sig = [t0 for nm, t0, _ in tl if nm == "G5_signal_arrived"]
+    red = [t0 for nm, t0, _ in tl if nm == "G5_pack_reduce"]
+    k4 = [t0 for nm, t0, _ in tl if nm.startswith("K4_syrk_packed")]
+    assert len(sig) == C and len(red) == C and k4
+    assert all(np.isfinite(v) and v >= 0 for _, v, _ in tl)
+    for s_, r_ in zip(sorted(sig), sorted(red)):
+        assert r_ >= s_ - 1e-3, "a chunk's sum started before its arrival flag"
+    G = rf.rf_gram(Xd, Wd, act="tanh", out="upper", ctx=ctx)
+    torch.cuda.synchronize()
+    tiles = rf.rf_tile_map(n, 1, 0)
+    TE = collective.TILE_ELEMS
+    for k in list(range(0, len(tiles), max(1, len(tiles) // 40))) + [len(tiles) - 1]:   # sampled whole tiles
+        I, J = (int(v) for v in tiles[k])
+        if I < 0:
+            continue
+        i0, j0 = I * 256, J * 256
+        i1, j1 = min(i0 + 256, n), min(j0 + 256, n)
+        blk = recv[k * TE:(k + 1) * TE].view(256, 256)[: i1 - i0, : j1 - j0]
+        ref = G[i0:i1, j0:j1]
+        mask = torch.arange(j0, j1, device="cuda")[None, :] >= torch.arange(i0, i1, device="cuda")[:, None]
+        assert torch.equal(blk[mask], ref[mask]), f"tile ({I}, {J}) differs from the dense K4"
+    ctx.destroy()
