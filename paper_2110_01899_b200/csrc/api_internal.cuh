@@ -557,7 +557,7 @@ rf_status max_clusters(int sms, int* mcl) {
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(Cm::THREADS);
   cfg.dynamicSmemBytes = Cm::SMEM_BYTES;
-  cfg.gridDim = dim3(sms);
+  cfg.gridDim = dim3((sms / Cm::CL) * Cm::CL);   // a whole number of clusters (148 is not a multiple of 8)
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = Cm::CL;

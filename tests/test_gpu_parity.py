@@ -378,7 +378,14 @@ def test_k4_hybrid_bit_exact(cl8, dyn, out):
     ctx = rf.Context(0)
     ctx.set_option("k4_cl8", int(cl8))
     ctx.set_option("k4_dynamic", dyn)      # 1: both kernels pull units from one device counter; 0: static split
+    torch.cuda.synchronize()
+    rf.rf_profile_read()
+    rf.rf_profile_enable(True)
     G1 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out=out, ctx=ctx)
+    torch.cuda.synchronize()
+    rf.rf_profile_enable(False)
+    names = {nm for nm, _ in rf.rf_profile_read()}
+    assert "K4_syrk_mc" in names and "K4_syrk_tail" in names, f"the hybrid did not run: {sorted(names)}"
     ctx.set_option("k4_hybrid", 0)
     G0 = rf.rf_gram(Xd, Wd, act="tanh", prec="bf16", out="upper" if out == "packed_tri" else out, ctx=ctx)
     torch.cuda.synchronize()
