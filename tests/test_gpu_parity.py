@@ -351,8 +351,13 @@ def test_k3_multicast_hybrid_bit_exact(act, prec):
     ctx = rf.Context(0)
     for mc in (1, 0):
         ctx.set_option("k3_hybrid", mc)
+        rf.rf_profile_read()
+        rf.rf_profile_enable(True)
         G = rf.rf_gram(Xd, Wd, act=act, prec=prec, out="upper", ctx=ctx)
         torch.cuda.synchronize()
+        rf.rf_profile_enable(False)
+        names = {nm for nm, _ in rf.rf_profile_read()}
+        assert ("K3_gemm_sigma_mc" in names) == bool(mc), f"k3_hybrid={mc}: {sorted(names)}"
         res.append(G)
     assert torch.equal(res[0], res[1])
     S = synthetic.sample_indices(n, count=256, tile_stride=512)
