@@ -165,8 +165,13 @@ def test_gram_ter_k3_multicast_hybrid_bit_exact():
     ctx = rf.Context(0)
     for mc in (1, 0):
         ctx.set_option("k3_hybrid", mc)
+        rf.rf_profile_read()
+        rf.rf_profile_enable(True)
         G = rf.rf_gram_ter(Xd, Td, eps, sm, sp, out="upper", ctx=ctx)
         torch.cuda.synchronize()
+        rf.rf_profile_enable(False)
+        names = {nm for nm, _ in rf.rf_profile_read()}
+        assert ("K3_ter_features_mc" in names) == bool(mc), f"k3_hybrid={mc}: {sorted(names)}"
         res.append(G)
     assert torch.equal(res[0], res[1])
     assert float(res[0].diagonal().min()) > 0.0
