@@ -175,3 +175,24 @@ def test_gram_ter_k3_multicast_hybrid_bit_exact():
         res.append(G)
     assert torch.equal(res[0], res[1])
     assert float(res[0].diagonal().min()) > 0.0
+
+
+def test_gram_ter_k4_hybrid_bit_exact():
+    """At n ≥ 64 row tiles K4^ter (the exact fp8 SYRK) runs as the multicast + pair hybrid with the unit queue; G^ter
+    equals the pair kernel's bit for bit (integer sums, exact in fp32 either way), and the hybrid did run."""
+    n, p, m, eps = 16384 + 77, 64, 512, 0.9
+    Xd, Td, Xb, T = _inputs(n, p, m, eps, cfg=1)
+    sm, sp = rf.rf_trf_thresholds_for("tanh", 1.0)
+    res = []
+    ctx = rf.Context(0)
+    for hyb in (1, 0):
+        ctx.set_option("k4_hybrid", hyb)
+        rf.rf_profile_read()
+        rf.rf_profile_enable(True)
+        G = rf.rf_gram_ter(Xd, Td, eps, sm, sp, out="upper", ctx=ctx)
+        torch.cuda.synchronize()
+        rf.rf_profile_enable(False)
+        names = {nm for nm, _ in rf.rf_profile_read()}
+        assert ("K4_ter_syrk_mc" in names) == bool(hyb), f"k4_hybrid={hyb}: {sorted(names)}"
+        res.append(G)
+    assert torch.equal(res[0], res[1])
