@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-phi", action="store_true")
     ap.add_argument("--no-trf", action="store_true", help="skip the NEXT-1 ternary G^ter measurement")
     ap.add_argument("--no-phi4", action="store_true", help="skip the configs[4] Φ-only measurement")
+    ap.add_argument("--phi4-n", type=int, default=0,
+                    help="testing only: run the configs[4] Φ leg with this n (also on --same-gpu, where the full n "
+                         "would not fit N dense Φ buffers on one GPU)")
     ap.add_argument("--g5", default="peers", choices=["peers", "nccl"],
                     help="N>1: G5 as the peer-memory exchange in K4's epilogue (default) or chunked NCCL reduce-scatter")
     ap.add_argument("--same-gpu", action="store_true",
@@ -632,17 +635,21 @@ def main():
     # ---------------- configs[4] (closed-form Φ only, p = 512, n = 131072): the HBM-write-heavy Φ pass the north star
     # reports in GB/s; rows split over ranks by equal triangle area, no collective.  Reported beside the headline.
     phi4_line = None
-    if world == 1 and args.config == 3 and not args.no_phi4:
+    # at N > 1 every rank runs its row block (rf_phi_row_split) and the time is the max over ranks (not on --same-gpu:
+    # N dense 68.7-GB Φ buffers on one GPU)
+    if (args.config == 3 or args.phi4_n > 0) and not args.no_phi4 and (not args.same_gpu or args.phi4_n > 0):
         if do_phi:
             del Phi, ws_p
-        if do_gram:
+        if do_gram and world == 1:   # (N > 1: the collective's receive buffer is G_own)
             del G, ws_g
         torch.cuda.empty_cache()
         c4 = synthetic.CONFIGS[4]
-        n4, p4 = c4.n, c4.p
-        X4f = torch.from_numpy(synthetic.make_X(c4)).to(torch.float32).to(device)
+        n4, p4 = (args.phi4_n or c4.n), c4.p
+        X4f = torch.from_numpy(synthetic.make_X(c4, n=n4) if args.phi4_n else synthetic.make_X(c4)).to(torch.float32)
+        X4f = X4f.to(device)
         Phi4 = torch.empty((n4, n4), dtype=torch.float32, device=device)
         tri4 = n4 * (n4 + 1) / 2.0
+        rb4, re4 = rf.rf_phi_row_split(n4, world, rank)
 
         def phi4_mode(mode, steps):
             """Time rf_phi_closed_form at configs[4] in one precision mode (bf16-stored X is
@@ -651,26 +658,31 @@ def main():
             ws4 = torch.empty(rf.rf_phi_workspace_size(p4, n4, mode), dtype=torch.uint8, device=device)
             tau4 = rf.rf_estimate_tau(X4)
             mom4 = rf.rf_moments(c4.act, tau4)
+            def phi4_call():
+                rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec=mode, row_begin=rb4, row_end=re4,
+                                      Phi=Phi4, ws=ws4)
             for _ in range(args.warmup):
-                rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec=mode, Phi=Phi4, ws=ws4)
+                phi4_call()
             torch.cuda.synchronize()
+            barrier()
             rf.rf_profile_read()
             rf.rf_profile_enable(True)
             pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             pa.record(stream)
             for _ in range(steps):
-                rf.rf_phi_closed_form(X4, act=c4.act, tau=tau4, mom=mom4, prec=mode, Phi=Phi4, ws=ws4)
+                phi4_call()
             pb.record(stream)
             torch.cuda.synchronize()
+            barrier()
             rf.rf_profile_enable(False)
             ks = [t for nm, t in rf.rf_profile_read() if nm.startswith("K5")]
-            k5ms = sum(ks) / max(1, len(ks))
-            pms = pa.elapsed_time(pb) / steps
+            k5ms = max_over_ranks(sum(ks) / max(1, len(ks)))
+            pms = max_over_ranks(pa.elapsed_time(pb)) / steps
             by4 = 4.0 * tri4 + X4.numel() * X4.element_size() + 4.0 * n4    # Φ triangle + X + row norms
             d = {"ms_per_step": pms, "entries_per_s": tri4 / (pms * 1e-3),
                  "tflops": p4 * n4 * (n4 + 1.0) / (pms * 1e-3) / 1e12,
                  "K5_ms": k5ms, "K5_hbm_gbs": by4 / (k5ms * 1e-3) / 1e9 if k5ms else None,
-                 "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / pk["hbm_gbs"] if k5ms else None,
+                 "K5_frac_hbm": by4 / (k5ms * 1e-3) / 1e9 / (pk["hbm_gbs"] * world) if k5ms else None,
                  "K5_tflops": p4 * n4 * (n4 + 1.0) / (k5ms * 1e-3) / 1e12 if k5ms else None}
             if k5ms:
                 # K5's two roofline floors (DESIGN.md §7 "K5's roofline"): the 2p-flop upper-triangle contraction on
@@ -678,8 +690,8 @@ def main():
                 # copy rate; at p = 512 the intensity 2p / 4 B = 256 flop/B is above the ridge, so the tensor floor
                 # binds.  frac_roofline = max(floors) / K5 time.
                 ptc = pk["bf16_tflops_sustained"] * (1.0 if mode == "bf16" else 0.5) / (3.0 if mode == "3xtf32" else 1.0)
-                t_tc = p4 * n4 * (n4 + 1.0) / (ptc * 1e12) * 1e3
-                t_hbm = by4 / (pk["hbm_gbs"] * 1e9) * 1e3
+                t_tc = p4 * n4 * (n4 + 1.0) / (ptc * 1e12) * 1e3 / world     # each rank: 1/world of the triangle
+                t_hbm = by4 / (pk["hbm_gbs"] * 1e9) * 1e3 / world
                 d.update({"K5_floor_tensor_ms": t_tc, "K5_floor_hbm_ms": t_hbm,
                           "K5_bound": "tensor" if t_tc >= t_hbm else "hbm",
                           "K5_frac_tensor_sustained": t_tc / k5ms,
@@ -688,9 +700,13 @@ def main():
             return d
 
         phi4_line = {"what": f"configs[4] {c4.name}: Φ by EQ1, fp32 upper triangle; headline = bf16-stored X "
-                             "(bf16 products exact in fp32)", **phi4_mode("bf16", args.steps)}
-        phi4_line["tf32"] = phi4_mode("tf32", max(2, args.steps // 2))
-        phi4_line["3xtf32"] = phi4_mode("3xtf32", max(2, args.steps // 2))
+                             "(bf16 products exact in fp32)"
+                             + (f"; {world} ranks, row blocks of equal triangle area, no collective, max over ranks; "
+                                "K5 roofline floors are whole-job figures divided by the ranks" if world > 1 else ""),
+                     **phi4_mode("bf16", args.steps)}
+        if world == 1:
+            phi4_line["tf32"] = phi4_mode("tf32", max(2, args.steps // 2))
+            phi4_line["3xtf32"] = phi4_mode("3xtf32", max(2, args.steps // 2))
         del Phi4, X4f
         torch.cuda.empty_cache()
 
