@@ -5,6 +5,8 @@ sys.path.insert(0, os.getcwd())
 import paper_2110_01899_b200 as rf, synthetic
 cfg = synthetic.CONFIGS[4]; n, p = cfg.n, cfg.p
 X = torch.from_numpy(synthetic.make_X(cfg)).to(torch.bfloat16).cuda()
+if "--roll" in sys.argv:   # move the data: row i gets sample (i + 40000) mod n (is the slow rank about data or position?)
+    X = torch.roll(X, shifts=-40000, dims=0).contiguous()
 PhiA = torch.empty((n, n), device="cuda")
 PhiB = torch.empty((n, n + 32), device="cuda")[:, :n]   # odd number of 128-B lines per row
 ws = torch.empty(rf.rf_phi_workspace_size(p, n, "bf16"), dtype=torch.uint8, device="cuda")
