@@ -103,7 +103,7 @@ def test_bench_two_ranks_on_one_gpu():
     test_gpu_packed.py (one process, no time-slicing)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", "1", "--prec", "tf32", "--same-gpu", "--no-trf",
+           "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", "1", "--prec", "tf32", "--same-gpu",
            "--phi4-n", "8192", "--no-cpu-baseline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-3000:], r.stderr[-3000:])
@@ -113,5 +113,6 @@ def test_bench_two_ranks_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert "G5_pack_reduce" in d["kernels"]
+    assert d["trf"]["ms_per_step"] > 0                 # the NEXT-1 leg's N > 1 branch
     # the configs[4]-shaped Φ leg in its N > 1 form (row blocks, max over ranks), at a reduced n
     assert d["phi_configs4"]["K5_ms"] > 0 and d["phi_configs4"]["entries_per_s"] > 0
