@@ -357,6 +357,9 @@ struct CtxScope {
   if (ctx_scope_.status) return ctx_scope_.status
 
 // Row tiles per L2 raster group (tc_gemm.cuh Sched) of kernel K3, K4, K5 (measured best).
+#ifndef K4_DYN_GM
+#define K4_DYN_GM 4   // super rows (512) per raster group of the K4 unit queue (A/B builds: -DK4_DYN_GM=k)
+#endif
 int raster_gm(int def, int kernel = 0) {
   (void)kernel;
   return def;
@@ -648,7 +651,7 @@ rf_status launch_k4_hybrid_cl(const char* name, const CUtensorMap& tS, const CUt
     // whole triangle from a shared counter (prog[256]); the multicast cluster computes a unit with its two pairs,
     // a pair cluster as two 256 × 512 tiles.  The pair kernel's SMs follow the raster front (L2 reuse) and both
     // kernels end together whatever their per-SM rates on this box.
-    sm = rfk::Sched::make(1, 256, 0, T2, T2, kb, 0, raster_gm(4, 4));
+    sm = rfk::Sched::make(1, 256, 0, T2, T2, kb, 0, raster_gm(K4_DYN_GM, 4));
     sp = sm;
     sm.queue = sp.queue = prog + 256;
     sp.nsub = 2;
