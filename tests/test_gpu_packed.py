@@ -146,9 +146,12 @@ def _dense_vs_packed(ctx, n, p, m, prec, act, calls=2):
     assert np.array_equal(got[I, J], G.cpu().numpy()[I, J]), "packed tiles must equal the dense K4 bit for bit"
 
 
-@pytest.mark.parametrize("prec", ["bf16", "tf32"])
-def test_peers_world1_equals_dense(prec):
+@pytest.mark.parametrize("prec,pipe", [("bf16", 1), ("tf32", 1), ("bf16", 0)])
+def test_peers_world1_equals_dense(prec, pipe):
+    """World-1 peers: the packed tiles equal the dense K4 bit for bit, with the per-chunk sums beside K4 (pipe 1, the
+    default) or after it on the caller's stream (RF_OPT_G5_PIPE = 0)."""
     ctx = rf.Context(0)
+    ctx.set_option("g5_pipe", pipe)
     ctx.attach_peers(0, 1, 1500)
     assert ctx.collective() == (0, 1, 2)
     _dense_vs_packed(ctx, 1500, 128, 1024, prec, "tanh", calls=3)
