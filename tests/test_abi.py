@@ -22,6 +22,15 @@ def _declared_symbols():
     return sorted(set(re.findall(r"\b(rf_[a-z0-9_]+)\s*\(", src)))
 
 
+def test_option_table_matches_header():
+    """The binding's context-option names (argument marshalling only) are include/rf.h's rf_opt enum, value for value."""
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "rf.h")).read(), flags=re.S)
+    enum = {k: int(v) for k, v in re.findall(r"\bRF_OPT_([A-Z0-9_]+)\s*=\s*(\d+)", src)}
+    count = enum.pop("COUNT")
+    assert sorted(enum.values()) == list(range(count))
+    assert {k.lower(): v for k, v in enum.items()} == _lib.OPT
+
+
 def test_library_exports_every_declared_symbol():
     lib = rf.load()
     declared = _declared_symbols()
