@@ -92,3 +92,45 @@ def test_theorem1_erf_converges(act):
         Kt = C.ktilde(X, V, A, mo["d0"], mo["d1"], mo["d2"])
         errs.append(_rel2(K, Kt))
     assert errs[1] < 0.03 and errs[1] < 0.75 * errs[0], errs
+
+
+def _offdiag_block_contrast(D, lab):
+    """m_11 − m_12 − m_21 + m_22 of the block means of D over i ≠ j.  Row- or column-additive terms (so also the
+    centering by P, and everything ‖x_i‖²‖x_j‖² contributes beyond α_iα_j) cancel in it exactly."""
+    D = D.copy()
+    np.fill_diagonal(D, 0.0)
+    m = np.zeros((2, 2))
+    for a in range(2):
+        for b in range(2):
+            ia, ib = np.where(lab == a)[0], np.where(lab == b)[0]
+            cnt = len(ia) * len(ib) - (len(ia) if a == b else 0)
+            m[a, b] = D[np.ix_(ia, ib)].sum() / cnt
+    return m[0, 0] - m[0, 1] - m[1, 0] + m[1, 1]
+
+
+def test_theorem1_2T_block_is_pinned_by_the_class_contrast():
+    """Sharp pin of the 2T block of A (Theorem 1).  For σ = t² the exact kernel is ‖x‖²‖y‖² + 2(xᵀy)², and
+    for i ≠ j in classes a, b: E[2(x_iᵀx_j)²] = 2·tr(C_aC_b)/p² + (terms additive in a and b) — Isserlis.  So the
+    double class contrast of (exact kernel − K̃ built with T = 0) must equal that of the (J/√p)(2T)(J/√p)ᵀ block,
+    (2/p)(T_11 − 2T_12 + T_22), up to the law-of-large-numbers noise of ≈ n²/4 entries per block (≈ 1 %).  A wrong
+    factor (T instead of 2T), a wrong T (tr C_a·tr C_b/p²) or a dropped block misses by 50 %, 80 % or 100 %."""
+    n, p = 2048, 1024
+    X, J, phi, t, T, tau = _gmm(n, p, seed=7)
+    lab = (J[:, 1] > 0).astype(int)
+    K = C.center(C.quadratic_kernel(X))
+    d0 = 2 * tau ** 2
+
+    def kt(TT):
+        V, A = C.gmm_V_A(J, phi, t, TT, p)
+        return C.ktilde(X, V, A, d0, 0.0, 1.0)
+
+    K0 = kt(0 * T)
+    want = _offdiag_block_contrast(K - K0, lab)                      # what the data say the block must supply
+    theory = 2.0 / p * (T[0, 0] - 2 * T[0, 1] + T[1, 1])             # (2/p)(1 − 3 + 3.25) = 2.5/p here
+    assert abs(want / theory - 1) < 0.05, (want, theory)
+    got = _offdiag_block_contrast(kt(T) - K0, lab)                   # what the oracle's K̃ supplies
+    assert abs(got / want - 1) < 0.05, (got, want)
+    assert abs(got / theory - 1) < 1e-9                              # and it is exactly the 2T block
+    outer = np.outer([1.0, T[0, 1]], [1.0, T[0, 1]])
+    for TT in (0.5 * T, outer):
+        assert abs(_offdiag_block_contrast(kt(TT) - K0, lab) / want - 1) > 0.4
