@@ -69,7 +69,8 @@ def test_theorem1_quadratic_sigma_converges():
 
 def test_theorem1_T_term_is_the_best_fit():
     """The 2T block of A is a small effect at these sizes; among T, T/2 and the isotropic guess tr(C_a)tr(C_b)/p²,
-    the theorem's T fits the exact kernel best (weak pin, stated as such in DESIGN.md)."""
+    the theorem's T fits the exact kernel best (a weak pin on its own; the sharp pin of the 2T block is the class
+    contrast in test_theorem1_2T_block_is_pinned_by_the_class_contrast)."""
     n, p = 2048, 1024
     X, J, phi, t, T, tau = _gmm(n, p, seed=5)
     K = C.center(C.quadratic_kernel(X))
