@@ -331,3 +331,19 @@ def test_param_act_registration():
     assert lib.rf_act_quadratic(0.0, float("inf"), 0.0, ctypes.byref(v)) == _lib.RF_E_INVALID
     m = ctypes.c_int()
     assert lib.rf_moments(200, 1.0, 0, None) == _lib.RF_E_INVALID      # an id never registered
+
+
+def test_dram_traffic_record_matches_the_current_sources():
+    """bench.py reports `roofline.traffic` only from an ncu record keyed by the hash of csrc/* and include/rf.h
+    (never stale bytes).  The committed record must be the one of the sources as they stand —
+    after a kernel change, re-run scripts/ncu_traffic.py on a B200 (or the bench line carries traffic = null)."""
+    import json
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    with open(os.path.join(root, "profiles", "ncu_traffic.json")) as f:
+        rec = json.load(f)
+    h = bench.source_hash()
+    assert h in rec, f"no ncu DRAM-traffic record for the current library sources ({h})"
+    assert rec[h].get("configs[3]:bf16:w1:K4_syrk", 0) > 17.2e9      # at least K4's compulsory bytes
